@@ -1,0 +1,163 @@
+/*
+ * sun_b200.h — C ABI of the B200-native SUN shared decode path.
+ *
+ * The reference (arxiv 2603.02599 "SUN", code: poolsim) has no FFI: its decode
+ * step is the analytic price `decode_step_time[_from_totals]`
+ * (/root/reference/pkg/src/poolsim/costmodel.py:101-140) called once per step
+ * from the decode worker (engine.py:427-429), and the KV hand-off is the
+ * `KvHandle` value object (domain.py:96-113). This library is the real thing
+ * behind those two extension points: the decode module's step on one B200, and
+ * the paged KV pool the hand-off writes into. The Python mirror of the reference
+ * API (paper_2603_02599_b200/) binds these symbols with ctypes; see
+ * INTEGRATION.md for the binding a poolsim maintainer would add.
+ *
+ * Conventions
+ *  - plain pointers and sizes only; every device buffer is caller-owned
+ *    (torch allocates), the library never allocates on the step path;
+ *  - calls are asynchronous on the given stream (`void*` = cudaStream_t) and
+ *    graph-capturable; a decoder's workspace is not re-entrant — one decoder
+ *    per decode worker / GPU, as each poolsim decode worker owns one GPU;
+ *  - status codes map 1:1 onto the reference's exceptions (see SunStatus).
+ */
+#ifndef SUN_B200_H
+#define SUN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SUN_ABI_VERSION 1
+
+typedef enum SunStatus {
+  SUN_OK = 0,
+  SUN_ERR_VALUE = 1,         /* ValueError: empty batch (costmodel.py:130-131), bad sizes   */
+  SUN_ERR_MIXED_DECODER = 2, /* MixedDecoderError: decoder geometry mismatch (costmodel.py:132-138,
+                                shared-decoder invariant domain.py:266-279)                    */
+  SUN_ERR_UNSUPPORTED = 3,   /* shape outside what the sm_100a kernels implement               */
+  SUN_ERR_CUDA = 4,          /* CUDA runtime / driver failure (message via sun_last_error)      */
+  SUN_ERR_CAPACITY = 5       /* workspace or KV pool too small (engine.py:394-401 OVER_CAPACITY) */
+} SunStatus;
+
+/* Geometry of the frozen shared decode module θ_d (Eq. 3). Every
+ * task-specific prefill module θ_p^τ that feeds this decoder must produce KV
+ * with the same (n_layers, n_kv_heads, head_dim, RoPE) — the analogue of the
+ * reference's "shared_decoder models agree on decode bits and param_count". */
+typedef struct SunDecoderDims {
+  int32_t vocab;
+  int32_t hidden;
+  int32_t n_layers;
+  int32_t n_q_heads;
+  int32_t n_kv_heads;
+  int32_t head_dim;    /* 64 or 128 */
+  int32_t ffn;         /* SwiGLU width f */
+  int32_t page_size;   /* tokens per KV page; 16 */
+  int32_t max_context; /* tokens per sequence upper bound (rope table rows) */
+  int32_t weight_bits; /* 16 = bf16; 4 = QSUN W4A16 (int4 symmetric, bf16 scale per group) */
+  int32_t group_size;  /* 128 when weight_bits == 4 */
+  int32_t qkv_bias;    /* 1 if the QKV projection has a bias (Qwen2.5) */
+  float rms_eps;
+} SunDecoderDims;
+
+/* Device pointers of one decoder layer (bf16 unless stated).
+ *  w_qkv      [(nq + 2 nkv) * d][hidden]           rows: q heads, k heads, v heads
+ *  w_o        [hidden][nq * d]
+ *  w_gate_up  [ceil(f/64) * 128][hidden]           64-row blocks: gate rows j..j+63 then
+ *                                                  up rows j..j+63 (zero rows pad f)
+ *  w_down     [hidden][f]
+ * For weight_bits == 4, w_* hold packed int4 (two per byte, low nibble = even k,
+ * row-major [rows][K/2]) and s_* the bf16 scales [rows][K/group]. */
+typedef struct SunLayerWeights {
+  const void* attn_norm;
+  const void* w_qkv;
+  const void* s_qkv;
+  const void* b_qkv;
+  const void* w_o;
+  const void* s_o;
+  const void* ffn_norm;
+  const void* w_gate_up;
+  const void* s_gate_up;
+  const void* w_down;
+  const void* s_down;
+} SunLayerWeights;
+
+typedef struct SunWeights {
+  const void* embed;       /* [vocab][hidden] */
+  const void* final_norm;  /* [hidden] */
+  const void* lm_head;     /* [vocab][hidden], bf16 always */
+  const float* rope_cos;   /* [max_context][head_dim/2] fp32 */
+  const float* rope_sin;
+  const SunLayerWeights* layers; /* host array, n_layers entries */
+} SunWeights;
+
+/* Paged KV pool shared by every prefill module (decoder-compatible by
+ * construction). Page p holds page_size consecutive tokens of
+ * one sequence for all layers: [n_layers][2 (K,V)][n_kv_heads][page_size][head_dim]
+ * bf16; K is stored after RoPE. A sequence's pages are listed in its block-table
+ * row (the physical form of KvHandle, domain.py:96-113). */
+typedef struct SunKvPool {
+  void* base;
+  int64_t num_pages;
+} SunKvPool;
+
+typedef struct SunDecoder SunDecoder;
+
+int32_t sun_abi_version(void);
+const char* sun_last_error(void);
+
+/* Bytes of device workspace a decoder needs for batches up to max_batch. */
+SunStatus sun_decoder_workspace_bytes(const SunDecoderDims* dims, int32_t max_batch, size_t* bytes);
+
+/* Build a decoder over caller-owned weights, KV pool and (zeroed) workspace.
+ * Encodes every TMA descriptor once. Replaces poolsim's per-worker
+ * `_DecodeWorker(weight_bytes, capacity)` (engine.py:148-212). */
+SunStatus sun_decoder_create(const SunDecoderDims* dims, const SunWeights* weights, const SunKvPool* kv,
+                             void* workspace, size_t workspace_bytes, int32_t max_batch, int32_t use_pdl,
+                             SunDecoder** out);
+SunStatus sun_decoder_destroy(SunDecoder* dec);
+
+/* One decode step of the shared decode module D_θd (Eq. 3) over a
+ * mixed-model batch: for each member b, consume tokens[b] at position
+ * positions[b] (= resident KV tokens before the step), append its K/V into the
+ * page block_tables[b*bt_stride + positions[b]/page_size], attend over
+ * positions[b]+1 tokens, and write next_tokens[b] = argmax logits (greedy).
+ * logits (fp32 [batch][vocab]) may be NULL (an internal buffer is used).
+ * pages_per_split: attention split-K granularity in pages (0 = automatic).
+ * This is the operator that replaces costmodel.decode_step_time_from_totals
+ * at engine.py:427-429. Errors: batch < 1 -> SUN_ERR_VALUE. */
+SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t* positions,
+                          const int32_t* block_tables, int32_t bt_stride, int32_t batch,
+                          int32_t pages_per_split, float* logits, int32_t* next_tokens, void* stream);
+
+/* ---- kernel-level entry points (unit parity tests; same kernels as the step) ---- */
+
+/* out[b][n] (=|+=) sum_k w[n][k] * x[b][k] for b < batch, bf16 in, fp32 out,
+ * tcgen05 swap-AB GEMM. x has x_rows >= round_up(batch,16) allocated rows of
+ * stride ldx elements. workspace >= sun_gemm_workspace_bytes(...), zeroed once. */
+SunStatus sun_gemm_workspace_bytes(int64_t n_out, int64_t k, int32_t batch, size_t* bytes);
+SunStatus sun_gemm_bf16(const void* w, int64_t n_out, int64_t k, const void* x, int64_t ldx, int64_t x_rows,
+                        int32_t batch, float* out, int64_t ldo, int32_t accumulate, void* workspace,
+                        size_t workspace_bytes, void* stream);
+
+/* Paged split-K decode attention for one layer: q bf16 [batch][nq][d] (post-RoPE),
+ * KV from the pool, out bf16 [batch][nq*d]. */
+SunStatus sun_attention_decode(const SunDecoderDims* dims, const SunKvPool* kv, int32_t layer, const void* q,
+                               const int32_t* positions, const int32_t* block_tables, int32_t bt_stride,
+                               int32_t batch, int32_t pages_per_split, void* out, void* workspace,
+                               size_t workspace_bytes, void* stream);
+
+/* y[b] = bf16(x[b] * rsqrt(mean(x[b]^2) + eps) * w), x fp32 [batch][h]. */
+SunStatus sun_rmsnorm(const float* x, const void* w, void* y, int32_t batch, int32_t h, float eps, void* stream);
+
+/* QSUN: quantize bf16 W[rows][K] to packed int4 + bf16 scales (group along K),
+ * symmetric, q = clamp(round_half_even(w / s), -8, 7), s = bf16(amax / 7). */
+SunStatus sun_quantize_w4(const void* w, int64_t rows, int64_t k, int32_t group, void* packed, void* scales,
+                          void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SUN_B200_H */

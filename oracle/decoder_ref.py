@@ -1,0 +1,186 @@
+"""ORACLE — test infrastructure only. CPU fp32 restatement of the SUN decoder.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+arm may import this module, and only as the checker or the timed CPU baseline,
+never as a product code path.
+
+What it restates
+----------------
+The reference (poolsim) has no decoder arithmetic: the decode step exists only
+as the price ``D + (W + sum KV)/(mbu*BW)`` (pkg/src/poolsim/costmodel.py:101-113)
+and the prefill/decode split only as per-phase weight bits
+(pkg/src/poolsim/domain.py:116-133). The math is defined by the paper:
+
+* PAPER.md:165-168 (Eq. 2): prefill module P_θp(X) -> (p(y1|X), C_X);
+* PAPER.md:166-172 (Eq. 3): decode module D_θd(y_{t-1}, C_{<t-1}) -> (p(y_t|...), C_t);
+* PAPER.md:176-184 (Eq. 4): C_{<=t} = C_X || C_{y<=t} — the decode module appends to
+  the cache the task-specific prefill module produced;
+* θ_d frozen and shared, θ_p^τ per task;
+* QSUN = W4 symmetric group-128 weight-only, lm_head full precision
+  (see quant_ref.py).
+
+The block is a standard Llama-3 / Qwen2.5 decoder layer (pre-RMSNorm, GQA with
+NeoX-style RoPE on q and k, SwiGLU MLP, optional QKV bias, untied or tied lm_head).
+
+Parity status: **parity unpinned** for logits / greedy tokens / QSUN numerics —
+no reference code computes them and the paper's stack (vLLM, LLM Compressor AWQ)
+is neither vendored nor pinned. The rounding points below are the
+ones the B200 path uses, so the comparison isolates accumulation-order effects:
+
+  resid fp32;  xn = bf16(resid * rsqrt(mean(resid^2)+eps) * g)
+  q,k = bf16(rope(xn @ Wqkv^T + b)),  v = bf16(...)          (K cached post-RoPE)
+  attn = bf16(softmax(q k^T / sqrt(d)) v)                     (fp32 softmax)
+  resid += attn @ Wo^T;  act = bf16(silu(g) * u);  resid += act @ Wdown^T
+  logits = fp32(bf16(rmsnorm(resid)) @ lm_head^T);  next = argmax (lowest index on ties)
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+BF16 = torch.bfloat16
+
+
+@dataclass(frozen=True)
+class OracleSpec:
+    vocab: int
+    hidden: int
+    n_layers: int
+    n_q_heads: int
+    n_kv_heads: int
+    head_dim: int
+    ffn: int
+    rope_theta: float
+    rms_eps: float
+    qkv_bias: bool = False
+
+
+def bf(x: torch.Tensor) -> torch.Tensor:
+    """Round fp32 -> bf16 -> fp32 (round-to-nearest-even), the GPU's storage rounding."""
+    return x.to(BF16).float()
+
+
+def rope_tables(max_pos: int, head_dim: int, theta: float) -> tuple[torch.Tensor, torch.Tensor]:
+    """cos/sin [max_pos, head_dim/2] fp32 of angle pos * theta^(-2i/d), computed in float64."""
+    half = head_dim // 2
+    inv = theta ** (-(torch.arange(half, dtype=torch.float64) * 2.0) / head_dim)
+    ang = torch.arange(max_pos, dtype=torch.float64)[:, None] * inv[None, :]
+    return torch.cos(ang).float(), torch.sin(ang).float()
+
+
+def rmsnorm(x: torch.Tensor, g: torch.Tensor, eps: float) -> torch.Tensor:
+    r = torch.rsqrt((x * x).mean(-1, keepdim=True) + eps)
+    return bf(x * r * g.float())
+
+
+def rope(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor:
+    """x [..., d] fp32, cos/sin [..., d/2] broadcastable; NeoX rotate-half."""
+    half = x.shape[-1] // 2
+    x1, x2 = x[..., :half], x[..., half:]
+    return torch.cat([x1 * cos - x2 * sin, x2 * cos + x1 * sin], dim=-1)
+
+
+def argmax_lowest(logits: torch.Tensor) -> torch.Tensor:
+    m = logits.max(dim=-1, keepdim=True).values
+    idx = torch.arange(logits.shape[-1]).expand_as(logits)
+    return torch.where(logits == m, idx, torch.full_like(idx, logits.shape[-1])).min(dim=-1).values
+
+
+class OracleDecoder:
+    """Weights: dict of CPU bf16 tensors in the standard (HF-like) layout:
+    embed [V,h], final_norm [h], lm_head [V,h], and per layer l:
+    attn_norm, wq [nq*d,h], wk [nkv*d,h], wv [nkv*d,h], (bq, bk, bv), wo [h,nq*d],
+    ffn_norm, wg [f,h], wu [f,h], wd [h,f].
+    """
+
+    def __init__(self, spec: OracleSpec, weights: dict, max_pos: int):
+        self.s = spec
+        self.w = {k: (v.float() if torch.is_tensor(v) else v) for k, v in weights.items()}
+        self.cos, self.sin = rope_tables(max_pos, spec.head_dim, spec.rope_theta)
+
+    # -- one layer over T new positions of one sequence ------------------------------
+    def _layer(self, l: int, resid: torch.Tensor, pos: torch.Tensor, kcache: list, vcache: list):
+        s, w = self.s, self.w
+        d, nq, nkv = s.head_dim, s.n_q_heads, s.n_kv_heads
+        T = resid.shape[0]
+        xn = rmsnorm(resid, w[f"l{l}.attn_norm"], s.rms_eps)
+        q = xn @ w[f"l{l}.wq"].t()
+        k = xn @ w[f"l{l}.wk"].t()
+        v = xn @ w[f"l{l}.wv"].t()
+        if s.qkv_bias:
+            q = q + w[f"l{l}.bq"]
+            k = k + w[f"l{l}.bk"]
+            v = v + w[f"l{l}.bv"]
+        cs, sn = self.cos[pos][:, None, :], self.sin[pos][:, None, :]
+        q = bf(rope(q.view(T, nq, d), cs, sn))
+        k = bf(rope(k.view(T, nkv, d), cs, sn))
+        v = bf(v.view(T, nkv, d))
+        K = torch.cat([kcache[l], k], 0) if kcache[l] is not None else k
+        V = torch.cat([vcache[l], v], 0) if vcache[l] is not None else v
+        kcache[l], vcache[l] = K, V
+        G = nq // nkv
+        n_past = K.shape[0] - T
+        out = torch.empty(T, nq, d)
+        for h in range(nq):
+            sc = (q[:, h, :] @ K[:, h // G, :].t()) / math.sqrt(d)  # [T, ctx]
+            causal = torch.arange(K.shape[0])[None, :] > (n_past + torch.arange(T))[:, None]
+            sc = sc.masked_fill(causal, float("-inf"))
+            out[:, h, :] = torch.softmax(sc, dim=-1) @ V[:, h // G, :]
+        attn = bf(out.reshape(T, nq * d))
+        resid = resid + attn @ w[f"l{l}.wo"].t()
+        xn = rmsnorm(resid, w[f"l{l}.ffn_norm"], s.rms_eps)
+        g = xn @ w[f"l{l}.wg"].t()
+        u = xn @ w[f"l{l}.wu"].t()
+        act = bf(g / (1.0 + torch.exp(-g)) * u)
+        return resid + act @ w[f"l{l}.wd"].t()
+
+    def forward(self, tokens: list[int], start: int, cache: dict | None):
+        """Run positions start..start+len(tokens)-1 of one sequence.
+
+        Returns (logits of the last position [V] fp32, cache) where cache holds
+        per-layer K/V [ctx, nkv, d] (bf16-valued fp32).
+        """
+        s, w = self.s, self.w
+        if cache is None:
+            cache = {"k": [None] * s.n_layers, "v": [None] * s.n_layers}
+        pos = torch.arange(start, start + len(tokens))
+        resid = w["embed"][torch.tensor(tokens)].clone()
+        for l in range(s.n_layers):
+            resid = self._layer(l, resid, pos, cache["k"], cache["v"])
+        xn = rmsnorm(resid[-1:], w["final_norm"], s.rms_eps)
+        logits = (xn @ w["lm_head"].t())[0]
+        return logits, cache
+
+    # Eq. 2: prefill module P_θp(X) -> (first-token logits, C_X)
+    def prefill(self, prompt: list[int]):
+        return self.forward(prompt, 0, None)
+
+    # Eq. 3: decode module D_θd(y_{t-1}, C_{<t-1}) -> (logits, C_t)
+    def decode(self, token: int, pos: int, cache: dict):
+        return self.forward([token], pos, cache)
+
+
+def greedy_shared_decode(prefills: list[OracleDecoder], decoder: OracleDecoder, prompts: list[list[int]],
+                         module_of: list[int], n_steps: int):
+    """Reference semantics of SUN: request i is prefilled by
+    its task module prefills[module_of[i]], then decoded greedily by the one shared
+    decoder. Returns (tokens [B][1+n_steps], per-step logits [n_steps][B][V],
+    per-step top-2 margins)."""
+    toks, caches, logs, margins = [], [], [], []
+    for p, m in zip(prompts, module_of):
+        lg, c = prefills[m].prefill(p)
+        toks.append([int(argmax_lowest(lg[None])[0])])
+        caches.append(c)
+    for t in range(n_steps):
+        step_logits = []
+        for i, p in enumerate(prompts):
+            lg, caches[i] = decoder.decode(toks[i][-1], len(p) + t, caches[i])
+            step_logits.append(lg)
+            toks[i].append(int(argmax_lowest(lg[None])[0]))
+        L = torch.stack(step_logits)
+        top2 = L.topk(2, dim=-1).values
+        margins.append((top2[:, 0] - top2[:, 1]))
+        logs.append(L)
+    return toks, logs, margins

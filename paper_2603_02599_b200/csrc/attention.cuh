@@ -1,0 +1,262 @@
+// attention.cuh — paged split-K flash-decoding attention over the shared KV pool.
+//
+// One CTA = one (split, kv_head, sequence) work unit. The GQA group of query
+// heads sharing that kv head (4 for Llama-3 shapes, 5 for Qwen2.5-14B) forms
+// the rows of an m16n8k16 tile, so K/V bytes are read exactly once per group.
+// K/V pages are staged by TMA (3-D tensor map over the page pool, SWIZZLE_128B,
+// 16-token x 128 B boxes) into per-warp mbarrier rings; each warp consumes every
+// NWARPS-th page with ldmatrix + mma.sync, online softmax in fp32 with
+// quad-shuffle reductions, then the warps merge through shared memory and the
+// unit's (m, l, O) partial goes to global memory for the split combine.
+//
+// Replaces the KV term `sum(resident_tokens * kv_bytes_per_token)` of the
+// reference step price (poolsim costmodel.py:112, 139; engine.py:427-428).
+#pragma once
+#include "sun_common.cuh"
+
+namespace sun {
+
+constexpr int kPageTokens = 16;  // tokens per KV page (one m16n8k16 k-step of P.V)
+
+struct AttnArgs {
+  const __nv_bfloat16* q;  // [B][n_q_heads][D]
+  const int* positions;    // [B] position of the decoded token; ctx = pos + 1
+  const int* block_tables; // [B][bt_stride]
+  int bt_stride;
+  int layer;
+  int n_q_heads;
+  int n_kv_heads;
+  int pages_per_split;
+  int max_splits;
+  float scale_log2;        // log2(e) / sqrt(D)
+  float* part_o;           // [B][n_q_heads][max_splits][D]
+  float* part_ml;          // [B][n_q_heads][max_splits][2]
+  __nv_bfloat16* out;      // [B][n_q_heads * D]   (combine output)
+  long long ld_out;
+};
+
+template <int D>
+struct AttnCfg {
+  static constexpr int kWarps = 4;
+  static constexpr int kStages = (D == 128) ? 3 : 4;
+  static constexpr int kBoxes = D / 64;                          // 128 B boxes per row
+  static constexpr uint32_t kTileBytes = kPageTokens * D * 2;    // K (or V) of one page
+  static constexpr uint32_t kStageBytes = 2 * kTileBytes;
+  static constexpr size_t kSmem = 1024 + size_t(kWarps) * kStages * kStageBytes + 1024;
+};
+
+// byte offset of (token, dim) inside one staged [16][D] tile (boxes of 64 cols, SW128)
+SUN_DEVICE uint32_t kv_swz(int tok, int dim) {
+  const int box = dim >> 6;
+  const int chunk = (dim & 63) >> 3;
+  return static_cast<uint32_t>(box * 2048 + tok * 128 + ((chunk ^ (tok & 7)) << 4));
+}
+
+template <int D>
+__global__ void __launch_bounds__(128)
+    attn_decode_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnArgs a) {
+  using C = AttnCfg<D>;
+  const int split = blockIdx.x;
+  const int kvh = blockIdx.y;
+  const int b = blockIdx.z;
+  pdl_wait();
+  const int ctx = a.positions[b] + 1;
+  const int n_pages = (ctx + kPageTokens - 1) / kPageTokens;
+  const int p0 = split * a.pages_per_split;
+  if (p0 >= n_pages) return;
+  const int p1 = min(n_pages, p0 + a.pages_per_split);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kWarps * C::kStages * C::kStageBytes);
+  float* merge_ml = reinterpret_cast<float*>(bars + C::kWarps * C::kStages);  // [warps][8][2]
+
+  const int warp = warp_id_sync();
+  const int lane = threadIdx.x & 31;
+  const int G = a.n_q_heads / a.n_kv_heads;  // <= 8
+  const int g = lane >> 2;                   // query row owned by this quad
+  const int t = lane & 3;
+  uint8_t* my_stages = smem + warp * C::kStages * C::kStageBytes;
+  uint64_t* my_bars = bars + warp * C::kStages;
+
+  const int n_my = (p1 - p0 - warp + C::kWarps - 1) / C::kWarps > 0 ? (p1 - p0 - warp + C::kWarps - 1) / C::kWarps : 0;
+  const int* bt = a.block_tables + static_cast<long long>(b) * a.bt_stride;
+  const int row_k = ((a.layer * 2 + 0) * a.n_kv_heads + kvh) * kPageTokens;
+  const int row_v = ((a.layer * 2 + 1) * a.n_kv_heads + kvh) * kPageTokens;
+
+  auto issue = [&](int i) {  // lane 0 only: stage the i-th page of this warp
+    const int s = i % C::kStages;
+    const int page = bt[p0 + warp + i * C::kWarps];
+    uint8_t* dst = my_stages + s * C::kStageBytes;
+    mbar_arrive_expect_tx(&my_bars[s], C::kStageBytes);
+#pragma unroll
+    for (int bx = 0; bx < C::kBoxes; ++bx) {
+      tma_load_3d(dst + bx * 2048, &tm_kv, &my_bars[s], bx * 64, row_k, page, kEvictFirst);
+      tma_load_3d(dst + C::kTileBytes + bx * 2048, &tm_kv, &my_bars[s], bx * 64, row_v, page, kEvictFirst);
+    }
+  };
+
+  if (lane == 0) {
+    for (int s = 0; s < C::kStages; ++s) mbar_init(&my_bars[s], 1);
+    fence_barrier_init();
+    const int pre = min(n_my, C::kStages);
+    for (int i = 0; i < pre; ++i) issue(i);
+  }
+  __syncwarp();
+
+  // Q fragments (A operand, rows = query heads of the group, zero-padded to 16).
+  uint32_t qa[D / 16][2];
+  {
+    const __nv_bfloat16* qrow = a.q + (static_cast<long long>(b) * a.n_q_heads + kvh * G + g) * D;
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+      if (g < G) {
+        qa[kk][0] = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * t);
+        qa[kk][1] = *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 8 + 2 * t);
+      } else {
+        qa[kk][0] = 0u;
+        qa[kk][1] = 0u;
+      }
+    }
+  }
+
+  float o[D / 8][4];
+#pragma unroll
+  for (int n = 0; n < D / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float m_run = -INFINITY;
+  float l_run = 0.f;
+
+  const int mi = lane >> 3;  // ldmatrix matrix index supplied by this lane
+  const int mr = lane & 7;   // row within that matrix
+
+  for (int i = 0; i < n_my; ++i) {
+    const int s = i % C::kStages;
+    mbar_wait(&my_bars[s], (i / C::kStages) & 1);
+    const uint32_t kbase = smem_u32(my_stages + s * C::kStageBytes);
+    const uint32_t vbase = kbase + C::kTileBytes;
+    const int tok0 = (p0 + warp + i * C::kWarps) * kPageTokens;
+
+    // S = Q . K^T  (two n-tiles of 8 tokens)
+    float sacc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+      uint32_t r0, r1, r2, r3;
+      const int tok = ((mi >> 1) << 3) + mr;
+      const int dim = kk * 16 + ((mi & 1) << 3);
+      ldmatrix_x4(kbase + kv_swz(tok, dim), r0, r1, r2, r3);
+      mma_16816(sacc[0], qa[kk][0], 0u, qa[kk][1], 0u, r0, r1);
+      mma_16816(sacc[1], qa[kk][0], 0u, qa[kk][1], 0u, r2, r3);
+    }
+    // scale, mask, online softmax (row g; c2/c3 are padding rows)
+    float sv[4];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int n = 0; n < 2; ++n) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int tok = tok0 + n * 8 + 2 * t + e;
+        const float x = tok < ctx ? sacc[n][e] * a.scale_log2 : -INFINITY;
+        sv[n * 2 + e] = x;
+        mx = fmaxf(mx, x);
+      }
+    }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const float m_new = fmaxf(m_run, mx);
+    const float corr = exp2f(m_run - m_new);  // m_run = -inf -> 0
+    m_run = m_new;
+    float p[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) p[e] = exp2f(sv[e] - m_new);
+    l_run = l_run * corr + (p[0] + p[1] + p[2] + p[3]);
+#pragma unroll
+    for (int n = 0; n < D / 8; ++n) {
+      o[n][0] *= corr;
+      o[n][1] *= corr;
+    }
+    const uint32_t pa0 = pack_bf16x2(p[0], p[1]);
+    const uint32_t pa2 = pack_bf16x2(p[2], p[3]);
+    // O += P . V
+#pragma unroll
+    for (int nn = 0; nn < D / 16; ++nn) {
+      uint32_t r0, r1, r2, r3;
+      const int tok = ((mi & 1) << 3) + mr;
+      const int dim = nn * 16 + ((mi >> 1) << 3);
+      ldmatrix_x4_trans(vbase + kv_swz(tok, dim), r0, r1, r2, r3);
+      mma_16816(o[2 * nn], pa0, 0u, pa2, 0u, r0, r1);
+      mma_16816(o[2 * nn + 1], pa0, 0u, pa2, 0u, r2, r3);
+    }
+    __syncwarp();
+    if (lane == 0 && i + C::kStages < n_my) {
+      fence_proxy_async_smem();
+      issue(i + C::kStages);
+    }
+  }
+  l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
+  l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
+
+  // ---- merge the warps of this CTA through shared memory ----
+  __syncthreads();  // every warp is done with its stage ring
+  float* merge_o = reinterpret_cast<float*>(smem);  // [warps][8][D]
+  if (g < G) {
+#pragma unroll
+    for (int n = 0; n < D / 8; ++n) {
+      merge_o[(warp * 8 + g) * D + n * 8 + 2 * t] = o[n][0];
+      merge_o[(warp * 8 + g) * D + n * 8 + 2 * t + 1] = o[n][1];
+    }
+    if (t == 0) {
+      merge_ml[(warp * 8 + g) * 2 + 0] = m_run;
+      merge_ml[(warp * 8 + g) * 2 + 1] = l_run;
+    }
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
+    const int gg = idx / D;
+    const int dim = idx % D;
+    float mm = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < C::kWarps; ++w) mm = fmaxf(mm, merge_ml[(w * 8 + gg) * 2]);
+    float acc = 0.f, ll = 0.f;
+#pragma unroll
+    for (int w = 0; w < C::kWarps; ++w) {
+      const float mw = merge_ml[(w * 8 + gg) * 2];
+      const float sc = (mw == -INFINITY) ? 0.f : exp2f(mw - mm);
+      acc += merge_o[(w * 8 + gg) * D + dim] * sc;
+      ll += merge_ml[(w * 8 + gg) * 2 + 1] * sc;
+    }
+    const int head = kvh * G + gg;
+    const long long u = (static_cast<long long>(b) * a.n_q_heads + head) * a.max_splits + split;
+    a.part_o[u * D + dim] = acc;
+    if (dim == 0) {
+      a.part_ml[u * 2 + 0] = mm;
+      a.part_ml[u * 2 + 1] = ll;
+    }
+  }
+  pdl_launch_dependents();
+}
+
+// Merge the split partials of one (sequence, query head) and emit bf16 output.
+template <int D>
+__global__ void __launch_bounds__(128) attn_combine_kernel(const AttnArgs a) {
+  pdl_wait();
+  const int head = blockIdx.x;
+  const int b = blockIdx.y;
+  const int ctx = a.positions[b] + 1;
+  const int n_pages = (ctx + kPageTokens - 1) / kPageTokens;
+  const int n_splits = (n_pages + a.pages_per_split - 1) / a.pages_per_split;
+  const long long u0 = (static_cast<long long>(b) * a.n_q_heads + head) * a.max_splits;
+  float mm = -INFINITY;
+  for (int s = 0; s < n_splits; ++s) mm = fmaxf(mm, a.part_ml[(u0 + s) * 2]);
+  for (int dim = threadIdx.x; dim < D; dim += blockDim.x) {
+    float acc = 0.f, ll = 0.f;
+    for (int s = 0; s < n_splits; ++s) {
+      const float sc = exp2f(a.part_ml[(u0 + s) * 2] - mm);
+      acc += a.part_o[(u0 + s) * D + dim] * sc;
+      ll += a.part_ml[(u0 + s) * 2 + 1] * sc;
+    }
+    a.out[static_cast<long long>(b) * a.ld_out + head * D + dim] = __float2bfloat16_rn(acc / ll);
+  }
+  pdl_launch_dependents();
+}
+
+}  // namespace sun

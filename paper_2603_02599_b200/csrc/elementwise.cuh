@@ -1,0 +1,106 @@
+// elementwise.cuh — row kernels of the decode step: embedding gather fused with
+// the first RMSNorm, RMSNorm producing the bf16 GEMM operand, and the final
+// greedy argmax over the lm_head tiles' (max, index) partials.
+#pragma once
+#include "sun_common.cuh"
+
+namespace sun {
+
+constexpr int kRowThreads = 256;
+
+SUN_DEVICE float block_sum(float v, float* red) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  float s = 0.f;
+  for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) s += red[i];
+  return s;
+}
+
+// y = bf16(x * rsqrt(mean(x^2) + eps) * w), fp32 math, one rounding.
+// If `tokens` is non-null the row is first gathered from the embedding table
+// into the fp32 residual stream (x := float(embed[token])).
+__global__ void __launch_bounds__(kRowThreads)
+    rmsnorm_kernel(const int* __restrict__ tokens, const __nv_bfloat16* __restrict__ embed,
+                   float* __restrict__ resid, const __nv_bfloat16* __restrict__ w,
+                   __nv_bfloat16* __restrict__ out, int h, long long ld_out, float eps) {
+  __shared__ float red[kRowThreads / 32];
+  pdl_wait();
+  const int b = blockIdx.x;
+  float* x = resid + static_cast<long long>(b) * h;
+  if (tokens != nullptr) {
+    const __nv_bfloat16* e = embed + static_cast<long long>(tokens[b]) * h;
+    for (int i = threadIdx.x * 2; i < h; i += kRowThreads * 2) {
+      const __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(e + i);
+      x[i] = __bfloat162float(v.x);
+      x[i + 1] = __bfloat162float(v.y);
+    }
+    __syncthreads();
+  }
+  float ss = 0.f;
+  for (int i = threadIdx.x * 4; i < h; i += kRowThreads * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(x + i);
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  const float tot = block_sum(ss, red);
+  const float r = rsqrtf(tot / static_cast<float>(h) + eps);
+  __nv_bfloat16* y = out + static_cast<long long>(b) * ld_out;
+  for (int i = threadIdx.x * 4; i < h; i += kRowThreads * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(x + i);
+    const __nv_bfloat162 w01 = *reinterpret_cast<const __nv_bfloat162*>(w + i);
+    const __nv_bfloat162 w23 = *reinterpret_cast<const __nv_bfloat162*>(w + i + 2);
+    __nv_bfloat162 o01 = __floats2bfloat162_rn(v.x * r * __bfloat162float(w01.x), v.y * r * __bfloat162float(w01.y));
+    __nv_bfloat162 o23 = __floats2bfloat162_rn(v.z * r * __bfloat162float(w23.x), v.w * r * __bfloat162float(w23.y));
+    *reinterpret_cast<__nv_bfloat162*>(y + i) = o01;
+    *reinterpret_cast<__nv_bfloat162*>(y + i + 2) = o23;
+  }
+  pdl_launch_dependents();
+}
+
+// next[b] = argmax over lm_head tiles (ties -> lowest vocabulary index).
+__global__ void __launch_bounds__(kRowThreads)
+    argmax_reduce_kernel(const float* __restrict__ val, const int* __restrict__ idx, int m_tiles, int bn,
+                         int* __restrict__ next) {
+  __shared__ float sv[kRowThreads / 32];
+  __shared__ int si[kRowThreads / 32];
+  pdl_wait();
+  const int b = blockIdx.x;
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int t = threadIdx.x; t < m_tiles; t += kRowThreads) {
+    const float v = val[static_cast<long long>(t) * bn + b];
+    const int i = idx[static_cast<long long>(t) * bn + b];
+    if (v > bv || (v == bv && i < bi)) {
+      bv = v;
+      bi = i;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+    if (ov > bv || (ov == bv && oi < bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sv[threadIdx.x >> 5] = bv;
+    si[threadIdx.x >> 5] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kRowThreads / 32; ++w) {
+      if (sv[w] > bv || (sv[w] == bv && si[w] < bi)) {
+        bv = sv[w];
+        bi = si[w];
+      }
+    }
+    next[b] = bi;
+  }
+  pdl_launch_dependents();
+}
+
+}  // namespace sun

@@ -1,0 +1,96 @@
+"""Kernel-level entry points over torch device tensors (unit parity surface).
+
+Each function calls exactly one C-ABI symbol of libsun_b200.so on the current
+torch stream. Tensors must already live on the GPU; nothing here falls back to
+PyTorch math.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _need_cuda(*ts: torch.Tensor) -> None:
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("SUN kernels take CUDA tensors only (no CPU fallback)")
+
+
+def gemm_workspace(n_out: int, k: int, batch: int, device) -> torch.Tensor:
+    lib = _lib.load()
+    nb = ctypes.c_size_t()
+    _lib.check(lib.sun_gemm_workspace_bytes(n_out, k, batch, ctypes.byref(nb)), "sun_gemm_workspace_bytes")
+    return torch.zeros(nb.value, dtype=torch.uint8, device=device)
+
+
+def gemm_bf16(w: torch.Tensor, x: torch.Tensor, batch: int, out: torch.Tensor | None = None,
+              accumulate: bool = False, workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """out[b, n] (=|+=) sum_k w[n, k] x[b, k] with the tcgen05 swap-AB GEMM.
+
+    ``x`` must have at least round_up(batch, 16) rows (rows >= batch are ignored).
+    """
+    _need_cuda(w, x)
+    assert w.dtype == torch.bfloat16 and x.dtype == torch.bfloat16
+    n_out, k = w.shape
+    if out is None:
+        out = torch.zeros(batch, n_out, dtype=torch.float32, device=w.device)
+    if workspace is None:
+        workspace = gemm_workspace(n_out, k, batch, w.device)
+    lib = _lib.load()
+    _lib.check(lib.sun_gemm_bf16(w.data_ptr(), n_out, k, x.data_ptr(), x.stride(0), x.shape[0], batch,
+                                 out.data_ptr(), out.stride(0), int(accumulate), workspace.data_ptr(),
+                                 workspace.numel(), _stream()), "sun_gemm_bf16")
+    return out
+
+
+def attention_decode(dims: _lib.SunDecoderDims, kv_pool: torch.Tensor, layer: int, q: torch.Tensor,
+                     positions: torch.Tensor, block_tables: torch.Tensor, pages_per_split: int = 0,
+                     out: torch.Tensor | None = None) -> torch.Tensor:
+    """Paged split-K decode attention for one layer; q bf16 [B, nq, d] post-RoPE."""
+    _need_cuda(kv_pool, q, positions, block_tables)
+    batch = q.shape[0]
+    if out is None:
+        out = torch.empty(batch, dims.n_q_heads * dims.head_dim, dtype=torch.bfloat16, device=q.device)
+    max_pages = (dims.max_context + 15) // 16
+    ws = torch.empty(batch * dims.n_q_heads * max_pages * (dims.head_dim + 2) * 4 + 4096, dtype=torch.uint8,
+                     device=q.device)
+    pool = _lib.SunKvPool(kv_pool.data_ptr(), kv_pool.shape[0])
+    lib = _lib.load()
+    _lib.check(lib.sun_attention_decode(ctypes.byref(dims), ctypes.byref(pool), layer, q.data_ptr(),
+                                        positions.data_ptr(), block_tables.data_ptr(), block_tables.stride(0),
+                                        batch, pages_per_split, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                        _stream()), "sun_attention_decode")
+    return out
+
+
+def rmsnorm(x: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
+    _need_cuda(x, w)
+    b, h = x.shape
+    y = torch.empty(b, h, dtype=torch.bfloat16, device=x.device)
+    lib = _lib.load()
+    _lib.check(lib.sun_rmsnorm(x.data_ptr(), w.data_ptr(), y.data_ptr(), b, h, eps, _stream()), "sun_rmsnorm")
+    return y
+
+
+def quantize_w4(w: torch.Tensor, group: int = 128) -> tuple[torch.Tensor, torch.Tensor]:
+    """QSUN SUN-W4 quantisation on the GPU -> (packed uint8, scales bf16 [K/g, rows_pad])."""
+    _need_cuda(w)
+    rows, k = w.shape
+    rows_pad = (rows + 127) // 128 * 128
+    packed = torch.zeros(rows_pad * k // 2, dtype=torch.uint8, device=w.device)
+    scales = torch.zeros(k // group, rows_pad, dtype=torch.bfloat16, device=w.device)
+    lib = _lib.load()
+    _lib.check(lib.sun_quantize_w4(w.contiguous().data_ptr(), rows, k, group, packed.data_ptr(), scales.data_ptr(),
+                                   _stream()), "sun_quantize_w4")
+    return packed, scales

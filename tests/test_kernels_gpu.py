@@ -1,0 +1,103 @@
+"""Kernel-level numerics on the B200: each sm_100a kernel vs a plain torch fp32
+restatement of the same op on the same inputs (tolerances stated inline)."""
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _r16(b):
+    return (b + 15) // 16 * 16
+
+
+@pytest.mark.parametrize(
+    "n_out,k,batch",
+    [(256, 256, 1), (768, 256, 8), (1408, 256, 17), (300, 688, 5), (4096, 4096, 64), (6144, 4096, 64),
+     (1000, 512, 256), (4096, 14336, 33), (512, 128, 128)],
+)
+def test_gemm_bf16_matches_fp32(cuda, n_out, k, batch):
+    from paper_2603_02599_b200 import kernels
+
+    g = torch.Generator(device="cpu").manual_seed(n_out * 7 + k + batch)
+    w = (torch.randn(n_out, k, generator=g) * 0.02).to(torch.bfloat16).to(cuda)
+    x = torch.randn(_r16(batch), k, generator=g).to(torch.bfloat16).to(cuda)
+    x[batch:] = float("nan")  # padded batch rows must not leak into valid columns
+    out = kernels.gemm_bf16(w, x, batch)
+    ref = x[:batch].float() @ w.float().t()
+    torch.cuda.synchronize()
+    # fp32 accumulation of bf16 products: only summation order differs
+    torch.testing.assert_close(out, ref, rtol=1e-4, atol=1e-4 * math.sqrt(k))
+    # accumulate mode adds onto the existing buffer
+    out2 = kernels.gemm_bf16(w, x, batch, out=out.clone(), accumulate=True)
+    torch.testing.assert_close(out2, 2 * ref, rtol=1e-4, atol=2e-4 * math.sqrt(k))
+
+
+def test_gemm_deterministic_split_k(cuda):
+    from paper_2603_02599_b200 import kernels
+
+    g = torch.Generator(device="cpu").manual_seed(3)
+    w = (torch.randn(4096, 14336, generator=g) * 0.02).to(torch.bfloat16).to(cuda)
+    x = torch.randn(64, 14336, generator=g).to(torch.bfloat16).to(cuda)
+    a = kernels.gemm_bf16(w, x, 64)
+    b = kernels.gemm_bf16(w, x, 64)
+    assert torch.equal(a, b)
+
+
+def _attn_ref(q, pool, layer, positions, bt, G):
+    B, nq, d = q.shape
+    out = torch.empty(B, nq * d, dtype=torch.float32)
+    for b in range(B):
+        ctx = int(positions[b]) + 1
+        pages = bt[b, : (ctx + 15) // 16].tolist()
+        kv = pool[pages, layer].float()  # [np, 2, nkv, 16, d]
+        K = kv[:, 0].permute(1, 0, 2, 3).reshape(kv.shape[2], -1, d)[:, :ctx]
+        V = kv[:, 1].permute(1, 0, 2, 3).reshape(kv.shape[2], -1, d)[:, :ctx]
+        for h in range(nq):
+            s = (K[h // G] @ q[b, h].float()) / math.sqrt(d)
+            p = torch.softmax(s, dim=0)
+            out[b, h * d:(h + 1) * d] = p @ V[h // G]
+    return out
+
+
+@pytest.mark.parametrize("d,nq,nkv", [(64, 8, 2), (128, 32, 8), (128, 40, 8)])
+@pytest.mark.parametrize("pps", [0, 1, 3])
+def test_attention_decode_matches_fp32(cuda, d, nq, nkv, pps):
+    from paper_2603_02599_b200 import _lib, kernels
+
+    L, num_pages, max_ctx = 2, 96, 600
+    ctxs = [1, 15, 16, 17, 300, 599]
+    B = len(ctxs)
+    g = torch.Generator(device="cpu").manual_seed(d + nq + pps)
+    pool = torch.randn(num_pages, L, 2, nkv, 16, d, generator=g).to(torch.bfloat16)
+    perm = torch.randperm(num_pages, generator=g)
+    maxp = (max_ctx + 15) // 16
+    bt = torch.zeros(B, maxp, dtype=torch.int32)
+    used = 0
+    for b, c in enumerate(ctxs):
+        n = (c + 15) // 16
+        bt[b, :n] = perm[used:used + n].to(torch.int32)
+        used += n
+    positions = torch.tensor([c - 1 for c in ctxs], dtype=torch.int32)
+    q = torch.randn(B, nq, d, generator=g).to(torch.bfloat16)
+    dims = _lib.SunDecoderDims(vocab=16, hidden=256, n_layers=L, n_q_heads=nq, n_kv_heads=nkv, head_dim=d,
+                               ffn=256, page_size=16, max_context=max_ctx, weight_bits=16, group_size=128,
+                               qkv_bias=0, rms_eps=1e-5)
+    for layer in range(L):
+        out = kernels.attention_decode(dims, pool.to(cuda), layer, q.to(cuda), positions.to(cuda), bt.to(cuda),
+                                       pages_per_split=pps)
+        ref = _attn_ref(q, pool, layer, positions, bt, nq // nkv)
+        # P is rounded to bf16 before P.V (flash-decoding), output rounded to bf16
+        torch.testing.assert_close(out.float().cpu(), ref, rtol=2e-2, atol=2e-2)
+
+
+def test_rmsnorm_matches_fp32(cuda):
+    from paper_2603_02599_b200 import kernels
+
+    g = torch.Generator(device="cpu").manual_seed(5)
+    x = torch.randn(7, 4096, generator=g)
+    w = (1 + 0.1 * torch.randn(4096, generator=g)).to(torch.bfloat16)
+    y = kernels.rmsnorm(x.to(cuda), w.to(cuda), 1e-5).cpu()
+    ref = x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + 1e-5) * w.float()
+    torch.testing.assert_close(y.float(), ref, rtol=8e-3, atol=1e-2)
