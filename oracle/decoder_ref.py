@@ -184,3 +184,20 @@ def greedy_shared_decode(prefills: list[OracleDecoder], decoder: OracleDecoder, 
         margins.append((top2[:, 0] - top2[:, 1]))
         logs.append(L)
     return toks, logs, margins
+
+
+def teacher_forced(prefills: list[OracleDecoder], decoder: OracleDecoder, prompts: list[list[int]],
+                   module_of: list[int], tokens: list[list[int]]):
+    """Score a given token history (e.g. the GPU's greedy output) with the oracle:
+    returns per-sequence logits [1 + n_steps, V] where row 0 is the prefill
+    module's first-token distribution and row t+1 the decoder's after consuming
+    tokens[i][t] at position len(prompt) + t."""
+    out = []
+    for i, (p, m) in enumerate(zip(prompts, module_of)):
+        lg, c = prefills[m].prefill(p)
+        rows = [lg]
+        for t, tok in enumerate(tokens[i][:-1]):
+            lg, c = decoder.decode(tok, len(p) + t, c)
+            rows.append(lg)
+        out.append(torch.stack(rows))
+    return out

@@ -174,8 +174,14 @@ __global__ void __launch_bounds__(128)
       o[n][0] *= corr;
       o[n][1] *= corr;
     }
+    // P is split into bf16 hi + lo parts (p = hi + lo to ~16 mantissa bits) so the
+    // bf16 tensor-core P.V keeps fp32-grade probabilities: with near-uniform
+    // attention a plain bf16 P perturbs the output by ~0.1% (1/3 of the bf16
+    // output roundings flip), which the hi/lo pair removes for 2x P.V mma.
     const uint32_t pa0 = pack_bf16x2(p[0], p[1]);
     const uint32_t pa2 = pack_bf16x2(p[2], p[3]);
+    const uint32_t pl0 = pack_bf16x2(p[0] - bf16_round(p[0]), p[1] - bf16_round(p[1]));
+    const uint32_t pl2 = pack_bf16x2(p[2] - bf16_round(p[2]), p[3] - bf16_round(p[3]));
     // O += P . V
 #pragma unroll
     for (int nn = 0; nn < D / 16; ++nn) {
@@ -185,6 +191,8 @@ __global__ void __launch_bounds__(128)
       ldmatrix_x4_trans(vbase + kv_swz(tok, dim), r0, r1, r2, r3);
       mma_16816(o[2 * nn], pa0, 0u, pa2, 0u, r0, r1);
       mma_16816(o[2 * nn + 1], pa0, 0u, pa2, 0u, r2, r3);
+      mma_16816(o[2 * nn], pl0, 0u, pl2, 0u, r0, r1);
+      mma_16816(o[2 * nn + 1], pl0, 0u, pl2, 0u, r2, r3);
     }
     __syncwarp();
     if (lane == 0 && i + C::kStages < n_my) {

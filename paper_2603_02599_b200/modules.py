@@ -1,0 +1,163 @@
+"""Prefill-module / decode-module split of SUN on the B200 (Eqs. 2-4).
+
+``SharedDecodeModule`` is the frozen decode module D_θd: one ``sun_decode_step``
+per step over a mixed-model batch (members prefilled by different task
+modules), optionally replayed from a CUDA graph per (batch, split) bucket.
+``PrefillModule`` is a task-specific P_θp^τ: it writes the prompt's KV into the
+shared paged pool with the same kernels (one position per launch chain — the
+producer side is not the measured hot path) and returns the
+first generated token, as Eq. 2 specifies.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from .kvpool import PAGE_TOKENS, KvPool, pages_for
+from .spec import DecoderSpec
+from .weights import DeviceWeights
+
+
+class _StepRunner:
+    """Owns one C decoder (TMA descriptors + workspace) over a weight set."""
+
+    def __init__(self, spec: DecoderSpec, weights: DeviceWeights, kv: KvPool, max_batch: int, max_context: int,
+                 use_pdl: bool = True):
+        self.spec, self.weights, self.kv = spec, weights, kv
+        self.max_batch, self.max_context = int(max_batch), int(max_context)
+        self.max_pages = pages_for(self.max_context)
+        lib = _lib.load()
+        self.dims = _lib.SunDecoderDims(
+            vocab=spec.vocab, hidden=spec.hidden, n_layers=spec.n_layers, n_q_heads=spec.n_q_heads,
+            n_kv_heads=spec.n_kv_heads, head_dim=spec.head_dim, ffn=spec.ffn, page_size=PAGE_TOKENS,
+            max_context=self.max_context, weight_bits=spec.weight_bits, group_size=spec.group_size,
+            qkv_bias=int(spec.qkv_bias), rms_eps=spec.rms_eps)
+        nb = ctypes.c_size_t()
+        _lib.check(lib.sun_decoder_workspace_bytes(ctypes.byref(self.dims), self.max_batch, ctypes.byref(nb)),
+                   "workspace sizing")
+        dev = weights.device
+        self.workspace = torch.zeros(nb.value, dtype=torch.uint8, device=dev)
+        self._pool = _lib.SunKvPool(kv.tensor.data_ptr(), kv.num_pages)
+        h = ctypes.c_void_p()
+        _lib.check(lib.sun_decoder_create(ctypes.byref(self.dims), ctypes.byref(weights.struct),
+                                          ctypes.byref(self._pool), self.workspace.data_ptr(), self.workspace.numel(),
+                                          self.max_batch, int(use_pdl), ctypes.byref(h)), "sun_decoder_create")
+        self._h = h
+        self._lib = lib
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.sun_decoder_destroy(h)
+            self._h = None
+
+    def launch(self, tokens: torch.Tensor, positions: torch.Tensor, block_tables: torch.Tensor, batch: int,
+               next_tokens: torch.Tensor, logits: torch.Tensor | None = None, pages_per_split: int = 0) -> None:
+        """Enqueue one decode step on the current stream (all tensors on device)."""
+        if batch < 1:
+            raise ValueError("decode batch must be non-empty")
+        if block_tables.shape[1] < 1 or block_tables.dtype != torch.int32:
+            raise ValueError("block_tables must be int32 [B, max_pages]")
+        st = torch.cuda.current_stream().cuda_stream
+        _lib.check(self._lib.sun_decode_step(
+            self._h, tokens.data_ptr(), positions.data_ptr(), block_tables.data_ptr(), block_tables.stride(0), batch,
+            pages_per_split, None if logits is None else logits.data_ptr(), next_tokens.data_ptr(), st),
+            "sun_decode_step")
+
+
+class SharedDecodeModule(_StepRunner):
+    """D_θd — the frozen shared decode module serving every task's requests.
+
+    Static device buffers (tokens / positions / block tables / next tokens /
+    logits) back an optional CUDA graph per (batch, pages_per_split) bucket, so
+    a step is one graph launch (32 layers x 8 kernels otherwise).
+    """
+
+    def __init__(self, spec, weights, kv, max_batch, max_context, use_pdl: bool = True, keep_logits: bool = True):
+        super().__init__(spec, weights, kv, max_batch, max_context, use_pdl)
+        dev = weights.device
+        self.tokens = torch.zeros(self.max_batch, dtype=torch.int32, device=dev)
+        self.positions = torch.zeros(self.max_batch, dtype=torch.int32, device=dev)
+        self.block_tables = torch.zeros(self.max_batch, self.max_pages, dtype=torch.int32, device=dev)
+        self.next_tokens = torch.zeros(self.max_batch, dtype=torch.int32, device=dev)
+        self.logits = torch.zeros(self.max_batch, spec.vocab, dtype=torch.float32, device=dev) if keep_logits else None
+        self._graphs: dict[tuple[int, int], torch.cuda.CUDAGraph] = {}
+
+    def step_static(self, batch: int, pages_per_split: int = 0, graph: bool = True) -> None:
+        """One step over the static buffers' first ``batch`` rows (device-resident inputs)."""
+        if not graph:
+            self.launch(self.tokens, self.positions, self.block_tables, batch, self.next_tokens, self.logits,
+                        pages_per_split)
+            return
+        key = (batch, pages_per_split)
+        g = self._graphs.get(key)
+        if g is None:
+            # warm (TMA descriptor cache for this batch bucket) then capture
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                self.launch(self.tokens, self.positions, self.block_tables, batch, self.next_tokens, self.logits,
+                            pages_per_split)
+            torch.cuda.current_stream().wait_stream(s)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.launch(self.tokens, self.positions, self.block_tables, batch, self.next_tokens, self.logits,
+                            pages_per_split)
+            self._graphs[key] = g
+        g.replay()
+
+    def decode(self, tokens: torch.Tensor, positions: torch.Tensor, block_tables: torch.Tensor,
+               pages_per_split: int = 0, graph: bool = True) -> torch.Tensor:
+        """Eq. 3 over a batch: copy inputs (host or device) into the static
+        buffers, run the step, return next tokens (device int32 view [B])."""
+        b = int(tokens.shape[0])
+        if b < 1:
+            raise ValueError("decode batch must be non-empty")
+        if b > self.max_batch:
+            raise ValueError(f"batch {b} > max_batch {self.max_batch}")
+        self.tokens[:b].copy_(tokens, non_blocking=True)
+        self.positions[:b].copy_(positions, non_blocking=True)
+        self.block_tables[:b, :block_tables.shape[1]].copy_(block_tables, non_blocking=True)
+        self.step_static(b, pages_per_split, graph)
+        return self.next_tokens[:b]
+
+
+class PrefillModule(_StepRunner):
+    """P_θp^τ — a task-specific prefill module writing into the shared pool."""
+
+    def __init__(self, spec, weights, kv, max_batch, max_context, task_id: int, use_pdl: bool = True):
+        super().__init__(spec, weights, kv, max_batch, max_context, use_pdl)
+        self.task_id = task_id
+        dev = weights.device
+        self._next = torch.zeros(self.max_batch, dtype=torch.int32, device=dev)
+        self._logits = torch.zeros(self.max_batch, spec.vocab, dtype=torch.float32, device=dev)
+
+    def prefill(self, prompts: list[list[int]], block_tables: list[list[int]]) -> tuple[list[int], torch.Tensor]:
+        """Fill each prompt's pages and return (first tokens, first-token logits [B, V])."""
+        dev = self.weights.device
+        B = len(prompts)
+        if B > self.max_batch:
+            raise ValueError("too many prompts for this prefill module")
+        lens = [len(p) for p in prompts]
+        if min(lens) < 1:
+            raise ValueError("isl must be >= 1")
+        bt = torch.zeros(B, self.max_pages, dtype=torch.int32)
+        for i, row in enumerate(block_tables):
+            bt[i, :len(row)] = torch.tensor(row, dtype=torch.int32)
+        first = [0] * B
+        last_logits = torch.zeros(B, self.spec.vocab, dtype=torch.float32, device=dev)
+        for t in range(max(lens)):
+            act = [i for i in range(B) if t < lens[i]]
+            toks = torch.tensor([prompts[i][t] for i in act], dtype=torch.int32).to(dev)
+            pos = torch.full((len(act),), t, dtype=torch.int32).to(dev)
+            bts = bt[act].to(dev)
+            self.launch(toks, pos, bts, len(act), self._next, self._logits)
+            done = [j for j, i in enumerate(act) if t == lens[i] - 1]
+            if done:
+                nt = self._next[:len(act)].cpu()
+                for j in done:
+                    first[act[j]] = int(nt[j])
+                    last_logits[act[j]] = self._logits[j]
+        return first, last_logits

@@ -88,8 +88,8 @@ def test_attention_decode_matches_fp32(cuda, d, nq, nkv, pps):
         out = kernels.attention_decode(dims, pool.to(cuda), layer, q.to(cuda), positions.to(cuda), bt.to(cuda),
                                        pages_per_split=pps)
         ref = _attn_ref(q, pool, layer, positions, bt, nq // nkv)
-        # P is rounded to bf16 before P.V (flash-decoding), output rounded to bf16
-        torch.testing.assert_close(out.float().cpu(), ref, rtol=2e-2, atol=2e-2)
+        # P kept as bf16 hi+lo pair; output rounded to bf16 (1 ulp = 2^-8 relative)
+        torch.testing.assert_close(out.float().cpu(), ref, rtol=1e-2, atol=2e-3)
 
 
 def test_rmsnorm_matches_fp32(cuda):
