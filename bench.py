@@ -1,0 +1,447 @@
+#!/usr/bin/env python
+"""bench.py — SUN shared-decode throughput on B200 (BASELINE.json metric).
+
+A "step" is one decode step of the frozen shared decode module over the
+rank's mixed-model batch (members prefilled by different task modules, routed
+to this GPU by the model-agnostic LOT decode router). Default workload = C3:
+Llama-3.1-8B-shaped bf16 decoder, 8 task prefill modules with a Zipf(1.5)
+request mix (poolsim trace seed 42), 64 sequences per GPU at ISL 1024 /
+OSL 256 steady state (contexts 1024..1279). Weights are random-init
+(no checkpoints offline) and the KV pages are a seeded on-device fill
+(cost excluded; the prefill→decode hand-off is measured separately).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c2|c4|c5|c1]
+       [--impl sun|reference] [--routing lot|pinned]
+Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N (one decode worker
+per GPU, weak scaling, no collective on the data path).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode tokens/s/GPU (mixed-model shared decode) at 1/2/4/8 B200; TPOT p50; HBM GB/s"
+
+CONFIGS = {
+    "c1": dict(spec="tiny", bits=16, batch=8, isl=48, osl=32, n_models=2, alpha=0.0,
+               workload="C1 tiny decoder, 2 task prefill modules + shared decoder, mixed batch 8"),
+    "c2": dict(spec="llama3.2-1b", bits=16, batch=64, isl=1984, osl=128, n_models=4, alpha=0.0,
+               workload="C2 Llama-3.2-1B-shaped bf16, 4 prefill modules, mixed batch 64, ctx ~2k"),
+    "c3": dict(spec="llama3.1-8b", bits=16, batch=64, isl=1024, osl=256, n_models=8, alpha=1.5,
+               workload="C3 Llama-3.1-8B-shaped bf16, 8 prefill modules, Zipf a=1.5 mix, 64 seq/GPU, "
+                        "ISL 1024 OSL 256 steady state (ctx 1024-1279)"),
+    "c4": dict(spec="llama3.1-8b", bits=4, batch=128, isl=4032, osl=128, n_models=8, alpha=1.5,
+               workload="C4 QSUN Llama-3.1-8B-shaped W4A16 g128 decoder, batch 128, ctx ~4k"),
+    "c5": dict(spec="qwen2.5-14b", bits=16, batch=32, isl=16320, osl=128, n_models=16, alpha=1.5,
+               workload="C5 Qwen2.5-14B-shaped bf16, 16 prefill modules, 32 seq/GPU, ctx ~16k"),
+}
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------------------- workload
+def build_assignment(cfg, world, routing):
+    """Route B*world requests of the Zipf trace over the decode pool with the
+    reference's rules (LOT anticipatory load, or PINNED model i -> worker i%K).
+    Returns per-worker lists of (request id, model id)."""
+    from paper_2603_02599_b200.router import DecodeDispatcher, PoolSnapshot
+    from paper_2603_02599_b200.sun_types import DecodeRule, RoutingPolicy
+    from paper_2603_02599_b200.trace import ArrivalProcess, WorkloadSpec, generate_trace
+
+    need = cfg["batch"] * world
+    ws = WorkloadSpec(n_models=cfg["n_models"], total_rps=100.0, alpha=cfg["alpha"], isl=cfg["isl"],
+                      osl=cfg["osl"], grace_period=0.0, measurement_window=need / 100.0 + 5, drain_margin=0.0,
+                      seed=42, arrival_process=ArrivalProcess.DETERMINISTIC)
+    trace = generate_trace(ws)[:need]
+    n = cfg["n_models"]
+    wids = list(range(n, n + world))
+    if routing == "pinned":
+        disp = DecodeDispatcher(RoutingPolicy(decode_rule=DecodeRule.PINNED),
+                                pinned_map={m: wids[m % world] for m in range(n)})
+    else:
+        disp = DecodeDispatcher(RoutingPolicy(decode_rule=DecodeRule.LEAST_OUTSTANDING_TOKENS))
+    load = {w: [0, 0, 0] for w in wids}
+    per = {w: [] for w in wids}
+    for r in trace:
+        pool = [PoolSnapshot(w, load[w][0], load[w][1], load[w][2]) for w in wids]
+        w = disp.route(r, pool)
+        load[w][1] += r.isl
+        load[w][2] += r.target_osl - 1
+        per[w].append((r.id, r.model_id))
+    return [per[w] for w in wids]
+
+
+def contexts_for(cfg, nseq):
+    """Steady-state continuous batching: members spread evenly over decode progress."""
+    return [cfg["isl"] + (j * cfg["osl"]) // max(nseq, 1) for j in range(nseq)]
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------------------- CPU baseline
+class CpuOracleStep:
+    """Oracle (CPU fp32, batched linear layers) on host cores, bounded sample:
+    one of the decoder's layers for the whole mixed batch + the lm_head,
+    extrapolated to the full layer count (set up once, then timed per step)."""
+
+    def __init__(self, cfg):
+        import torch
+        from dataclasses import replace
+
+        from oracle.decoder_ref import OracleDecoder, OracleSpec
+        from paper_2603_02599_b200.spec import SPECS
+        from paper_2603_02599_b200.weights import init_weights
+
+        torch.set_num_threads(os.cpu_count() or 1)
+        self.threads = torch.get_num_threads()
+        self.spec = SPECS[cfg["spec"]]
+        one = replace(self.spec, n_layers=1)
+        self.one = one
+        w = init_weights(one, seed=0)
+        osp = OracleSpec(one.vocab, one.hidden, 1, one.n_q_heads, one.n_kv_heads, one.head_dim, one.ffn,
+                         one.rope_theta, one.rms_eps, one.qkv_bias)
+        self.B = cfg["batch"]
+        self.ctx = contexts_for(cfg, self.B)
+        self.dec = OracleDecoder(osp, w, max(self.ctx) + 64)
+        g = torch.Generator().manual_seed(7)
+        self.caches = [{"k": [torch.randn(c, one.n_kv_heads, one.head_dim, generator=g)],
+                        "v": [torch.randn(c, one.n_kv_heads, one.head_dim, generator=g)]} for c in self.ctx]
+        self.toks = [int(x) for x in torch.randint(0, one.vocab, (self.B,), generator=g)]
+        self.i = 0
+        self.sample = (f"oracle decode of the {self.B}-sequence mixed batch through 1 of {self.spec.n_layers} "
+                       f"layers + lm_head (fp32, batched GEMMs, per-sequence attention over ctx "
+                       f"{min(self.ctx)}-{max(self.ctx)}), time x{self.spec.n_layers} layers + lm_head")
+
+    def step(self) -> float:
+        """Seconds of one extrapolated full decode step."""
+        from oracle.decoder_ref import decode_batch_layers, rmsnorm
+
+        pos = [c + self.i for c in self.ctx]
+        self.i += 1
+        t0 = time.perf_counter()
+        resid = decode_batch_layers(self.dec, self.toks, pos, self.caches, range(1), lm_head=False)
+        t1 = time.perf_counter()
+        rmsnorm(resid, self.dec.w["final_norm"], self.one.rms_eps) @ self.dec.w["lm_head"].t()
+        t2 = time.perf_counter()
+        return self.spec.n_layers * (t1 - t0) + (t2 - t1)
+
+
+def cpu_baseline(cfg, steps=2, warmup=1):
+    o = CpuOracleStep(cfg)
+    ts = [o.step() for _ in range(warmup + steps)][warmup:]
+    t = statistics.median(ts)
+    return o.B / t, o.sample + f"; median of {steps}", o.threads, t
+
+
+def reference_arm(args, cfg):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    o = CpuOracleStep(cfg)
+    for _ in range(args.warmup):
+        o.step()
+    times = [o.step() for _ in range(args.steps)]
+    t = sum(times) / len(times)
+    value = o.B / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg["workload"],
+                   "impl": "CPU oracle port (oracle/decoder_ref.py; the reference has no decoder code)"},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": o.threads, "kind": "port", "sample": o.sample},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+def kernel_bytes(spec, B, ctx):
+    """Algorithmic bytes per launch of each kernel class (SURVEY.md §8(d) terms)."""
+    h, d = spec.hidden, spec.head_dim
+    qd, kd, f, V = spec.n_q_heads * d, spec.n_kv_heads * d, spec.ffn, spec.vocab
+
+    def wbytes(rows, k):
+        return rows * k // 2 + rows * (k // spec.group_size) * 2 if spec.weight_bits == 4 else rows * k * 2
+
+    kv_layer = sum(c + 1 for c in ctx) * 2 * kd * 2
+    return {
+        "gemm_qkv_rope_kv": wbytes(qd + 2 * kd, h) + B * h * 2 + B * (qd + 2 * kd) * 2,
+        "attention": kv_layer + B * qd * 2 + B * spec.n_q_heads * 8,
+        "attn_combine": B * qd * 2,
+        "gemm_o_resid": wbytes(h, qd) + B * qd * 2 + B * h * 8,
+        "gemm_gate_up_swiglu": wbytes(2 * f, h) + B * h * 2 + B * f * 2,
+        "gemm_down_resid": wbytes(h, f) + B * f * 2 + B * h * 8,
+        "gemm_lm_head_argmax": V * h * 2 + B * h * 2 + B * V * 4,
+        "rmsnorm": B * h * 6,
+        "embed_rmsnorm": B * h * 8,
+        "argmax": 0,
+    }
+
+
+def gpu_arm(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_02599_b200.kvpool import KvPool, pages_for
+    from paper_2603_02599_b200.modules import SharedDecodeModule, launch_count
+    from paper_2603_02599_b200.pricing import step_bytes
+    from paper_2603_02599_b200.spec import SPECS
+    from paper_2603_02599_b200.weights import DeviceWeights, init_weights
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    spec = SPECS[cfg["spec"]].with_bits(cfg["bits"]) if cfg["bits"] == 4 else SPECS[cfg["spec"]]
+    assign = build_assignment(cfg, world, args.routing)
+    mine = assign[rank]
+    B = len(mine)
+    ctx = contexts_for(cfg, B)
+    total_steps = args.warmup + args.steps
+    max_ctx = max(ctx) + total_steps + args.steps + 8
+
+    t0 = time.perf_counter()
+    w = init_weights(spec, seed=0, device=dev)
+    dw = DeviceWeights(spec, w, dev, max_ctx, free_source=True)
+    del w
+    kv = KvPool(spec, sum(pages_for(c + total_steps + args.steps + 2) for c in ctx) + 4, dev)
+    kv.fill_random_(seed=1000 + rank)
+    dec = SharedDecodeModule(spec, dw, kv, max_batch=B, max_context=max_ctx, use_pdl=not args.no_pdl)
+    # block tables: contiguous page runs per member
+    bt = torch.zeros(B, dec.max_pages, dtype=torch.int32)
+    nxt = 0
+    for i, c in enumerate(ctx):
+        n = pages_for(c + total_steps + args.steps + 2)
+        bt[i, :n] = torch.arange(nxt, nxt + n, dtype=torch.int32)
+        nxt += n
+    g = torch.Generator().manual_seed(11 + rank)
+    tokens0 = torch.randint(0, spec.vocab, (B,), generator=g, dtype=torch.int32)
+    dec.block_tables[:B].copy_(bt.to(dev))
+    dec.tokens[:B].copy_(tokens0.to(dev))
+    dec.positions[:B].copy_(torch.tensor(ctx, dtype=torch.int32).to(dev))
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+
+    graph = not args.no_graph
+    for _ in range(args.warmup):
+        dec.step_static(B, 0, graph=graph, feedback=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = launch_count()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    evs[0].record()
+    for i in range(args.steps):
+        dec.step_static(B, 0, graph=graph, feedback=True)
+        evs[i + 1].record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    total_ms = evs[0].elapsed_time(evs[-1])
+    t_max = torch.tensor([total_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    t_max = float(t_max.item())
+    tok_total = B * args.steps
+    tok_all = torch.tensor([float(tok_total)], device=dev)
+    if world > 1:
+        dist.all_reduce(tok_all)
+    value = float(tok_all.item()) / (t_max / 1e3)
+
+    # launches inside the timed region: graph replays do not pass through the
+    # library's host launch counter, so count the kernels of one captured step
+    per_step_launches = len(dec.kernel_names())
+    gpu_launches = per_step_launches * args.steps
+
+    # ---- per-kernel attribution (serialised, events after every launch) ----
+    pos_now = [c + args.warmup + args.steps for c in ctx]
+    prof = dec.profile(dec.tokens, dec.positions, dec.block_tables, B, dec.next_tokens, None, 0)
+    names = dec.kernel_names()
+    by = {}
+    for n_, ms in zip(names, prof):
+        t = by.setdefault(n_, [0.0, 0])
+        t[0] += ms
+        t[1] += 1
+    kb = kernel_bytes(spec, B, pos_now)
+    prof_total = sum(prof)
+    dominant = max((k for k in by if k in kb), key=lambda k: by[k][0])
+    dom_ms = by[dominant][0] / by[dominant][1]
+    peak, peak_kind = load_peaks()
+    achieved = kb[dominant] / (dom_ms / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(args.config, {}).get(dominant)
+    except Exception:
+        pass
+    ms_step = t_max / args.steps
+    sb = step_bytes(spec, [c + args.warmup for c in ctx])
+    step_gbs = sb / (ms_step / 1e3) / 1e9
+
+    # ---- e2e through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda t: t.pin_memory()  # noqa: E731
+        h_tok = pin(tokens0.clone())
+        h_bt = pin(bt.clone())
+        h_pos = pin(torch.tensor(pos_now, dtype=torch.int32))
+        out = pin(torch.zeros(B, dtype=torch.int32))
+        for i in range(2):  # warm the non-feedback graph
+            dec.decode(h_tok, h_pos, h_bt, graph=graph)
+            out.copy_(dec.next_tokens[:B])
+            h_pos += 1
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        te = time.perf_counter()
+        for i in range(args.steps):
+            nt = dec.decode(h_tok, h_pos, h_bt, graph=graph)
+            out.copy_(nt)  # D2H read of the step's result (synchronises)
+            h_tok.copy_(out)
+            h_pos += 1
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - te
+        t_e = torch.tensor([e2e_s], device=dev)
+        if world > 1:
+            dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
+        e2e = {"value": float(tok_all.item()) / float(t_e.item()), "unit": "tokens/s",
+               "h2d_bytes_per_step": int(h_tok.numel() * 4 + h_pos.numel() * 4 + h_bt.numel() * 4),
+               "d2h_bytes_per_step": int(out.numel() * 4),
+               "api": "SharedDecodeModule.decode(host pinned tokens/positions/block_tables) -> next tokens"}
+
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu:
+        v, sample, threads, _ = cpu_baseline(cfg, steps=2, warmup=1)
+        cpu = {"value": v, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16" if spec.weight_bits == 16 else "bf16 act / int4 weight",
+            "data": "synthetic: random-init weights N(0,0.02) seed 0, seeded on-device KV fill, poolsim Zipf trace seed 42",
+            "config": {"workload": cfg["workload"], "decoder": spec.name, "batch_per_gpu": B,
+                       "global_batch": int(tok_all.item()) // args.steps, "ctx_min": min(ctx), "ctx_max": max(ctx),
+                       "routing": args.routing, "parallelism": f"{world} shared decode workers (request-level DP)",
+                       "models_in_batch": sorted({m for _, m in mine}), "cuda_graph": graph,
+                       "pdl": not args.no_pdl,
+                       "l2": "inputs larger than L2 (weights + KV per step >> 126 MB), no explicit flush"},
+            "tokens_per_s_per_gpu": value / world,
+            "tpot_ms_p50": statistics.median(step_ms),
+            "hbm_gbps_step": step_gbs,
+            "step_bytes": sb,
+            "step_roofline_frac": step_gbs / peak,
+            "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "bytes_per_launch": kb[dominant], "avg_launch_ms": dom_ms},
+            "kernel_ms_per_step": {k: round(v[0], 4) for k, v in sorted(by.items(), key=lambda x: -x[1][0])},
+            "kernel_share": {k: round(v[0] / prof_total, 4) for k, v in by.items()},
+            "serialised_step_ms": prof_total,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk,
+            "gpu_launches": gpu_launches,
+            "setup_s": setup_s,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="sun", choices=["sun", "reference"])
+    ap.add_argument("--routing", default="lot", choices=["lot", "pinned"])
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-pdl", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        reference_arm(args, cfg)
+    else:
+        gpu_arm(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

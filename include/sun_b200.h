@@ -127,9 +127,23 @@ SunStatus sun_decoder_destroy(SunDecoder* dec);
  * pages_per_split: attention split-K granularity in pages (0 = automatic).
  * This is the operator that replaces costmodel.decode_step_time_from_totals
  * at engine.py:427-429. Errors: batch < 1 -> SUN_ERR_VALUE. */
+#define SUN_STEP_FEEDBACK 1 /* flags: also write tokens[b] = next_tokens[b], positions[b] += 1 on device */
 SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t* positions,
                           const int32_t* block_tables, int32_t bt_stride, int32_t batch,
-                          int32_t pages_per_split, float* logits, int32_t* next_tokens, void* stream);
+                          int32_t pages_per_split, float* logits, int32_t* next_tokens, int32_t flags,
+                          void* stream);
+
+/* Same step, serialised, with a CUDA event after every kernel: kernel_ms[i] is the
+ * device time of the i-th launch (order: embed+norm, then per layer [norm], qkv,
+ * attention, combine, o, norm, gate_up, down; final norm, lm_head, argmax).
+ * Synchronises the stream. For measurement only. */
+SunStatus sun_decode_step_profile(SunDecoder* dec, const int32_t* tokens, const int32_t* positions,
+                                  const int32_t* block_tables, int32_t bt_stride, int32_t batch,
+                                  int32_t pages_per_split, float* logits, int32_t* next_tokens, void* stream,
+                                  float* kernel_ms, int32_t capacity, int32_t* n_kernels);
+
+/* Number of kernels this thread has launched through the library so far. */
+SunStatus sun_launch_count(int64_t* launches);
 
 /* ---- kernel-level entry points (unit parity tests; same kernels as the step) ---- */
 

@@ -201,3 +201,43 @@ def teacher_forced(prefills: list[OracleDecoder], decoder: OracleDecoder, prompt
             rows.append(lg)
         out.append(torch.stack(rows))
     return out
+
+
+def decode_batch_layers(dec: OracleDecoder, tokens: list[int], positions: list[int], caches: list[dict],
+                        layers: range, lm_head: bool = True):
+    """Batched CPU decode step (the timed CPU baseline): the linear layers run on
+    the whole [B, h] batch (weights streamed once per step, like the GPU path),
+    attention per sequence over its own cache. ``layers`` may be a subset (the
+    bench's bounded sample); caches hold K/V [ctx, nkv, d] per layer index.
+    Returns logits [B, V] (or the residual stream if lm_head=False)."""
+    s, w = dec.s, dec.w
+    d, nq, nkv = s.head_dim, s.n_q_heads, s.n_kv_heads
+    G = nq // nkv
+    B = len(tokens)
+    pos = torch.tensor(positions)
+    resid = w["embed"][torch.tensor(tokens)].clone()
+    for l in layers:
+        xn = rmsnorm(resid, w[f"l{l}.attn_norm"], s.rms_eps)
+        q, k, v = xn @ w[f"l{l}.wq"].t(), xn @ w[f"l{l}.wk"].t(), xn @ w[f"l{l}.wv"].t()
+        if s.qkv_bias:
+            q, k, v = q + w[f"l{l}.bq"], k + w[f"l{l}.bk"], v + w[f"l{l}.bv"]
+        cs, sn = dec.cos[pos][:, None, :], dec.sin[pos][:, None, :]
+        q = bf(rope(q.view(B, nq, d), cs, sn))
+        k = bf(rope(k.view(B, nkv, d), cs, sn))
+        v = bf(v.view(B, nkv, d))
+        out = torch.empty(B, nq, d)
+        for b in range(B):
+            K = torch.cat([caches[b]["k"][l], k[b:b + 1]])
+            V = torch.cat([caches[b]["v"][l], v[b:b + 1]])
+            caches[b]["k"][l], caches[b]["v"][l] = K, V
+            qg = q[b].view(nkv, G, d)
+            sc = torch.einsum("hgd,thd->hgt", qg, K) / math.sqrt(d)
+            out[b] = torch.einsum("hgt,thd->hgd", torch.softmax(sc, -1), V).reshape(nq, d)
+        attn = bf(out.reshape(B, nq * d))
+        resid = resid + attn @ w[f"l{l}.wo"].t()
+        xn = rmsnorm(resid, w[f"l{l}.ffn_norm"], s.rms_eps)
+        g, u = xn @ w[f"l{l}.wg"].t(), xn @ w[f"l{l}.wu"].t()
+        resid = resid + bf(g / (1.0 + torch.exp(-g)) * u) @ w[f"l{l}.wd"].t()
+    if not lm_head:
+        return resid
+    return rmsnorm(resid, w["final_norm"], s.rms_eps) @ w["lm_head"].t()

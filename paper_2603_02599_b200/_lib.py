@@ -28,6 +28,7 @@ SUN_ERR_MIXED_DECODER = 2
 SUN_ERR_UNSUPPORTED = 3
 SUN_ERR_CUDA = 4
 SUN_ERR_CAPACITY = 5
+SUN_STEP_FEEDBACK = 1
 
 
 class SunDecoderDims(ctypes.Structure):
@@ -66,7 +67,10 @@ SIGNATURES = {
     "sun_decoder_create": (c_i32, [ctypes.POINTER(SunDecoderDims), ctypes.POINTER(SunWeights),
                                    ctypes.POINTER(SunKvPool), c_vp, c_size, c_i32, c_i32, ctypes.POINTER(c_vp)]),
     "sun_decoder_destroy": (c_i32, [c_vp]),
-    "sun_decode_step": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp]),
+    "sun_decode_step": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_i32, c_vp]),
+    "sun_decode_step_profile": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp,
+                                        ctypes.POINTER(c_f32), c_i32, ctypes.POINTER(c_i32)]),
+    "sun_launch_count": (c_i32, [ctypes.POINTER(c_i64)]),
     "sun_gemm_workspace_bytes": (c_i32, [c_i64, c_i64, c_i32, ctypes.POINTER(c_size)]),
     "sun_gemm_bf16": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i32, c_vp, c_i64, c_i32, c_vp,
                               c_size, c_vp]),

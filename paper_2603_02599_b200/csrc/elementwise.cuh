@@ -59,10 +59,11 @@ __global__ void __launch_bounds__(kRowThreads)
   pdl_launch_dependents();
 }
 
-// next[b] = argmax over lm_head tiles (ties -> lowest vocabulary index).
+// next[b] = argmax over lm_head tiles (ties -> lowest vocabulary index). With
+// feedback, also tokens[b] = next[b] and positions[b] += 1 (graph-replayable loop).
 __global__ void __launch_bounds__(kRowThreads)
     argmax_reduce_kernel(const float* __restrict__ val, const int* __restrict__ idx, int m_tiles, int bn,
-                         int* __restrict__ next) {
+                         int* __restrict__ next, int* __restrict__ feedback_tokens, int* __restrict__ positions) {
   __shared__ float sv[kRowThreads / 32];
   __shared__ int si[kRowThreads / 32];
   pdl_wait();
@@ -99,6 +100,10 @@ __global__ void __launch_bounds__(kRowThreads)
       }
     }
     next[b] = bi;
+    if (feedback_tokens != nullptr) {  // device-resident autoregressive loop
+      feedback_tokens[b] = bi;
+      positions[b] += 1;
+    }
   }
   pdl_launch_dependents();
 }

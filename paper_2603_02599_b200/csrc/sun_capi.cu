@@ -152,8 +152,8 @@ void init_kernel_attrs() {
 }
 
 template <typename... KArgs, typename... Args>
-cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
-                   Args&&... args) {
+cudaError_t launch_raw(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
+                       Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -165,6 +165,31 @@ cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, c
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// Per-thread launch accounting + optional per-kernel event timing (profile mode).
+struct LaunchTrace {
+  long long launches = 0;
+  std::vector<cudaEvent_t>* events = nullptr;  // record one event after each launch
+};
+thread_local LaunchTrace g_trace;
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
+                   Args&&... args) {
+  cudaError_t e = launch_raw(kern, grid, block, smem, st, pdl, std::forward<Args>(args)...);
+  if (e == cudaSuccess) {
+    ++g_trace.launches;
+    if (g_trace.events) {
+      cudaEvent_t ev;
+      e = cudaEventCreate(&ev);
+      if (e == cudaSuccess) {
+        g_trace.events->push_back(ev);
+        e = cudaEventRecord(ev, st);
+      }
+    }
+  }
+  return e;
 }
 
 // Workspace layout shared by sizing and creation.
@@ -443,7 +468,8 @@ SunStatus sun_decoder_destroy(SunDecoder* dec) {
 
 SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t* positions,
                           const int32_t* block_tables, int32_t bt_stride, int32_t batch,
-                          int32_t pages_per_split, float* logits, int32_t* next_tokens, void* stream) {
+                          int32_t pages_per_split, float* logits, int32_t* next_tokens, int32_t flags,
+                          void* stream) {
   if (!dec) return fail(SUN_ERR_VALUE, "null decoder");
   if (batch < 1) return fail(SUN_ERR_VALUE, "decode batch must be non-empty");
   if (batch > dec->max_batch) return fail(SUN_ERR_CAPACITY, "batch %d > max_batch %d", batch, dec->max_batch);
@@ -548,7 +574,46 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
   a.amax_idx = dec->amax_idx;
   if ((s = run_gemm<EPI_LOGITS>(dec->tm_lm, xm->xn, a, dec->p_lm, st, pdl)) != SUN_OK) return s;
   SUN_CUDA(launch(argmax_reduce_kernel, dim3(batch), dim3(kRowThreads), 0, st, pdl, (const float*)dec->amax_val,
-                  (const int*)dec->amax_idx, dec->p_lm.m_tiles, bn, next_tokens));
+                  (const int*)dec->amax_idx, dec->p_lm.m_tiles, bn, next_tokens,
+                  (flags & SUN_STEP_FEEDBACK) ? const_cast<int*>(tokens) : (int*)nullptr,
+                  const_cast<int*>(positions)));
+  return SUN_OK;
+}
+
+SunStatus sun_launch_count(int64_t* launches) {
+  if (!launches) return fail(SUN_ERR_VALUE, "null argument");
+  *launches = g_trace.launches;
+  return SUN_OK;
+}
+
+SunStatus sun_decode_step_profile(SunDecoder* dec, const int32_t* tokens, const int32_t* positions,
+                                  const int32_t* block_tables, int32_t bt_stride, int32_t batch,
+                                  int32_t pages_per_split, float* logits, int32_t* next_tokens, void* stream,
+                                  float* kernel_ms, int32_t capacity, int32_t* n_kernels) {
+  if (!dec || !kernel_ms || !n_kernels) return fail(SUN_ERR_VALUE, "null argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  std::vector<cudaEvent_t> evs;
+  cudaEvent_t start;
+  SUN_CUDA(cudaEventCreate(&start));
+  SUN_CUDA(cudaEventRecord(start, st));
+  const bool pdl = dec->pdl;
+  dec->pdl = false;  // serialise kernels so event deltas attribute time to one kernel
+  g_trace.events = &evs;
+  SunStatus s = sun_decode_step(dec, tokens, positions, block_tables, bt_stride, batch, pages_per_split, logits,
+                                next_tokens, 0, stream);
+  g_trace.events = nullptr;
+  dec->pdl = pdl;
+  if (s != SUN_OK) return s;
+  SUN_CUDA(cudaStreamSynchronize(st));
+  const int n = int(evs.size());
+  *n_kernels = n;
+  cudaEvent_t prev = start;
+  for (int i = 0; i < n && i < capacity; ++i) {
+    SUN_CUDA(cudaEventElapsedTime(&kernel_ms[i], prev, evs[i]));
+    prev = evs[i];
+  }
+  cudaEventDestroy(start);
+  for (auto e : evs) cudaEventDestroy(e);
   return SUN_OK;
 }
 

@@ -54,8 +54,12 @@ class _StepRunner:
             self._h = None
 
     def launch(self, tokens: torch.Tensor, positions: torch.Tensor, block_tables: torch.Tensor, batch: int,
-               next_tokens: torch.Tensor, logits: torch.Tensor | None = None, pages_per_split: int = 0) -> None:
-        """Enqueue one decode step on the current stream (all tensors on device)."""
+               next_tokens: torch.Tensor, logits: torch.Tensor | None = None, pages_per_split: int = 0,
+               feedback: bool = False) -> None:
+        """Enqueue one decode step on the current stream (all tensors on device).
+
+        feedback=True also writes the sampled tokens back into ``tokens`` and
+        advances ``positions`` on the device (autoregressive loop without host)."""
         if batch < 1:
             raise ValueError("decode batch must be non-empty")
         if block_tables.shape[1] < 1 or block_tables.dtype != torch.int32:
@@ -63,8 +67,37 @@ class _StepRunner:
         st = torch.cuda.current_stream().cuda_stream
         _lib.check(self._lib.sun_decode_step(
             self._h, tokens.data_ptr(), positions.data_ptr(), block_tables.data_ptr(), block_tables.stride(0), batch,
-            pages_per_split, None if logits is None else logits.data_ptr(), next_tokens.data_ptr(), st),
-            "sun_decode_step")
+            pages_per_split, None if logits is None else logits.data_ptr(), next_tokens.data_ptr(),
+            _lib.SUN_STEP_FEEDBACK if feedback else 0, st), "sun_decode_step")
+
+    def profile(self, tokens, positions, block_tables, batch, next_tokens, logits=None, pages_per_split=0):
+        """Serialised step with a CUDA event after every kernel -> per-launch device ms."""
+        cap = 16 + 16 * self.spec.n_layers
+        buf = (ctypes.c_float * cap)()
+        n = ctypes.c_int32()
+        st = torch.cuda.current_stream().cuda_stream
+        _lib.check(self._lib.sun_decode_step_profile(
+            self._h, tokens.data_ptr(), positions.data_ptr(), block_tables.data_ptr(), block_tables.stride(0), batch,
+            pages_per_split, None if logits is None else logits.data_ptr(), next_tokens.data_ptr(), st, buf, cap,
+            ctypes.byref(n)), "sun_decode_step_profile")
+        return [buf[i] for i in range(min(n.value, cap))]
+
+    def kernel_names(self) -> list[str]:
+        """Launch order of one step (matches sun_decode_step)."""
+        names = ["embed_rmsnorm"]
+        for l in range(self.spec.n_layers):
+            if l > 0:
+                names.append("rmsnorm")
+            names += ["gemm_qkv_rope_kv", "attention", "attn_combine", "gemm_o_resid", "rmsnorm",
+                      "gemm_gate_up_swiglu", "gemm_down_resid"]
+        return names + ["rmsnorm", "gemm_lm_head_argmax", "argmax"]
+
+
+def launch_count() -> int:
+    """Kernels launched by libsun_b200.so on this thread so far."""
+    n = ctypes.c_int64()
+    _lib.check(_lib.load().sun_launch_count(ctypes.byref(n)), "sun_launch_count")
+    return n.value
 
 
 class SharedDecodeModule(_StepRunner):
@@ -83,28 +116,31 @@ class SharedDecodeModule(_StepRunner):
         self.block_tables = torch.zeros(self.max_batch, self.max_pages, dtype=torch.int32, device=dev)
         self.next_tokens = torch.zeros(self.max_batch, dtype=torch.int32, device=dev)
         self.logits = torch.zeros(self.max_batch, spec.vocab, dtype=torch.float32, device=dev) if keep_logits else None
-        self._graphs: dict[tuple[int, int], torch.cuda.CUDAGraph] = {}
+        self._graphs: dict[tuple, torch.cuda.CUDAGraph] = {}
 
-    def step_static(self, batch: int, pages_per_split: int = 0, graph: bool = True) -> None:
+    def step_static(self, batch: int, pages_per_split: int = 0, graph: bool = True, feedback: bool = False) -> None:
         """One step over the static buffers' first ``batch`` rows (device-resident inputs)."""
         if not graph:
             self.launch(self.tokens, self.positions, self.block_tables, batch, self.next_tokens, self.logits,
-                        pages_per_split)
+                        pages_per_split, feedback)
             return
-        key = (batch, pages_per_split)
+        key = (batch, pages_per_split, feedback)
         g = self._graphs.get(key)
         if g is None:
             # warm (TMA descriptor cache for this batch bucket) then capture
             s = torch.cuda.Stream()
             s.wait_stream(torch.cuda.current_stream())
+            saved = (self.tokens.clone(), self.positions.clone())
             with torch.cuda.stream(s):
                 self.launch(self.tokens, self.positions, self.block_tables, batch, self.next_tokens, self.logits,
-                            pages_per_split)
+                            pages_per_split, feedback)
             torch.cuda.current_stream().wait_stream(s)
+            self.tokens.copy_(saved[0])
+            self.positions.copy_(saved[1])
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 self.launch(self.tokens, self.positions, self.block_tables, batch, self.next_tokens, self.logits,
-                            pages_per_split)
+                            pages_per_split, feedback)
             self._graphs[key] = g
         g.replay()
 
