@@ -61,7 +61,15 @@ typedef struct SunDecoderDims {
   float rms_eps;
 } SunDecoderDims;
 
-/* Device pointers of one decoder layer (bf16 unless stated).
+/* SUN-BLK weight layout (bf16 linear layers and the lm_head as passed to the
+ * decoder and sun_gemm_bf16): W[rows][k] is stored as [ceil(rows/128)]
+ * [ceil(k/64)] blocks of 128 x 64 elements, each block 16 KB contiguous with the
+ * 16-byte chunk c of row r at chunk position c ^ (r & 7) (the SWIZZLE_128B shared
+ * memory image), zero padded. Every pipeline stage is then one linear bulk copy. */
+SunStatus sun_blocked_bytes(int64_t rows, int64_t k, size_t* bytes);
+SunStatus sun_block_weights_bf16(const void* w, int64_t rows, int64_t k, void* out, void* stream);
+
+/* Device pointers of one decoder layer (bf16 unless stated; matrices in SUN-BLK).
  *  w_qkv      [(nq + 2 nkv) * d][hidden]           rows: q heads, k heads, v heads
  *  w_o        [hidden][nq * d]
  *  w_gate_up  [ceil(f/64) * 128][hidden]           64-row blocks: gate rows j..j+63 then
@@ -86,7 +94,7 @@ typedef struct SunLayerWeights {
 typedef struct SunWeights {
   const void* embed;       /* [vocab][hidden] */
   const void* final_norm;  /* [hidden] */
-  const void* lm_head;     /* [vocab][hidden], bf16 always */
+  const void* lm_head;     /* [vocab][hidden] SUN-BLK, bf16 always */
   const float* rope_cos;   /* [max_context][head_dim/2] fp32 */
   const float* rope_sin;
   const SunLayerWeights* layers; /* host array, n_layers entries */
@@ -147,13 +155,26 @@ SunStatus sun_launch_count(int64_t* launches);
 
 /* ---- kernel-level entry points (unit parity tests; same kernels as the step) ---- */
 
-/* out[b][n] (=|+=) sum_k w[n][k] * x[b][k] for b < batch, bf16 in, fp32 out,
- * tcgen05 swap-AB GEMM. x has x_rows >= round_up(batch,16) allocated rows of
+/* out[b][n] (=|+=) sum_k w[n][k] * x[b][k] for b < batch, bf16 in (w in SUN-BLK),
+ * fp32 out, tcgen05 swap-AB GEMM. x has x_rows >= round_up(batch,16) allocated rows of
  * stride ldx elements. workspace >= sun_gemm_workspace_bytes(...), zeroed once. */
 SunStatus sun_gemm_workspace_bytes(int64_t n_out, int64_t k, int32_t batch, size_t* bytes);
 SunStatus sun_gemm_bf16(const void* w, int64_t n_out, int64_t k, const void* x, int64_t ldx, int64_t x_rows,
                         int32_t batch, float* out, int64_t ldo, int32_t accumulate, void* workspace,
                         size_t workspace_bytes, void* stream);
+
+/* sun_gemm_bf16 with per-CTA %globaltimer stamps (stamps: uint64 [148][8]; slots:
+ * 0 start, 1 setup done, 2 first stage landed, 3 last MMA issued, 4 first
+ * accumulator ready, 5 epilogue done, 6 exit). Profiling aid. */
+SunStatus sun_gemm_bf16_stamped(const void* w, int64_t n_out, int64_t k, const void* x, int64_t ldx,
+                                int64_t x_rows, int32_t batch, float* out, int64_t ldo, int32_t accumulate,
+                                void* workspace, size_t workspace_bytes, void* stream, uint64_t* stamps);
+
+/* Same with QSUN SUN-W4 weights (packed int4 + bf16 group scales, see gemm_w4.cuh),
+ * dequantised in-kernel to bf16 tcgen05 operands. k must be a multiple of 128. */
+SunStatus sun_gemm_w4(const void* packed, const void* scales, int64_t n_out, int64_t k, const void* x, int64_t ldx,
+                      int64_t x_rows, int32_t batch, float* out, int64_t ldo, int32_t accumulate, void* workspace,
+                      size_t workspace_bytes, void* stream);
 
 /* Paged split-K decode attention for one layer: q bf16 [batch][nq][d] (post-RoPE),
  * KV from the pool, out bf16 [batch][nq*d]. */

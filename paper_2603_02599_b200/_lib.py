@@ -74,8 +74,14 @@ SIGNATURES = {
     "sun_gemm_workspace_bytes": (c_i32, [c_i64, c_i64, c_i32, ctypes.POINTER(c_size)]),
     "sun_gemm_bf16": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i32, c_vp, c_i64, c_i32, c_vp,
                               c_size, c_vp]),
+    "sun_gemm_bf16_stamped": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i32, c_vp, c_i64, c_i32, c_vp,
+                                      c_size, c_vp, c_vp]),
+    "sun_gemm_w4": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i32, c_vp, c_i64, c_i32, c_vp,
+                            c_size, c_vp]),
     "sun_attention_decode": (c_i32, [ctypes.POINTER(SunDecoderDims), ctypes.POINTER(SunKvPool), c_i32, c_vp,
                                      c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_size, c_vp]),
+    "sun_blocked_bytes": (c_i32, [c_i64, c_i64, ctypes.POINTER(c_size)]),
+    "sun_block_weights_bf16": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_vp]),
     "sun_rmsnorm": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_f32, c_vp]),
     "sun_quantize_w4": (c_i32, [c_vp, c_i64, c_i64, c_i32, c_vp, c_vp, c_vp]),
 }

@@ -12,7 +12,7 @@
 // Replaces the KV term `sum(resident_tokens * kv_bytes_per_token)` of the
 // reference step price (poolsim costmodel.py:112, 139; engine.py:427-428).
 #pragma once
-#include "sun_common.cuh"
+#include "gemm_tc.cuh"  // act_offset (SUN-ACT layout)
 
 namespace sun {
 
@@ -33,6 +33,7 @@ struct AttnArgs {
   float* part_ml;          // [B][n_q_heads][max_splits][2]
   __nv_bfloat16* out;      // [B][n_q_heads * D]   (combine output)
   long long ld_out;
+  int act_rows;            // > 0: write `out` in SUN-ACT (the O-projection operand)
 };
 
 template <int D>
@@ -262,7 +263,11 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(const AttnArgs a) {
       acc += a.part_o[(u0 + s) * D + dim] * sc;
       ll += a.part_ml[(u0 + s) * 2 + 1] * sc;
     }
-    a.out[static_cast<long long>(b) * a.ld_out + head * D + dim] = __float2bfloat16_rn(acc / ll);
+    const __nv_bfloat16 o = __float2bfloat16_rn(acc / ll);
+    if (a.act_rows > 0)
+      *reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<uint8_t*>(a.out) + act_offset(b, head * D + dim, a.act_rows)) = o;
+    else
+      a.out[static_cast<long long>(b) * a.ld_out + head * D + dim] = o;
   }
   pdl_launch_dependents();
 }

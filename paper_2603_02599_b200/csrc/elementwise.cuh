@@ -2,7 +2,7 @@
 // the first RMSNorm, RMSNorm producing the bf16 GEMM operand, and the final
 // greedy argmax over the lm_head tiles' (max, index) partials.
 #pragma once
-#include "sun_common.cuh"
+#include "gemm_tc.cuh"  // act_offset (SUN-ACT layout)
 
 namespace sun {
 
@@ -22,10 +22,12 @@ SUN_DEVICE float block_sum(float v, float* red) {
 // y = bf16(x * rsqrt(mean(x^2) + eps) * w), fp32 math, one rounding.
 // If `tokens` is non-null the row is first gathered from the embedding table
 // into the fp32 residual stream (x := float(embed[token])).
+// act_rows > 0: the output goes to the SUN-ACT layout the GEMMs stream
+// (gemm_tc.cuh), otherwise row-major with stride ld_out.
 __global__ void __launch_bounds__(kRowThreads)
     rmsnorm_kernel(const int* __restrict__ tokens, const __nv_bfloat16* __restrict__ embed,
                    float* __restrict__ resid, const __nv_bfloat16* __restrict__ w,
-                   __nv_bfloat16* __restrict__ out, int h, long long ld_out, float eps) {
+                   __nv_bfloat16* __restrict__ out, int h, long long ld_out, float eps, int act_rows) {
   __shared__ float red[kRowThreads / 32];
   pdl_wait();
   const int b = blockIdx.x;
@@ -53,8 +55,11 @@ __global__ void __launch_bounds__(kRowThreads)
     const __nv_bfloat162 w23 = *reinterpret_cast<const __nv_bfloat162*>(w + i + 2);
     __nv_bfloat162 o01 = __floats2bfloat162_rn(v.x * r * __bfloat162float(w01.x), v.y * r * __bfloat162float(w01.y));
     __nv_bfloat162 o23 = __floats2bfloat162_rn(v.z * r * __bfloat162float(w23.x), v.w * r * __bfloat162float(w23.y));
-    *reinterpret_cast<__nv_bfloat162*>(y + i) = o01;
-    *reinterpret_cast<__nv_bfloat162*>(y + i + 2) = o23;
+    __nv_bfloat16* dst = act_rows > 0 ? reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<uint8_t*>(out) +
+                                                                         act_offset(b, i, act_rows))
+                                      : y + i;
+    *reinterpret_cast<__nv_bfloat162*>(dst) = o01;  // 4 consecutive columns stay in one 16-byte chunk
+    *reinterpret_cast<__nv_bfloat162*>(dst + 2) = o23;
   }
   pdl_launch_dependents();
 }

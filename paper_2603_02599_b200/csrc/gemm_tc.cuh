@@ -3,12 +3,27 @@
 //   D^T[n_out, B] = W[n_out, K] . X[B, K]^T
 //
 // Weight rows are the MMA M dimension (128 per tile), the cross-model decode
-// batch is the MMA N dimension (bn = round_up(B, 16) <= 256), K is streamed in
-// 64-element (128 B, SWIZZLE_128B) blocks by TMA through an mbarrier ring.
-// Warp roles: warp 0 = TMA producer, warp 1 = TMEM allocator + single-thread
-// MMA issuer, warps 2..5 = epilogue (TMEM -> registers -> fused epilogue).
-// Split-K across CTAs is reduced deterministically by the last-arriving CTA of
-// each tile (fixed split order), so results are run-to-run bit-identical.
+// batch is the MMA N dimension (bn = round_up(B, 16) <= 256). K advances 128 per
+// pipeline stage (two 64-wide SWIZZLE_128B atoms). Both operands are stored in
+// the exact shared-memory image the UMMA descriptors expect, so every stage is
+// two linear cp.async.bulk copies (one 32 KB weight run, one activation run):
+//   * SUN-BLK weights: [m_tiles][k/64][128 rows][64 cols] with 16-byte chunk c of
+//     row r at position c ^ (r & 7) — a tile's whole K is one sequential stream;
+//   * SUN-ACT activations: [k/64][bn rows][64 cols], same swizzle, written in
+//     that form by the kernels that produce them (RMSNorm, attention combine,
+//     SwiGLU epilogue).
+// Per-request cost dominates small TMA boxes on B200 (a 4 KB bulk stream reaches
+// ~2.3 TB/s, 16 KB 6.3, 64 KB 7.2; scripts/probe/stream_probe.cu), hence the
+// large linear requests. QSUN W4 stages bring packed int4 + scales instead and
+// converter warps dequantise into a bf16 SW128 tile (gemm_w4.cuh).
+//
+// Schedules: with <= 148 tiles the S CTAs of a thread-block cluster split K for
+// one tile and reduce through DSMEM in fixed rank order (deterministic, one
+// wave, no global partials); with more tiles one persistent CTA per SM walks a
+// contiguous range of whole tiles with a double-buffered TMEM accumulator so a
+// tile's epilogue overlaps the next tile's stream. Warp roles: 0 = producer,
+// 1 = TMEM owner + single-thread MMA issuer, 2..5 = epilogue, 6..9 = W4
+// converters. Every kernel prefetches its weights before griddepcontrol.wait.
 //
 // Replaces the weight term `decoder_weight_bytes / (mbu * hbm_bandwidth)` of
 // the reference's step price (poolsim costmodel.py:101-113) with real work.
@@ -26,21 +41,23 @@ enum EpiKind : int {
 };
 
 struct GemmArgs {
+  const uint8_t* wblk;     // bf16 weights, SUN-BLK
+  const uint8_t* w4_packed;  // QSUN: SUN-W4 packed int4 (tile-contiguous 128x64 B blocks)
+  const __nv_bfloat16* w4_scales;  // QSUN: [k/128][m_tiles*128]
+  const uint8_t* xact;     // activations, SUN-ACT with bn rows per atom
   int n_out;         // rows of W (incl. zero padding rows for SWIGLU)
   int k;             // reduction length
   int batch;         // valid batch columns
   int bn;            // padded N: multiple of 16, <= 256
-  int kb_total;      // ceil(k / 64)
-  int kb_per_split;  // k-blocks handled by one CTA
-  int splits;        // gridDim.y
+  int kb64;          // ceil(k / 64): 64-wide k blocks per tile
+  int ksteps;        // ceil(kb64 / 2): 128-wide pipeline stages per tile
+  int m_tiles;       // ceil(n_out / 128)
+  int splits;        // cluster split-K factor S (> 1: cluster schedule)
   int stages;        // smem pipeline depth
-  int weight_bits;   // 16 (bf16) — 4 handled by the W4 kernel
-  float* partial;    // [m_tiles][splits][bn][128] fp32 (splits > 1)
-  unsigned* counters;  // [m_tiles], zero-initialised, self-resetting
   // STORE / RESID / LOGITS
   float* out_f32;
   long long ldo;
-  // SWIGLU (act) / QKV (q)
+  // SWIGLU (act, written SUN-ACT with bn rows) / QKV (q, row-major with ldb)
   __nv_bfloat16* out_bf16;
   long long ldb;
   int n_valid_out;   // SWIGLU: ffn width f (outputs j < f are written)
@@ -61,16 +78,46 @@ struct GemmArgs {
   // LOGITS
   float* amax_val;  // [m_tiles][bn]
   int* amax_idx;    // [m_tiles][bn]
+  // optional per-CTA %globaltimer stamps [gridDim.x][8] (profiling only)
+  unsigned long long* stamps;
 };
 
+SUN_DEVICE unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SUN_STAMP(i) \
+  do { if (a.stamps) a.stamps[blockIdx.x * 8 + (i)] = gtimer(); } while (0)
+
 constexpr int kGemmThreads = 192;
+constexpr int kW4Threads = 320;
 constexpr int kTileM = 128;
 constexpr int kTileK = 64;
-constexpr uint32_t kTileWBytes = kTileM * kTileK * 2;  // 16 KB
-constexpr uint32_t kTmemCols = 256;
+constexpr uint32_t kTileWBytes = kTileM * kTileK * 2;  // 16 KB: one SUN-BLK block
+constexpr uint32_t kW4PackedBytes = kTileM * 128 / 2;  // 8 KB: one SUN-W4 block (128 x 128)
+constexpr uint32_t kW4DeqBytes = kTileM * 128 * 2;     // 32 KB dequantised bf16 tile
 
-__host__ __device__ inline size_t gemm_smem_bytes(int bn, int stages) {
-  return 1024 + static_cast<size_t>(stages) * (kTileWBytes + bn * 128) + 256;
+constexpr uint32_t kEpiSmemBytes = 16 * kTileM * 4 + 512 + 2048 + 512;  // partner staging, argmax scratch, column meta
+
+// byte offset of activation element (row b, column k) in SUN-ACT with `rows` rows per atom
+__host__ __device__ inline long long act_offset(int b, long long k, int rows) {
+  return (k >> 6) * (static_cast<long long>(rows) * 128) + static_cast<long long>(b) * 128 +
+         (((((k & 63) >> 3) ^ (b & 7))) << 4) + (k & 7) * 2;
+}
+
+__host__ __device__ inline uint32_t gemm_stage_bytes(int bn, bool w4) {
+  return (w4 ? kW4PackedBytes + 1024u : 2u * kTileWBytes) + static_cast<uint32_t>(bn) * 256u;
+}
+__host__ __device__ inline size_t gemm_smem_bytes(int bn, int stages, bool w4) {
+  return 1024 + (w4 ? 2 * size_t(kW4DeqBytes) : 0) + static_cast<size_t>(stages) * gemm_stage_bytes(bn, w4) +
+         kEpiSmemBytes + 512;
+}
+
+__host__ __device__ inline uint32_t tmem_cols_for(int bn) {
+  uint32_t c = 32;
+  while (c < static_cast<uint32_t>(2 * bn)) c <<= 1;
+  return c;
 }
 
 SUN_DEVICE void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
@@ -82,14 +129,19 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
   const int B = a.batch;
   if constexpr (EPI == EPI_STORE_F32 || EPI == EPI_RESID_ADD) {
     if (row < a.n_out) {
+      float* base = a.out_f32 + static_cast<long long>(c0) * a.ldo + row;
+      if constexpr (EPI == EPI_RESID_ADD) {
+        // issue all 16 residual loads before any store (one memory round trip)
+        float old[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int b = c0 + j;
-        if (b < B) {
-          float* p = a.out_f32 + static_cast<long long>(b) * a.ldo + row;
-          if constexpr (EPI == EPI_RESID_ADD) *p += v[j];
-          else *p = v[j];
-        }
+        for (int j = 0; j < 16; ++j) old[j] = (c0 + j < B) ? base[j * a.ldo] : 0.f;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (c0 + j < B) base[j * a.ldo] = old[j] + v[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (c0 + j < B) base[j * a.ldo] = v[j];
       }
     }
   } else if constexpr (EPI == EPI_LOGITS) {
@@ -159,7 +211,8 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
               const float g = v[j];
               const float u = stage_f32[j * kTileM + row_local + 64];
               const float s = g / (1.f + expf(-g));
-              a.out_bf16[static_cast<long long>(b) * a.ldb + jo] = __float2bfloat16_rn(s * u);
+              *reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<uint8_t*>(a.out_bf16) + act_offset(b, jo, a.bn)) =
+                  __float2bfloat16_rn(s * u);
             }
           }
         }
@@ -174,30 +227,39 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
         const int fi = i < half ? i : i - half;
         const int partner = i < half ? row_local + half : row_local - half;
         const bool is_v = row >= qd + kd;
-#pragma unroll 4
+        const int* meta = reinterpret_cast<const int*>(red_idx + 64);  // [0,256) pos, [256,512) page
+        // hoisted, independent loads: one round trip for the 32 table values
+        float cs[16], sn[16], pv[16];
+#pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const int b = c0 + j;
-          if (b >= B) break;
-          const int pos = a.positions[b];
-          float o = v[j];
-          if (!is_v) {
-            const float pv = stage_f32[j * kTileM + partner];
-            const float cs = a.rope_cos[static_cast<long long>(pos) * half + fi];
-            const float sn = a.rope_sin[static_cast<long long>(pos) * half + fi];
-            o = i < half ? (v[j] * cs - pv * sn) : (v[j] * cs + pv * sn);
+          const int pos = meta[(c0 + j) & 255];
+          const bool ok = !is_v && (c0 + j < B);
+          cs[j] = ok ? a.rope_cos[static_cast<long long>(pos) * half + fi] : 1.f;
+          sn[j] = ok ? a.rope_sin[static_cast<long long>(pos) * half + fi] : 0.f;
+          pv[j] = stage_f32[j * kTileM + partner];
+        }
+        const bool lo_half = i < half;
+        if (row < qd) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (c0 + j < B) {
+              const float o = lo_half ? (v[j] * cs[j] - pv[j] * sn[j]) : (v[j] * cs[j] + pv[j] * sn[j]);
+              a.out_bf16[static_cast<long long>(c0 + j) * a.ldb + row] = __float2bfloat16_rn(o);
+            }
           }
-          const __nv_bfloat16 ob = __float2bfloat16_rn(o);
-          if (row < qd) {
-            a.out_bf16[static_cast<long long>(b) * a.ldb + row] = ob;
-          } else {
-            const int kvsel = is_v ? 1 : 0;
-            const int g = (row - qd - kvsel * kd) / d;
-            const int page = a.block_tables[static_cast<long long>(b) * a.bt_stride + pos / a.page_size];
-            const int slot = pos % a.page_size;
-            const long long off =
-                static_cast<long long>(page) * a.page_stride +
-                ((static_cast<long long>(a.layer * 2 + kvsel) * a.n_kv_heads + g) * a.page_size + slot) * d + i;
-            a.kv_base[off] = ob;
+        } else {
+          const int kvsel = is_v ? 1 : 0;
+          const int g = (row - qd - kvsel * kd) / d;
+          const long long inner = ((static_cast<long long>(a.layer * 2 + kvsel) * a.n_kv_heads + g) * a.page_size) * d + i;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (c0 + j < B) {
+              const float o = is_v ? v[j] : (lo_half ? (v[j] * cs[j] - pv[j] * sn[j]) : (v[j] * cs[j] + pv[j] * sn[j]));
+              const int pos = meta[(c0 + j) & 255];
+              const int page = meta[256 + ((c0 + j) & 255)];
+              a.kv_base[static_cast<long long>(page) * a.page_stride + inner + static_cast<long long>(pos % a.page_size) * d] =
+                  __float2bfloat16_rn(o);
+            }
           }
         }
       }
@@ -205,140 +267,363 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
   }
 }
 
+
+// SUN-BLK: W[rows][k] bf16 -> [m_tiles][k/64][128 rows][64 cols] with the
+// 16-byte chunk c of row r stored at chunk position c ^ (r & 7) (SWIZZLE_128B
+// image), zero padded to whole tiles / k-blocks. One-time, at weight load.
+__global__ void block_weights_kernel(const __nv_bfloat16* __restrict__ w, long long rows, long long k, int kb64,
+                                     uint8_t* __restrict__ out) {
+  const long long blk = blockIdx.x;  // tile * kb64 + kb
+  const long long tile = blk / kb64;
+  const int kb = static_cast<int>(blk % kb64);
+  uint8_t* dst = out + blk * kTileWBytes;
+  for (int i = threadIdx.x; i < kTileM * 8; i += blockDim.x) {
+    const int r = i >> 3, c = i & 7;
+    const long long row = tile * kTileM + r;
+    const long long col = static_cast<long long>(kb) * kTileK + c * 8;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (row < rows && col < k) v = *reinterpret_cast<const uint4*>(w + row * k + col);  // k % 8 == 0
+    *reinterpret_cast<uint4*>(dst + r * 128 + ((c ^ (r & 7)) << 4)) = v;
+  }
+}
+
+// Row-major bf16 X[rows][k] (stride ld) -> SUN-ACT with `act_rows` rows per atom.
+__global__ void block_activations_kernel(const __nv_bfloat16* __restrict__ x, int rows, long long k, long long ld,
+                                         int act_rows, uint8_t* __restrict__ out) {
+  const long long n = static_cast<long long>(act_rows) * ((k + 63) / 64) * 8;  // 16-byte chunks
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i & 7);
+    const int b = static_cast<int>((i >> 3) % act_rows);
+    const long long kb = (i >> 3) / act_rows;
+    const long long col = kb * 64 + c * 8;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (b < rows && col < k) v = *reinterpret_cast<const uint4*>(x + b * ld + col);
+    *reinterpret_cast<uint4*>(out + act_offset(b, col, act_rows)) = v;
+  }
+}
+
+// Unsplit tile: TMEM accumulator -> fused epilogue directly.
 template <int EPI>
-__global__ void __launch_bounds__(kGemmThreads, 1)
-    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
-                     const GemmArgs a) {
+SUN_DEVICE void direct_epilogue(const GemmArgs& a, int tile, uint32_t taddr, float* epi) {
+  const int q = (threadIdx.x / 32) & 3;
+  const int row_local = q * 32 + (threadIdx.x & 31);
+  float* red_val = epi + 16 * kTileM;
+  int* red_idx = reinterpret_cast<int*>(red_val + 64);
+  float v[16];
+  for (int c0 = 0; c0 < a.bn; c0 += 16) {
+    tmem_ld16(taddr + c0, v);
+    epi_chunk<EPI>(a, tile, row_local, c0, v, epi, red_val, red_idx);
+  }
+}
+
+template <int EPI>
+SUN_DEVICE void load_qkv_meta(const GemmArgs& a, float* epi) {
+  if constexpr (EPI == EPI_QKV_ROPE) {
+    int* meta = reinterpret_cast<int*>(epi + 16 * kTileM + 128);
+    for (int b = threadIdx.x - 64; b < a.bn; b += 128) {
+      const int pos = b < a.batch ? a.positions[b] : 0;
+      meta[b] = pos;
+      meta[256 + b] = b < a.batch ? a.block_tables[static_cast<long long>(b) * a.bt_stride + pos / a.page_size] : 0;
+    }
+    epi_bar();
+  }
+}
+
+SUN_DEVICE void cvt_bar() { asm volatile("bar.sync 2, 128;" ::: "memory"); }
+
+// Dequantise one 128x128 block: packed (128 rows x 64 B) + scales -> SW128 bf16 tile.
+SUN_DEVICE void w4_dequant_block(const uint8_t* pk, const __nv_bfloat16* sc, uint8_t* dq, int ct) {
+  const __nv_bfloat162 off = __floats2bfloat162_rn(136.f, 136.f);
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int r = p * 32 + (ct >> 2);
+    const int c4 = ct & 3;  // 16-byte packed chunk = 32 k elements
+    const uint4 w = *reinterpret_cast<const uint4*>(pk + r * 64 + c4 * 16);
+    const __nv_bfloat162 s2 = __bfloat162bfloat162(sc[r]);
+    const uint32_t words[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t u = ((words[q] >> (4 * e)) & 0x000F000Fu) | 0x43004300u;
+        __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(&u);
+        v = __hmul2(__hsub2(v, off), s2);
+        o[e] = *reinterpret_cast<uint32_t*>(&v);
+      }
+      const int c = c4 * 4 + q;  // 16-byte bf16 chunk index within the 128-wide k block
+      const int atom = c >> 3;
+      const int phys = (c & 7) ^ (r & 7);
+      *reinterpret_cast<uint4*>(dq + atom * (kTileM * 128) + r * 128 + phys * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
+
+template <int EPI, bool W4>
+__global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel(const GemmArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int stages = a.stages;
-  const uint32_t x_bytes = static_cast<uint32_t>(a.bn) * 128u;
-  const uint32_t stage_bytes = kTileWBytes + x_bytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
+  const uint32_t sb = gemm_stage_bytes(a.bn, W4);
+  const uint32_t xoff = W4 ? kW4PackedBytes + 1024u : 2u * kTileWBytes;  // X offset inside a stage
+  uint8_t* deq = smem;                                                    // W4: [2][32 KB]
+  uint8_t* stg = smem + (W4 ? 2 * kW4DeqBytes : 0);
+  float* epi = reinterpret_cast<float*>(stg + stages * sb);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(epi) + kEpiSmemBytes);
   uint64_t* empty = full + stages;
-  uint64_t* tmem_full = empty + stages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
-  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+  uint64_t* tfull = empty + stages;  // [2]
+  uint64_t* tempty = tfull + 2;      // [2]
+  uint64_t* dfull = tempty + 2;      // [2] W4
+  uint64_t* dempty = dfull + 2;      // [2] W4
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + 2);
 
   const int warp = warp_id_sync();
-  const int lane = threadIdx.x & 31;
-  const int m_tile = blockIdx.x;
-  const int split = blockIdx.y;
-  const int kb0 = split * a.kb_per_split;
-  const int kb1 = min(a.kb_total, kb0 + a.kb_per_split);
-  const int nkb = kb1 - kb0;
+  const uint32_t S = a.splits > 1 ? static_cast<uint32_t>(a.splits) : 1u;
+  const bool clustered = S > 1;
+  const uint32_t rank = clustered ? cluster_ctarank() : 0u;
+  // this CTA's work: tiles [t_lo, t_hi) x ksteps [ks0, ks1)
+  int t_lo, t_hi, ks0, ks1;
+  if (clustered) {
+    t_lo = static_cast<int>(blockIdx.x / S);
+    t_hi = t_lo + 1;
+    ks0 = static_cast<int>(rank * a.ksteps / S);
+    ks1 = static_cast<int>((rank + 1) * a.ksteps / S);
+  } else {
+    t_lo = static_cast<int>(static_cast<long long>(blockIdx.x) * a.m_tiles / gridDim.x);
+    t_hi = static_cast<int>(static_cast<long long>(blockIdx.x + 1) * a.m_tiles / gridDim.x);
+    ks0 = 0;
+    ks1 = a.ksteps;
+  }
+  const int nks = ks1 - ks0;
+  const int n = (t_hi - t_lo) * nks;
+  const uint32_t ncols = tmem_cols_for(a.bn);
+  const long long rows_pad = static_cast<long long>(a.m_tiles) * kTileM;
+  if (threadIdx.x == 0) SUN_STAMP(0);
 
   if (warp == 0 && elect_one()) {
-    tma_prefetch_desc(&tm_w);
-    tma_prefetch_desc(&tm_x);
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], W4 ? 2 : 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int j = 0; j < 2; ++j) {
+      mbar_init(&tfull[j], 1);
+      mbar_init(&tempty[j], 1);
+      mbar_init(&dfull[j], 1);
+      mbar_init(&dempty[j], 1);
+    }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+  if (warp == 1) tmem_alloc(tmem_slot, ncols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) SUN_STAMP(1);
+
+  auto nblk_of = [&](int ks) { return min(2, a.kb64 - 2 * ks); };
 
   if (warp == 0) {
     if (elect_one()) {
-      // Weights do not depend on the previous kernel: start streaming them
-      // before the grid dependency resolves, then the activations.
-      const int pre = min(nkb, stages);
-      for (int i = 0; i < pre; ++i) {
-        mbar_arrive_expect_tx(&full[i], stage_bytes);
-        tma_load_2d(smem + i * stage_bytes, &tm_w, &full[i], (kb0 + i) * kTileK, m_tile * kTileM, kEvictFirst);
-      }
+      // issue weight (or packed+scales) loads of stage j; X is added separately
+      auto issue_w = [&](int j) {
+        const int s = j % stages;
+        const int tile = t_lo + j / nks;
+        const int ks = ks0 + j % nks;
+        const int nb = nblk_of(ks);
+        uint8_t* st = stg + s * sb;
+        if constexpr (W4) {
+          mbar_arrive_expect_tx(&full[s], kW4PackedBytes + 256u + 2u * a.bn * 128u);
+          bulk_load_hint(st, a.w4_packed + (static_cast<long long>(tile) * a.ksteps + ks) * kW4PackedBytes,
+                         kW4PackedBytes, &full[s], kEvictFirst);
+          bulk_load_hint(st + kW4PackedBytes, a.w4_scales + ks * rows_pad + static_cast<long long>(tile) * kTileM,
+                         256u, &full[s], kEvictFirst);
+        } else {
+          mbar_arrive_expect_tx(&full[s], nb * (kTileWBytes + a.bn * 128u));
+          bulk_load_hint(st, a.wblk + (static_cast<long long>(tile) * a.kb64 + 2 * ks) * kTileWBytes,
+                         nb * kTileWBytes, &full[s], kEvictFirst);
+        }
+      };
+      auto issue_x = [&](int j) {
+        const int s = j % stages;
+        const int ks = ks0 + j % nks;
+        const int nb = W4 ? 2 : nblk_of(ks);
+        bulk_load_hint(stg + s * sb + xoff, a.xact + static_cast<long long>(2 * ks) * a.bn * 128,
+                       nb * a.bn * 128u, &full[s], kEvictLast);
+      };
+      const int pre = n < stages ? n : stages;
+      for (int j = 0; j < pre; ++j) issue_w(j);  // weights never depend on the previous kernel
       pdl_wait();
-      for (int i = 0; i < pre; ++i)
-        tma_load_2d(smem + i * stage_bytes + kTileWBytes, &tm_x, &full[i], (kb0 + i) * kTileK, 0, kEvictLast);
-      for (int i = pre; i < nkb; ++i) {
-        const int s = i % stages;
-        const uint32_t ph = (i / stages) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&full[s], stage_bytes);
-        tma_load_2d(smem + s * stage_bytes, &tm_w, &full[s], (kb0 + i) * kTileK, m_tile * kTileM, kEvictFirst);
-        tma_load_2d(smem + s * stage_bytes + kTileWBytes, &tm_x, &full[s], (kb0 + i) * kTileK, 0, kEvictLast);
+      for (int j = 0; j < pre; ++j) issue_x(j);
+      for (int j = pre; j < n; ++j) {
+        const int s = j % stages;
+        mbar_wait(&empty[s], ((j / stages) & 1) ^ 1);
+        issue_w(j);
+        issue_x(j);
       }
     }
   } else if (warp == 1) {
     const uint32_t idesc = make_idesc_bf16(kTileM, a.bn);
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % stages;
-      const uint32_t ph = (i / stages) & 1;
-      mbar_wait(&full[s], ph);
+    int seg = 0;
+    for (int j = 0; j < n; ++j) {
+      const int s = j % stages;
+      const int jj = j % nks;
+      const bool first = jj == 0, last = jj == nks - 1;
+      const int buf = seg & 1;
+      const int nb = nblk_of(ks0 + jj);
+      if (first) {
+        mbar_wait(&tempty[buf], ((seg >> 1) & 1) ^ 1);
+        tc_fence_after();
+      }
+      mbar_wait(&full[s], (j / stages) & 1);
+      if constexpr (W4) mbar_wait(&dfull[j & 1], (j >> 1) & 1);
       tc_fence_after();
+      if (j == 0 && threadIdx.x == 32) SUN_STAMP(2);
       if (elect_one()) {
-        const uint32_t wa = smem_u32(smem + s * stage_bytes);
-        const uint32_t xa = wa + kTileWBytes;
-#pragma unroll
-        for (int kk = 0; kk < kTileK / 16; ++kk) {
-          umma_bf16(tmem_base, make_sw128_desc(wa + kk * 32), make_sw128_desc(xa + kk * 32), idesc,
-                    (i | kk) != 0 ? 1u : 0u);
+        const uint32_t wa = W4 ? smem_u32(deq + (j & 1) * kW4DeqBytes) : smem_u32(stg + s * sb);
+        const uint32_t xa = smem_u32(stg + s * sb + xoff);
+        const uint32_t tacc = tmem_base + static_cast<uint32_t>(buf * a.bn);
+        for (int kk = 0; kk < nb * 4; ++kk) {
+          const uint32_t atom = kk >> 2;
+          const uint32_t koff = (kk & 3) * 32;
+          umma_bf16(tacc, make_sw128_desc(wa + atom * kTileWBytes + koff),
+                    make_sw128_desc(xa + atom * (a.bn * 128u) + koff), idesc, (first && kk == 0) ? 0u : 1u);
         }
         umma_commit(&empty[s]);
-        if (i == nkb - 1) umma_commit(tmem_full);
+        if constexpr (W4) umma_commit(&dempty[j & 1]);
+        if (last) umma_commit(&tfull[buf]);
       }
       __syncwarp();
+      if (last) ++seg;
     }
-  } else {
+    if (threadIdx.x == 32) SUN_STAMP(3);
+  } else if (warp < 6) {
     // ---------------- epilogue: warps 2..5 ----------------
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int row_local = q * 32 + lane;
-    const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-    float* stage_f32 = reinterpret_cast<float*>(smem);  // pipeline buffers are idle now
-    float* red_val = stage_f32 + 16 * kTileM;
-    int* red_idx = reinterpret_cast<int*>(red_val + 64);
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
-    float v[16];
-    if (a.splits == 1) {
-      for (int c0 = 0; c0 < a.bn; c0 += 16) {
-        tmem_ld16(taddr + c0, v);
-        epi_chunk<EPI>(a, m_tile, row_local, c0, v, stage_f32, red_val, red_idx);
-      }
-    } else {
-      float* part = a.partial + (static_cast<long long>(m_tile) * a.splits + split) * a.bn * kTileM;
-      for (int c0 = 0; c0 < a.bn; c0 += 16) {
-        tmem_ld16(taddr + c0, v);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) part[(c0 + j) * kTileM + row_local] = v[j];
-      }
-      __threadfence();
-      epi_bar();
-      if (threadIdx.x == 64) {
-        const unsigned prev = atomicAdd(&a.counters[m_tile], 1u);
-        const int last = (prev == static_cast<unsigned>(a.splits - 1));
-        if (last) a.counters[m_tile] = 0u;
-        *last_flag = last;
-      }
-      epi_bar();
-      if (*last_flag) {
-        __threadfence();
-        const float* base = a.partial + static_cast<long long>(m_tile) * a.splits * a.bn * kTileM;
+    pdl_wait();
+    load_qkv_meta<EPI>(a, epi);
+    const int q = warp & 3;
+    const int row_local = q * 32 + (threadIdx.x & 31);
+    for (int seg = 0; seg < t_hi - t_lo; ++seg) {
+      const int buf = seg & 1;
+      mbar_wait(&tfull[buf], (seg >> 1) & 1);
+      tc_fence_after();
+      if (threadIdx.x == 64 && seg == 0) SUN_STAMP(4);
+      const uint32_t taddr = tmem_base + static_cast<uint32_t>(buf * a.bn) + (static_cast<uint32_t>(q * 32) << 16);
+      if (!clustered) {
+        direct_epilogue<EPI>(a, t_lo + seg, taddr, epi);
+        tc_fence_before();
+        epi_bar();
+        if (threadIdx.x == 64) mbar_arrive(&tempty[buf]);
+      } else {
+        // park the partial in (now idle) shared memory: [128 rows][bn + 4] fp32
+        float* part = reinterpret_cast<float*>(smem);
+        const int ld = a.bn + 4;
+        float v[16];
         for (int c0 = 0; c0 < a.bn; c0 += 16) {
+          tmem_ld16(taddr + c0, v);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = __ldcg(base + (c0 + j) * kTileM + row_local);
-          for (int s = 1; s < a.splits; ++s) {
-            const float* ps = base + static_cast<long long>(s) * a.bn * kTileM;
-#pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] += __ldcg(ps + (c0 + j) * kTileM + row_local);
-          }
-          epi_chunk<EPI>(a, m_tile, row_local, c0, v, stage_f32, red_val, red_idx);
+          for (int j = 0; j < 16; j += 4)
+            *reinterpret_cast<float4*>(part + row_local * ld + c0 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
         }
+      }
+    }
+  } else if constexpr (W4) {
+    // ---------------- converters: warps 6..9 ----------------
+    const int ct = threadIdx.x - 192;
+    for (int j = 0; j < n; ++j) {
+      const int s = j % stages;
+      mbar_wait(&full[s], (j / stages) & 1);
+      if (j >= 2) mbar_wait(&dempty[j & 1], ((j >> 1) & 1) ^ 1);
+      const uint8_t* pk = stg + s * sb;
+      w4_dequant_block(pk, reinterpret_cast<const __nv_bfloat16*>(pk + kW4PackedBytes), deq + (j & 1) * kW4DeqBytes, ct);
+      fence_proxy_async_smem();
+      cvt_bar();
+      if (ct == 0) {
+        mbar_arrive(&dfull[j & 1]);
+        mbar_arrive(&empty[s]);
       }
     }
   }
+
+  if (clustered) {
+    cluster_sync_all();  // every rank's partial is visible cluster-wide
+    if (warp >= 2 && warp < 6) {
+      const int q = warp & 3;
+      const int row_local = q * 32 + (threadIdx.x & 31);
+      float* part = reinterpret_cast<float*>(smem);
+      const int ld = a.bn + 4;
+      float* red_val = epi + 16 * kTileM;
+      int* red_idx = reinterpret_cast<int*>(red_val + 64);
+      for (int c0 = static_cast<int>(rank) * 16; c0 < a.bn; c0 += static_cast<int>(S) * 16) {
+        float4 x[4][4];
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = 0.f;
+        for (uint32_t r0 = 0; r0 < S; r0 += 4) {  // 4 ranks' loads in flight, summed in rank order
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              x[u][j] = (r0 + u < S) ? ld_dsmem_f4(dsmem_addr(part + row_local * ld + c0 + 4 * j, r0 + u))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              v[4 * j] += x[u][j].x;
+              v[4 * j + 1] += x[u][j].y;
+              v[4 * j + 2] += x[u][j].z;
+              v[4 * j + 3] += x[u][j].w;
+            }
+        }
+        epi_chunk<EPI>(a, t_lo, row_local, c0, v, epi, red_val, red_idx);
+      }
+    }
+    cluster_sync_all();  // nobody exits while a peer may still read its partial
+  }
+  if (threadIdx.x == 64) SUN_STAMP(5);
   pdl_launch_dependents();
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, kTmemCols);
+    tmem_dealloc(tmem_base, ncols);
+  }
+  if (threadIdx.x == 0) SUN_STAMP(6);
+}
+
+// Offline quantiser (one thread per (row, group)); produces the tile-contiguous
+// SUN-W4 layout consumed above: packed block (m_tile, kb) is 128 rows x 64 B.
+__global__ void quantize_w4_kernel(const __nv_bfloat16* __restrict__ w, long long rows, long long rows_pad,
+                                   long long k, uint8_t* __restrict__ packed, __nv_bfloat16* __restrict__ scales) {
+  const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long ngroups = k / 128;
+  if (gid >= rows * ngroups) return;
+  const long long r = gid / ngroups;
+  const long long g = gid % ngroups;
+  const __nv_bfloat16* src = w + r * k + g * 128;
+  float amax = 0.f;
+  for (int i = 0; i < 128; ++i) amax = fmaxf(amax, fabsf(__bfloat162float(src[i])));
+  const __nv_bfloat16 sb = __float2bfloat16_rn(amax / 7.5f);
+  const float s = __bfloat162float(sb);
+  scales[g * rows_pad + r] = sb;
+  const long long kb_total = k / 128;
+  uint8_t* dst = packed + ((r / 128) * kb_total + g) * 8192 + (r % 128) * 64;
+  for (int wd = 0; wd < 16; ++wd) {  // 16 words of 8 elements
+    uint32_t word = 0;
+    for (int e = 0; e < 8; ++e) {
+      const float x = __bfloat162float(src[wd * 8 + e]);
+      int qv = 0;
+      if (s > 0.f) {
+        qv = static_cast<int>(rintf(x / s));
+        qv = qv < -8 ? -8 : (qv > 7 ? 7 : qv);
+      }
+      const uint32_t u = static_cast<uint32_t>(qv + 8);
+      const int nib = (e & 1) ? 4 + (e >> 1) : (e >> 1);  // order [0,2,4,6,1,3,5,7]
+      word |= u << (4 * nib);
+    }
+    reinterpret_cast<uint32_t*>(dst)[wd] = word;
   }
 }
 

@@ -104,25 +104,23 @@ SunStatus make_map_kv(CUtensorMap* m, const SunDecoderDims& d, const SunKvPool& 
 constexpr int kNumSms = 148;
 
 struct GemmPlan {
-  int m_tiles, kb_total, kb_per_split, splits;
+  int m_tiles, kb64, ksteps;
 };
 
 GemmPlan plan_gemm(int64_t n_out, int64_t k) {
   GemmPlan p;
   p.m_tiles = int((n_out + kTileM - 1) / kTileM);
-  p.kb_total = int((k + kTileK - 1) / kTileK);
-  const int target = 2 * kNumSms;
-  int splits = (target + p.m_tiles - 1) / p.m_tiles;
-  splits = std::max(1, std::min(splits, std::max(1, p.kb_total / 4)));
-  p.kb_per_split = (p.kb_total + splits - 1) / splits;
-  p.splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
+  p.kb64 = int((k + kTileK - 1) / kTileK);
+  p.ksteps = (p.kb64 + 1) / 2;
   return p;
 }
 
-int gemm_stages(int bn) {
-  const int budget = 110 * 1024 - 1280;
-  int st = budget / int(kTileWBytes + bn * 128);
-  return std::max(2, std::min(8, st));
+constexpr int kSmemBudget = 220 * 1024;
+
+int gemm_stages(int bn, bool w4) {
+  const int avail = kSmemBudget - 1024 - (w4 ? 2 * int(kW4DeqBytes) : 0) - int(kEpiSmemBytes) - 512;
+  int st = avail / int(gemm_stage_bytes(bn, w4));
+  return std::max(2, std::min(6, st));
 }
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -137,19 +135,21 @@ void set_max_smem(K kern) {
 std::once_flag g_attr_once;
 void init_kernel_attrs() {
   std::call_once(g_attr_once, [] {
-    set_max_smem(gemm_bf16_kernel<EPI_STORE_F32>);
-    set_max_smem(gemm_bf16_kernel<EPI_RESID_ADD>);
-    set_max_smem(gemm_bf16_kernel<EPI_QKV_ROPE>);
-    set_max_smem(gemm_bf16_kernel<EPI_SWIGLU>);
-    set_max_smem(gemm_bf16_kernel<EPI_LOGITS>);
-    set_max_smem(gemm_w4_kernel<EPI_RESID_ADD>);
-    set_max_smem(gemm_w4_kernel<EPI_QKV_ROPE>);
-    set_max_smem(gemm_w4_kernel<EPI_SWIGLU>);
-    set_max_smem(gemm_w4_kernel<EPI_STORE_F32>);
+    set_max_smem(gemm_kernel<EPI_STORE_F32, false>);
+    set_max_smem(gemm_kernel<EPI_RESID_ADD, false>);
+    set_max_smem(gemm_kernel<EPI_QKV_ROPE, false>);
+    set_max_smem(gemm_kernel<EPI_SWIGLU, false>);
+    set_max_smem(gemm_kernel<EPI_LOGITS, false>);
+    set_max_smem(gemm_kernel<EPI_STORE_F32, true>);
+    set_max_smem(gemm_kernel<EPI_RESID_ADD, true>);
+    set_max_smem(gemm_kernel<EPI_QKV_ROPE, true>);
+    set_max_smem(gemm_kernel<EPI_SWIGLU, true>);
     set_max_smem(attn_decode_kernel<64>);
     set_max_smem(attn_decode_kernel<128>);
   });
 }
+
+thread_local unsigned g_cluster = 1;  // cluster size for the next launch_raw (1 = none)
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_raw(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
@@ -159,12 +159,55 @@ cudaError_t launch_raw(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  if (pdl) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (g_cluster > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = g_cluster;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  cfg.numAttrs = n;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  g_cluster = 1;
+  return e;
+}
+
+// How many clusters of `size` CTAs (each `smem` bytes, 1 per SM) can be co-resident.
+int max_active_clusters(unsigned size, size_t smem, bool w4) {
+  static std::map<std::pair<unsigned, size_t>, int> cache;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(size * 2 + (w4 ? 1u : 0u), smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(size * 16);
+  cfg.blockDim = dim3(w4 ? kW4Threads : kGemmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = size;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  const cudaError_t e = w4 ? cudaOccupancyMaxActiveClusters(&n, gemm_kernel<EPI_STORE_F32, true>, &cfg)
+                           : cudaOccupancyMaxActiveClusters(&n, gemm_kernel<EPI_STORE_F32, false>, &cfg);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    n = size == 1 ? kNumSms : 0;
+  }
+  cache[key] = n;
+  return n;
 }
 
 // Per-thread launch accounting + optional per-kernel event timing (profile mode).
@@ -194,7 +237,7 @@ cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, c
 
 // Workspace layout shared by sizing and creation.
 struct WsLayout {
-  size_t resid, xn, q, attn, act, part_o, part_ml, gemm_part, counters, amax_val, amax_idx, logits, total;
+  size_t resid, xn, q, attn, act, part_o, part_ml, amax_val, amax_idx, logits, total;
   int max_splits;
 };
 
@@ -213,24 +256,14 @@ WsLayout layout_ws(const SunDecoderDims& d, int max_batch) {
     off = align_up(off + bytes, 1024);
     return o;
   };
+  auto act_bytes = [&](int k) { return size_t(bmp) * size_t((k + 63) / 64) * 128; };  // SUN-ACT, padded K
   w.resid = take(size_t(max_batch) * d.hidden * 4);
-  w.xn = take(size_t(bmp) * d.hidden * 2);
+  w.xn = take(act_bytes(d.hidden));
   w.q = take(size_t(max_batch) * qd * 2);
-  w.attn = take(size_t(bmp) * qd * 2);
-  w.act = take(size_t(bmp) * d.ffn * 2);
+  w.attn = take(act_bytes(qd));
+  w.act = take(act_bytes(d.ffn));
   w.part_o = take(size_t(max_batch) * d.n_q_heads * w.max_splits * d.head_dim * 4);
   w.part_ml = take(size_t(max_batch) * d.n_q_heads * w.max_splits * 2 * 4);
-  size_t gp = 0;
-  int max_tiles = 0;
-  const int64_t shapes[5][2] = {{qkv_rows(d), d.hidden}, {d.hidden, qd}, {gu_rows(d), d.hidden},
-                                {d.hidden, d.ffn}, {d.vocab, d.hidden}};
-  for (auto& s : shapes) {
-    GemmPlan p = plan_gemm(s[0], s[1]);
-    if (p.splits > 1) gp = std::max(gp, size_t(p.m_tiles) * p.splits * bmp * kTileM * 4);
-    max_tiles = std::max(max_tiles, p.m_tiles);
-  }
-  w.gemm_part = take(std::max<size_t>(gp, 4));
-  w.counters = take(size_t(max_tiles) * 4);
   const int lm_tiles = (d.vocab + kTileM - 1) / kTileM;
   w.amax_val = take(size_t(lm_tiles) * bmp * 4);
   w.amax_idx = take(size_t(lm_tiles) * bmp * 4);
@@ -259,10 +292,6 @@ SunStatus check_dims(const SunDecoderDims* d) {
   return SUN_OK;
 }
 
-struct XMaps {
-  CUtensorMap xn, attn, act;
-};
-
 }  // namespace
 
 struct SunDecoder {
@@ -274,66 +303,60 @@ struct SunDecoder {
   SunKvPool kv;
   long long page_stride = 0;
   CUtensorMap tm_kv;
-  std::vector<CUtensorMap> tm_qkv, tm_o, tm_gu, tm_down;
-  CUtensorMap tm_lm;
-  std::map<int, XMaps> xmaps;
   WsLayout L;
   uint8_t* ws = nullptr;
   float* resid;
-  __nv_bfloat16 *xn, *q, *attn, *act;
-  float *part_o, *part_ml, *gemm_part, *amax_val, *logits;
-  unsigned* counters;
+  __nv_bfloat16 *xn, *q, *attn, *act;  // xn / attn / act in SUN-ACT (GEMM operands)
+  float *part_o, *part_ml, *amax_val, *logits;
   int* amax_idx;
   GemmPlan p_qkv, p_o, p_gu, p_down, p_lm;
 };
 
 namespace {
 
-SunStatus get_xmaps(SunDecoder* dec, int bn, XMaps** out) {
-  auto it = dec->xmaps.find(bn);
-  if (it == dec->xmaps.end()) {
-    XMaps m;
-    const SunDecoderDims& d = dec->d;
-    SunStatus st;
-    if ((st = make_map_2d(&m.xn, dec->xn, dec->bmp, d.hidden, d.hidden, bn)) != SUN_OK) return st;
-    if ((st = make_map_2d(&m.attn, dec->attn, dec->bmp, d.n_q_heads * d.head_dim, d.n_q_heads * d.head_dim, bn)) != SUN_OK) return st;
-    if ((st = make_map_2d(&m.act, dec->act, dec->bmp, d.ffn, d.ffn, bn)) != SUN_OK) return st;
-    it = dec->xmaps.emplace(bn, m).first;
-  }
-  *out = &it->second;
-  return SUN_OK;
-}
-
-GemmArgs base_args(const GemmPlan& p, int64_t n_out, int64_t k, int batch, int bn, float* part, unsigned* counters) {
+GemmArgs base_args(const GemmPlan& p, int64_t n_out, int64_t k, int batch, int bn, const void* xact) {
   GemmArgs a;
   memset(&a, 0, sizeof(a));
   a.n_out = int(n_out);
   a.k = int(k);
   a.batch = batch;
   a.bn = bn;
-  a.kb_total = p.kb_total;
-  a.kb_per_split = p.kb_per_split;
-  a.splits = p.splits;
-  a.stages = gemm_stages(bn);
-  a.weight_bits = 16;
-  a.partial = part;
-  a.counters = counters;
+  a.kb64 = p.kb64;
+  a.ksteps = p.ksteps;
+  a.m_tiles = p.m_tiles;
+  a.xact = static_cast<const uint8_t*>(xact);
   return a;
 }
 
-template <int EPI>
-SunStatus run_gemm(const CUtensorMap& tw, const CUtensorMap& tx, const GemmArgs& a, const GemmPlan& p,
-                   cudaStream_t st, bool pdl) {
-  const size_t smem = gemm_smem_bytes(a.bn, a.stages);
-  SUN_CUDA(launch(gemm_bf16_kernel<EPI>, dim3(p.m_tiles, p.splits), dim3(kGemmThreads), smem, st, pdl, tw, tx, a));
-  return SUN_OK;
+// Cluster split factor for a GEMM with <= 148 tiles: the largest S <= 8 (and
+// <= k-steps) whose m_tiles clusters of S CTAs are co-resident in one wave.
+int cluster_splits(const GemmPlan& p, size_t smem, bool w4) {
+  if (p.m_tiles > kNumSms) return 1;
+  int s = std::min(std::min(8, kNumSms / std::max(1, p.m_tiles)), p.ksteps);
+  while (s > 1 && max_active_clusters(unsigned(s), smem, w4) < p.m_tiles) --s;
+  return std::max(1, s);
 }
 
+// Launch one GEMM: bf16 SUN-BLK weights (wblk) or QSUN SUN-W4 (packed, scales).
 template <int EPI>
-SunStatus run_gemm_w4(const W4Weights& ww, const CUtensorMap& tx, const GemmArgs& a, const GemmPlan& p,
-                      cudaStream_t st, bool pdl) {
-  const size_t smem = w4_smem_bytes(a.bn, a.stages);
-  SUN_CUDA(launch(gemm_w4_kernel<EPI>, dim3(p.m_tiles, p.splits), dim3(kW4Threads), smem, st, pdl, ww, tx, a));
+SunStatus run_gemm(const void* wblk, const void* packed, const void* scales, GemmArgs a, const GemmPlan& p,
+                   cudaStream_t st, bool pdl) {
+  const bool w4 = packed != nullptr;
+  a.wblk = static_cast<const uint8_t*>(wblk);
+  a.w4_packed = static_cast<const uint8_t*>(packed);
+  a.w4_scales = static_cast<const __nv_bfloat16*>(scales);
+  a.stages = gemm_stages(a.bn, w4);
+  const size_t smem = gemm_smem_bytes(a.bn, a.stages, w4);
+  const int S = cluster_splits(p, smem, w4);
+  a.splits = S;
+  const int grid = S > 1 ? p.m_tiles * S : std::min(p.m_tiles, kNumSms);
+  g_cluster = unsigned(S);
+  if (w4) {
+    if constexpr (EPI == EPI_LOGITS) return fail(SUN_ERR_UNSUPPORTED, "lm_head is bf16");
+    else SUN_CUDA(launch(gemm_kernel<EPI, true>, dim3(grid), dim3(kW4Threads), smem, st, pdl, a));
+  } else {
+    SUN_CUDA(launch(gemm_kernel<EPI, false>, dim3(grid), dim3(kGemmThreads), smem, st, pdl, a));
+  }
   return SUN_OK;
 }
 
@@ -412,8 +435,6 @@ SunStatus sun_decoder_create(const SunDecoderDims* dims, const SunWeights* weigh
   dec->act = reinterpret_cast<__nv_bfloat16*>(ws + dec->L.act);
   dec->part_o = reinterpret_cast<float*>(ws + dec->L.part_o);
   dec->part_ml = reinterpret_cast<float*>(ws + dec->L.part_ml);
-  dec->gemm_part = reinterpret_cast<float*>(ws + dec->L.gemm_part);
-  dec->counters = reinterpret_cast<unsigned*>(ws + dec->L.counters);
   dec->amax_val = reinterpret_cast<float*>(ws + dec->L.amax_val);
   dec->amax_idx = reinterpret_cast<int*>(ws + dec->L.amax_idx);
   dec->logits = reinterpret_cast<float*>(ws + dec->L.logits);
@@ -426,33 +447,8 @@ SunStatus sun_decoder_create(const SunDecoderDims* dims, const SunWeights* weigh
   dec->p_down = plan_gemm(d.hidden, d.ffn);
   dec->p_lm = plan_gemm(d.vocab, d.hidden);
   if ((st = make_map_kv(&dec->tm_kv, d, *kv)) != SUN_OK) { delete dec; return st; }
-  if (d.weight_bits == 16) {
-    dec->tm_qkv.resize(d.n_layers);
-    dec->tm_o.resize(d.n_layers);
-    dec->tm_gu.resize(d.n_layers);
-    dec->tm_down.resize(d.n_layers);
-    for (int l = 0; l < d.n_layers; ++l) {
-      const SunLayerWeights& lw = dec->layers[l];
-      if ((st = make_map_2d(&dec->tm_qkv[l], lw.w_qkv, qkv_rows(d), d.hidden, d.hidden, kTileM)) != SUN_OK ||
-          (st = make_map_2d(&dec->tm_o[l], lw.w_o, d.hidden, qd, qd, kTileM)) != SUN_OK ||
-          (st = make_map_2d(&dec->tm_gu[l], lw.w_gate_up, gu_rows(d), d.hidden, d.hidden, kTileM)) != SUN_OK ||
-          (st = make_map_2d(&dec->tm_down[l], lw.w_down, d.hidden, d.ffn, d.ffn, kTileM)) != SUN_OK) {
-        delete dec;
-        return st;
-      }
-    }
-  }
-  if ((st = make_map_2d(&dec->tm_lm, weights->lm_head, d.vocab, d.hidden, d.hidden, kTileM)) != SUN_OK) {
-    delete dec;
-    return st;
-  }
-  cudaError_t e = cudaMemset(ws + dec->L.counters, 0, size_t(std::max(dec->p_lm.m_tiles, 1)) * 4);
-  if (e != cudaSuccess) {
-    delete dec;
-    return fail(SUN_ERR_CUDA, "cudaMemset counters: %s", cudaGetErrorString(e));
-  }
-  // zero the padded activation rows once (rows >= batch are never written)
-  e = cudaMemset(ws, 0, dec->L.part_o);
+  // zero the activation buffers once (K padding of SUN-ACT is never written)
+  cudaError_t e = cudaMemset(ws, 0, dec->L.part_o);
   if (e != cudaSuccess) {
     delete dec;
     return fail(SUN_ERR_CUDA, "cudaMemset ws: %s", cudaGetErrorString(e));
@@ -477,14 +473,13 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
   const SunDecoderDims& d = dec->d;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool pdl = dec->pdl;
-  const int bn = round16(batch);
-  XMaps* xm = nullptr;
+  const int bn = round16(batch);  // MMA N and the SUN-ACT row count of this step
   SunStatus s;
-  if ((s = get_xmaps(dec, bn, &xm)) != SUN_OK) return s;
   const int qd = d.n_q_heads * d.head_dim;
   const int max_pages = (d.max_context + kPageTokens - 1) / kPageTokens;
   const int pps = pages_per_split > 0 ? std::min(pages_per_split, max_pages) : auto_pages_per_split(d, batch);
   float* lg = logits ? logits : dec->logits;
+  const bool w4 = d.weight_bits == 4;
 
   AttnArgs aa;
   memset(&aa, 0, sizeof(aa));
@@ -501,20 +496,21 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
   aa.part_ml = dec->part_ml;
   aa.out = dec->attn;
   aa.ld_out = qd;
+  aa.act_rows = bn;
 
   // embedding gather + first attention RMSNorm
   SUN_CUDA(launch(rmsnorm_kernel, dim3(batch), dim3(kRowThreads), 0, st, pdl, tokens,
                   static_cast<const __nv_bfloat16*>(dec->w.embed), dec->resid,
                   static_cast<const __nv_bfloat16*>(dec->layers[0].attn_norm), dec->xn, d.hidden,
-                  (long long)d.hidden, d.rms_eps));
+                  (long long)d.hidden, d.rms_eps, bn));
   for (int l = 0; l < d.n_layers; ++l) {
     const SunLayerWeights& lw = dec->layers[l];
     if (l > 0)
       SUN_CUDA(launch(rmsnorm_kernel, dim3(batch), dim3(kRowThreads), 0, st, pdl, (const int*)nullptr,
                       (const __nv_bfloat16*)nullptr, dec->resid, static_cast<const __nv_bfloat16*>(lw.attn_norm),
-                      dec->xn, d.hidden, (long long)d.hidden, d.rms_eps));
+                      dec->xn, d.hidden, (long long)d.hidden, d.rms_eps, bn));
     // QKV + bias + RoPE + KV append
-    GemmArgs a = base_args(dec->p_qkv, qkv_rows(d), d.hidden, batch, bn, dec->gemm_part, dec->counters);
+    GemmArgs a = base_args(dec->p_qkv, qkv_rows(d), d.hidden, batch, bn, dec->xn);
     a.out_bf16 = dec->q;
     a.ldb = qd;
     a.bias = static_cast<const __nv_bfloat16*>(lw.b_qkv);
@@ -530,49 +526,49 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     a.n_kv_heads = d.n_kv_heads;
     a.head_dim = d.head_dim;
     a.page_size = d.page_size;
-    if (d.weight_bits == 16) s = run_gemm<EPI_QKV_ROPE>(dec->tm_qkv[l], xm->xn, a, dec->p_qkv, st, pdl);
-    else s = run_gemm_w4<EPI_QKV_ROPE>(W4Weights{lw.w_qkv, lw.s_qkv}, xm->xn, a, dec->p_qkv, st, pdl);
+    s = w4 ? run_gemm<EPI_QKV_ROPE>(nullptr, lw.w_qkv, lw.s_qkv, a, dec->p_qkv, st, pdl)
+           : run_gemm<EPI_QKV_ROPE>(lw.w_qkv, nullptr, nullptr, a, dec->p_qkv, st, pdl);
     if (s != SUN_OK) return s;
     // paged attention
     aa.layer = l;
     if ((s = run_attention(d, dec->tm_kv, aa, batch, st, pdl)) != SUN_OK) return s;
     // O projection + residual
-    a = base_args(dec->p_o, d.hidden, qd, batch, bn, dec->gemm_part, dec->counters);
+    a = base_args(dec->p_o, d.hidden, qd, batch, bn, dec->attn);
     a.out_f32 = dec->resid;
     a.ldo = d.hidden;
-    if (d.weight_bits == 16) s = run_gemm<EPI_RESID_ADD>(dec->tm_o[l], xm->attn, a, dec->p_o, st, pdl);
-    else s = run_gemm_w4<EPI_RESID_ADD>(W4Weights{lw.w_o, lw.s_o}, xm->attn, a, dec->p_o, st, pdl);
+    s = w4 ? run_gemm<EPI_RESID_ADD>(nullptr, lw.w_o, lw.s_o, a, dec->p_o, st, pdl)
+           : run_gemm<EPI_RESID_ADD>(lw.w_o, nullptr, nullptr, a, dec->p_o, st, pdl);
     if (s != SUN_OK) return s;
     // FFN RMSNorm
     SUN_CUDA(launch(rmsnorm_kernel, dim3(batch), dim3(kRowThreads), 0, st, pdl, (const int*)nullptr,
                     (const __nv_bfloat16*)nullptr, dec->resid, static_cast<const __nv_bfloat16*>(lw.ffn_norm),
-                    dec->xn, d.hidden, (long long)d.hidden, d.rms_eps));
+                    dec->xn, d.hidden, (long long)d.hidden, d.rms_eps, bn));
     // gate/up + SwiGLU
-    a = base_args(dec->p_gu, gu_rows(d), d.hidden, batch, bn, dec->gemm_part, dec->counters);
+    a = base_args(dec->p_gu, gu_rows(d), d.hidden, batch, bn, dec->xn);
     a.out_bf16 = dec->act;
     a.ldb = d.ffn;
     a.n_valid_out = d.ffn;
-    if (d.weight_bits == 16) s = run_gemm<EPI_SWIGLU>(dec->tm_gu[l], xm->xn, a, dec->p_gu, st, pdl);
-    else s = run_gemm_w4<EPI_SWIGLU>(W4Weights{lw.w_gate_up, lw.s_gate_up}, xm->xn, a, dec->p_gu, st, pdl);
+    s = w4 ? run_gemm<EPI_SWIGLU>(nullptr, lw.w_gate_up, lw.s_gate_up, a, dec->p_gu, st, pdl)
+           : run_gemm<EPI_SWIGLU>(lw.w_gate_up, nullptr, nullptr, a, dec->p_gu, st, pdl);
     if (s != SUN_OK) return s;
     // down + residual
-    a = base_args(dec->p_down, d.hidden, d.ffn, batch, bn, dec->gemm_part, dec->counters);
+    a = base_args(dec->p_down, d.hidden, d.ffn, batch, bn, dec->act);
     a.out_f32 = dec->resid;
     a.ldo = d.hidden;
-    if (d.weight_bits == 16) s = run_gemm<EPI_RESID_ADD>(dec->tm_down[l], xm->act, a, dec->p_down, st, pdl);
-    else s = run_gemm_w4<EPI_RESID_ADD>(W4Weights{lw.w_down, lw.s_down}, xm->act, a, dec->p_down, st, pdl);
+    s = w4 ? run_gemm<EPI_RESID_ADD>(nullptr, lw.w_down, lw.s_down, a, dec->p_down, st, pdl)
+           : run_gemm<EPI_RESID_ADD>(lw.w_down, nullptr, nullptr, a, dec->p_down, st, pdl);
     if (s != SUN_OK) return s;
   }
   // final norm, lm_head (+ argmax partials), greedy sampling
   SUN_CUDA(launch(rmsnorm_kernel, dim3(batch), dim3(kRowThreads), 0, st, pdl, (const int*)nullptr,
                   (const __nv_bfloat16*)nullptr, dec->resid, static_cast<const __nv_bfloat16*>(dec->w.final_norm),
-                  dec->xn, d.hidden, (long long)d.hidden, d.rms_eps));
-  GemmArgs a = base_args(dec->p_lm, d.vocab, d.hidden, batch, bn, dec->gemm_part, dec->counters);
+                  dec->xn, d.hidden, (long long)d.hidden, d.rms_eps, bn));
+  GemmArgs a = base_args(dec->p_lm, d.vocab, d.hidden, batch, bn, dec->xn);
   a.out_f32 = lg;
   a.ldo = d.vocab;
   a.amax_val = dec->amax_val;
   a.amax_idx = dec->amax_idx;
-  if ((s = run_gemm<EPI_LOGITS>(dec->tm_lm, xm->xn, a, dec->p_lm, st, pdl)) != SUN_OK) return s;
+  if ((s = run_gemm<EPI_LOGITS>(dec->w.lm_head, nullptr, nullptr, a, dec->p_lm, st, pdl)) != SUN_OK) return s;
   SUN_CUDA(launch(argmax_reduce_kernel, dim3(batch), dim3(kRowThreads), 0, st, pdl, (const float*)dec->amax_val,
                   (const int*)dec->amax_idx, dec->p_lm.m_tiles, bn, next_tokens,
                   (flags & SUN_STEP_FEEDBACK) ? const_cast<int*>(tokens) : (int*)nullptr,
@@ -619,36 +615,64 @@ SunStatus sun_decode_step_profile(SunDecoder* dec, const int32_t* tokens, const 
 
 SunStatus sun_gemm_workspace_bytes(int64_t n_out, int64_t k, int32_t batch, size_t* bytes) {
   if (n_out < 1 || k < 1 || batch < 1 || batch > 256) return fail(SUN_ERR_VALUE, "bad gemm shape");
-  GemmPlan p = plan_gemm(n_out, k);
-  const int bn = round16(batch);
-  *bytes = align_up(size_t(p.m_tiles) * 4, 1024) + size_t(p.m_tiles) * p.splits * bn * kTileM * 4;
+  *bytes = size_t(round16(batch)) * size_t((k + 63) / 64) * 128;  // SUN-ACT copy of X
   return SUN_OK;
 }
 
-SunStatus sun_gemm_bf16(const void* w, int64_t n_out, int64_t k, const void* x, int64_t ldx, int64_t x_rows,
-                        int32_t batch, float* out, int64_t ldo, int32_t accumulate, void* workspace,
-                        size_t workspace_bytes, void* stream) {
+extern "C++" {
+namespace {
+template <int EPI>
+SunStatus gemm_api(const void* wblk, const void* packed, const void* scales, int64_t n_out, int64_t k, const void* x,
+                   int64_t ldx, int64_t x_rows, int32_t batch, float* out, int64_t ldo, void* workspace,
+                   size_t workspace_bytes, void* stream, uint64_t* stamps) {
   if (batch < 1) return fail(SUN_ERR_VALUE, "empty batch");
+  if (k % 8 != 0) return fail(SUN_ERR_UNSUPPORTED, "k must be a multiple of 8");
   size_t need = 0;
   SunStatus s = sun_gemm_workspace_bytes(n_out, k, batch, &need);
   if (s != SUN_OK) return s;
   if (workspace_bytes < need) return fail(SUN_ERR_CAPACITY, "gemm workspace too small");
   const int bn = round16(batch);
-  if (x_rows < bn) return fail(SUN_ERR_VALUE, "x must have >= round_up(batch,16) rows");
+  if (x_rows < batch) return fail(SUN_ERR_VALUE, "x has fewer rows than batch");
   init_kernel_attrs();
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SUN_CUDA(launch(block_activations_kernel, dim3(148), dim3(256), 0, st, false, static_cast<const __nv_bfloat16*>(x),
+                  int(batch), (long long)k, (long long)ldx, bn, static_cast<uint8_t*>(workspace)));
   GemmPlan p = plan_gemm(n_out, k);
-  CUtensorMap tw, tx;
-  if ((s = make_map_2d(&tw, w, n_out, k, k, kTileM)) != SUN_OK) return s;
-  if ((s = make_map_2d(&tx, x, x_rows, k, ldx, bn)) != SUN_OK) return s;
-  uint8_t* ws = static_cast<uint8_t*>(workspace);
-  unsigned* counters = reinterpret_cast<unsigned*>(ws);
-  float* part = reinterpret_cast<float*>(ws + align_up(size_t(p.m_tiles) * 4, 1024));
-  GemmArgs a = base_args(p, n_out, k, batch, bn, part, counters);
+  GemmArgs a = base_args(p, n_out, k, batch, bn, workspace);
   a.out_f32 = out;
   a.ldo = ldo;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (accumulate) return run_gemm<EPI_RESID_ADD>(tw, tx, a, p, st, false);
-  return run_gemm<EPI_STORE_F32>(tw, tx, a, p, st, false);
+  a.stamps = reinterpret_cast<unsigned long long*>(stamps);
+  return run_gemm<EPI>(wblk, packed, scales, a, p, st, false);
+}
+}  // namespace
+}  // extern "C++"
+
+SunStatus sun_gemm_bf16(const void* w, int64_t n_out, int64_t k, const void* x, int64_t ldx, int64_t x_rows,
+                        int32_t batch, float* out, int64_t ldo, int32_t accumulate, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+  return accumulate ? gemm_api<EPI_RESID_ADD>(w, nullptr, nullptr, n_out, k, x, ldx, x_rows, batch, out, ldo,
+                                              workspace, workspace_bytes, stream, nullptr)
+                    : gemm_api<EPI_STORE_F32>(w, nullptr, nullptr, n_out, k, x, ldx, x_rows, batch, out, ldo,
+                                              workspace, workspace_bytes, stream, nullptr);
+}
+
+SunStatus sun_gemm_bf16_stamped(const void* w, int64_t n_out, int64_t k, const void* x, int64_t ldx,
+                                int64_t x_rows, int32_t batch, float* out, int64_t ldo, int32_t accumulate,
+                                void* workspace, size_t workspace_bytes, void* stream, uint64_t* stamps) {
+  return accumulate ? gemm_api<EPI_RESID_ADD>(w, nullptr, nullptr, n_out, k, x, ldx, x_rows, batch, out, ldo,
+                                              workspace, workspace_bytes, stream, stamps)
+                    : gemm_api<EPI_STORE_F32>(w, nullptr, nullptr, n_out, k, x, ldx, x_rows, batch, out, ldo,
+                                              workspace, workspace_bytes, stream, stamps);
+}
+
+SunStatus sun_gemm_w4(const void* packed, const void* scales, int64_t n_out, int64_t k, const void* x, int64_t ldx,
+                      int64_t x_rows, int32_t batch, float* out, int64_t ldo, int32_t accumulate, void* workspace,
+                      size_t workspace_bytes, void* stream) {
+  if (k % 128 != 0) return fail(SUN_ERR_UNSUPPORTED, "W4 needs k multiple of 128");
+  return accumulate ? gemm_api<EPI_RESID_ADD>(nullptr, packed, scales, n_out, k, x, ldx, x_rows, batch, out, ldo,
+                                              workspace, workspace_bytes, stream, nullptr)
+                    : gemm_api<EPI_STORE_F32>(nullptr, packed, scales, n_out, k, x, ldx, x_rows, batch, out, ldo,
+                                              workspace, workspace_bytes, stream, nullptr);
 }
 
 SunStatus sun_attention_decode(const SunDecoderDims* dims, const SunKvPool* kv, int32_t layer, const void* q,
@@ -686,11 +710,27 @@ SunStatus sun_attention_decode(const SunDecoderDims* dims, const SunKvPool* kv, 
   return run_attention(d, tm, aa, batch, static_cast<cudaStream_t>(stream), false);
 }
 
+SunStatus sun_blocked_bytes(int64_t rows, int64_t k, size_t* bytes) {
+  if (rows < 1 || k < 1 || !bytes) return fail(SUN_ERR_VALUE, "bad shape");
+  *bytes = size_t((rows + kTileM - 1) / kTileM) * size_t((k + kTileK - 1) / kTileK) * kTileWBytes;
+  return SUN_OK;
+}
+
+SunStatus sun_block_weights_bf16(const void* w, int64_t rows, int64_t k, void* out, void* stream) {
+  if (rows < 1 || k < 1 || k % 8 != 0) return fail(SUN_ERR_VALUE, "block_weights: k must be a multiple of 8");
+  const long long m_tiles = (rows + kTileM - 1) / kTileM;
+  const int kb64 = int((k + kTileK - 1) / kTileK);
+  SUN_CUDA(launch(block_weights_kernel, dim3(unsigned(m_tiles * kb64)), dim3(256), 0, static_cast<cudaStream_t>(stream),
+                  false, static_cast<const __nv_bfloat16*>(w), (long long)rows, (long long)k, kb64,
+                  static_cast<uint8_t*>(out)));
+  return SUN_OK;
+}
+
 SunStatus sun_rmsnorm(const float* x, const void* w, void* y, int32_t batch, int32_t h, float eps, void* stream) {
   if (batch < 1 || h % 4 != 0) return fail(SUN_ERR_VALUE, "bad rmsnorm shape");
   SUN_CUDA(launch(rmsnorm_kernel, dim3(batch), dim3(kRowThreads), 0, static_cast<cudaStream_t>(stream), false,
                   (const int*)nullptr, (const __nv_bfloat16*)nullptr, const_cast<float*>(x),
-                  static_cast<const __nv_bfloat16*>(w), static_cast<__nv_bfloat16*>(y), h, (long long)h, eps));
+                  static_cast<const __nv_bfloat16*>(w), static_cast<__nv_bfloat16*>(y), h, (long long)h, eps, 0));
   return SUN_OK;
 }
 

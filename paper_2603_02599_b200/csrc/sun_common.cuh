@@ -101,6 +101,14 @@ SUN_DEVICE void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint
       : "memory");
 }
 
+SUN_DEVICE void bulk_load_hint(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar, uint64_t hint) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(smem_u32(bar)), "l"(hint)
+      : "memory");
+}
+
 // ----------------------------------------------------------------------------
 // Programmatic dependent launch
 // ----------------------------------------------------------------------------
@@ -182,6 +190,32 @@ __host__ __device__ __forceinline__ uint32_t make_idesc_bf16(int M, int N) {
   d |= static_cast<uint32_t>(N >> 3) << 17;       // n_dim
   d |= static_cast<uint32_t>(M >> 4) << 24;       // m_dim
   return d;
+}
+
+// ----------------------------------------------------------------------------
+// thread-block clusters / distributed shared memory
+// ----------------------------------------------------------------------------
+SUN_DEVICE uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+SUN_DEVICE void cluster_sync_all() {
+  __syncwarp();
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Address of the same shared-memory offset in CTA `rank` of this cluster.
+SUN_DEVICE uint32_t dsmem_addr(const void* local, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(smem_u32(local)), "r"(rank));
+  return out;
+}
+SUN_DEVICE float4 ld_dsmem_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
 }
 
 // ----------------------------------------------------------------------------

@@ -34,15 +34,34 @@ def gemm_workspace(n_out: int, k: int, batch: int, device) -> torch.Tensor:
     return torch.zeros(nb.value, dtype=torch.uint8, device=device)
 
 
+def block_weights(w: torch.Tensor) -> torch.Tensor:
+    """bf16 [rows, k] -> SUN-BLK (16 KB pre-swizzled 128x64 blocks), on the GPU."""
+    _need_cuda(w)
+    rows, k = w.shape
+    lib = _lib.load()
+    nb = ctypes.c_size_t()
+    _lib.check(lib.sun_blocked_bytes(rows, k, ctypes.byref(nb)), "sun_blocked_bytes")
+    out = torch.empty(nb.value, dtype=torch.uint8, device=w.device)
+    _lib.check(lib.sun_block_weights_bf16(w.contiguous().data_ptr(), rows, k, out.data_ptr(), _stream()),
+               "sun_block_weights_bf16")
+    return out
+
+
 def gemm_bf16(w: torch.Tensor, x: torch.Tensor, batch: int, out: torch.Tensor | None = None,
-              accumulate: bool = False, workspace: torch.Tensor | None = None) -> torch.Tensor:
+              accumulate: bool = False, workspace: torch.Tensor | None = None,
+              shape: tuple[int, int] | None = None) -> torch.Tensor:
     """out[b, n] (=|+=) sum_k w[n, k] x[b, k] with the tcgen05 swap-AB GEMM.
 
+    ``w`` is bf16 [n, k] (blocked here) or already SUN-BLK uint8 with ``shape``.
     ``x`` must have at least round_up(batch, 16) rows (rows >= batch are ignored).
     """
     _need_cuda(w, x)
-    assert w.dtype == torch.bfloat16 and x.dtype == torch.bfloat16
-    n_out, k = w.shape
+    assert x.dtype == torch.bfloat16
+    if w.dtype == torch.bfloat16:
+        n_out, k = w.shape
+        w = block_weights(w)
+    else:
+        n_out, k = shape
     if out is None:
         out = torch.zeros(batch, n_out, dtype=torch.float32, device=w.device)
     if workspace is None:
@@ -51,6 +70,20 @@ def gemm_bf16(w: torch.Tensor, x: torch.Tensor, batch: int, out: torch.Tensor | 
     _lib.check(lib.sun_gemm_bf16(w.data_ptr(), n_out, k, x.data_ptr(), x.stride(0), x.shape[0], batch,
                                  out.data_ptr(), out.stride(0), int(accumulate), workspace.data_ptr(),
                                  workspace.numel(), _stream()), "sun_gemm_bf16")
+    return out
+
+
+def gemm_w4(packed: torch.Tensor, scales: torch.Tensor, n_out: int, k: int, x: torch.Tensor, batch: int,
+            out: torch.Tensor | None = None, accumulate: bool = False) -> torch.Tensor:
+    """QSUN W4A16 GEMM: out[b, n] (=|+=) sum_k deq(w)[n, k] x[b, k]."""
+    _need_cuda(packed, scales, x)
+    if out is None:
+        out = torch.zeros(batch, n_out, dtype=torch.float32, device=x.device)
+    ws = gemm_workspace(n_out, k, batch, x.device)
+    lib = _lib.load()
+    _lib.check(lib.sun_gemm_w4(packed.data_ptr(), scales.data_ptr(), n_out, k, x.data_ptr(), x.stride(0), x.shape[0],
+                               batch, out.data_ptr(), out.stride(0), int(accumulate), ws.data_ptr(), ws.numel(),
+                               _stream()), "sun_gemm_w4")
     return out
 
 

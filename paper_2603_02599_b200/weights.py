@@ -98,7 +98,10 @@ class DeviceWeights:
         to = lambda t: t.to(dev, non_blocking=True).contiguous()  # noqa: E731
         self.embed = to(w["embed"])
         self.final_norm = to(w["final_norm"])
-        self.lm_head = self.embed if spec.tie_embeddings else to(w["lm_head"])
+        # lm_head stays bf16, stored SUN-BLK for the GEMM stream
+        self.lm_head = kernels.block_weights(self.embed if spec.tie_embeddings else to(w["lm_head"]))
+        if free_source and not spec.tie_embeddings:
+            w.pop("lm_head", None)
         cos, sin = rope_tables(max_context, spec.head_dim, spec.rope_theta)
         self.rope_cos, self.rope_sin = cos.to(dev), sin.to(dev)
         self.layers = []
@@ -107,13 +110,15 @@ class DeviceWeights:
             qkv = torch.cat([to(w[f"l{l}.wq"]), to(w[f"l{l}.wk"]), to(w[f"l{l}.wv"])])
             gu = interleave_gate_up(to(w[f"l{l}.wg"]), to(w[f"l{l}.wu"]))
             mats = {"qkv": qkv, "o": to(w[f"l{l}.wo"]), "gate_up": gu, "down": to(w[f"l{l}.wd"])}
+            del qkv, gu
             if spec.qkv_bias:
                 L["b_qkv"] = torch.cat([to(w[f"l{l}.bq"]), to(w[f"l{l}.bk"]), to(w[f"l{l}.bv"])])
             for name, m in mats.items():
                 if spec.weight_bits == 4:
                     L["w_" + name], L["s_" + name] = kernels.quantize_w4(m, spec.group_size)
                 else:
-                    L["w_" + name] = m
+                    L["w_" + name] = kernels.block_weights(m)
+                del m
             if free_source:
                 for k in ("wq", "wk", "wv", "wo", "wg", "wu", "wd"):
                     w.pop(f"l{l}.{k}", None)
@@ -135,10 +140,7 @@ class DeviceWeights:
 
     def nbytes(self) -> int:
         n = sum(t.numel() * t.element_size() for L in self.layers for t in L.values())
-        n += self.embed.numel() * 2 + self.final_norm.numel() * 2
-        if self.lm_head is not self.embed:
-            n += self.lm_head.numel() * 2
-        return n
+        return n + self.embed.numel() * 2 + self.final_norm.numel() * 2 + self.lm_head.numel()
 
 
 def std_layout_to_cpu(w: dict) -> dict:

@@ -101,3 +101,42 @@ def test_rmsnorm_matches_fp32(cuda):
     y = kernels.rmsnorm(x.to(cuda), w.to(cuda), 1e-5).cpu()
     ref = x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + 1e-5) * w.float()
     torch.testing.assert_close(y.float(), ref, rtol=8e-3, atol=1e-2)
+
+
+@pytest.mark.parametrize("rows,k", [(256, 256), (300, 512), (4096, 4096)])
+def test_w4_quantizer_bit_exact_vs_oracle(cuda, rows, k):
+    """GPU quantiser == oracle restatement of SUN-W4, byte for byte (valid rows)."""
+    import numpy as np
+
+    from oracle import quant_ref
+    from paper_2603_02599_b200 import kernels
+
+    g = torch.Generator(device="cpu").manual_seed(rows + k)
+    w = (torch.randn(rows, k, generator=g) * 0.02).to(torch.bfloat16)
+    w[0, :128] = 0  # all-zero group -> scale 0, q 0
+    packed, scales = kernels.quantize_w4(w.to(cuda))
+    q, s = quant_ref.quantize(w)
+    p_ref, s_ref = quant_ref.pack(q, s)
+    rows_pad = (rows + 127) // 128 * 128
+    pg = packed.cpu().numpy().reshape(rows_pad // 128, k // 128, 128, 64).transpose(0, 2, 1, 3).reshape(rows_pad, -1)
+    pr = p_ref.reshape(rows_pad // 128, k // 128, 128, 64).transpose(0, 2, 1, 3).reshape(rows_pad, -1)
+    assert np.array_equal(pg[:rows], pr[:rows])
+    assert np.array_equal(scales.cpu().view(torch.int16).numpy().astype(np.uint16)[:, :rows], s_ref[:, :rows])
+    assert torch.equal(quant_ref.unpack(packed.cpu().numpy(), rows, k), q)
+
+
+@pytest.mark.parametrize("n_out,k,batch", [(256, 256, 1), (768, 512, 8), (4096, 4096, 64), (1536, 14336, 128),
+                                           (28672, 4096, 128), (512, 128, 256)])
+def test_gemm_w4_matches_dequantized_fp32(cuda, n_out, k, batch):
+    from oracle import quant_ref
+    from paper_2603_02599_b200 import kernels
+
+    g = torch.Generator(device="cpu").manual_seed(n_out + k + batch)
+    w = (torch.randn(n_out, k, generator=g) * 0.02).to(torch.bfloat16)
+    x = torch.randn(_r16(batch), k, generator=g).to(torch.bfloat16)
+    packed, scales = kernels.quantize_w4(w.to(cuda))
+    out = kernels.gemm_w4(packed, scales, n_out, k, x.to(cuda), batch).cpu()
+    q, s = quant_ref.quantize(w)
+    deq = quant_ref.dequantize(q, s)  # bf16(q * s): the exact tcgen05 operand
+    ref = x[:batch].float() @ deq.float().t()
+    torch.testing.assert_close(out, ref, rtol=1e-4, atol=1e-4 * math.sqrt(k))
