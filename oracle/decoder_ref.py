@@ -70,9 +70,9 @@ def rope_tables(max_pos: int, head_dim: int, theta: float) -> tuple[torch.Tensor
     return torch.cos(ang).float(), torch.sin(ang).float()
 
 
-def rmsnorm(x: torch.Tensor, g: torch.Tensor, eps: float) -> torch.Tensor:
+def rmsnorm(x: torch.Tensor, g: torch.Tensor, eps: float, rnd=None) -> torch.Tensor:
     r = torch.rsqrt((x * x).mean(-1, keepdim=True) + eps)
-    return bf(x * r * g.float())
+    return (rnd or bf)(x * r * g.float())
 
 
 def rope(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor:
@@ -95,17 +95,20 @@ class OracleDecoder:
     ffn_norm, wg [f,h], wu [f,h], wd [h,f].
     """
 
-    def __init__(self, spec: OracleSpec, weights: dict, max_pos: int):
+    def __init__(self, spec: OracleSpec, weights: dict, max_pos: int, round_bf16: bool = True):
+        """round_bf16=False drops every bf16 storage rounding (pure fp32 model), the
+        mode used to pin the block definition against transformers' Llama / Qwen2."""
         self.s = spec
         self.w = {k: (v.float() if torch.is_tensor(v) else v) for k, v in weights.items()}
         self.cos, self.sin = rope_tables(max_pos, spec.head_dim, spec.rope_theta)
+        self.rnd = bf if round_bf16 else (lambda x: x)
 
     # -- one layer over T new positions of one sequence ------------------------------
     def _layer(self, l: int, resid: torch.Tensor, pos: torch.Tensor, kcache: list, vcache: list):
         s, w = self.s, self.w
         d, nq, nkv = s.head_dim, s.n_q_heads, s.n_kv_heads
         T = resid.shape[0]
-        xn = rmsnorm(resid, w[f"l{l}.attn_norm"], s.rms_eps)
+        xn = rmsnorm(resid, w[f"l{l}.attn_norm"], s.rms_eps, self.rnd)
         q = xn @ w[f"l{l}.wq"].t()
         k = xn @ w[f"l{l}.wk"].t()
         v = xn @ w[f"l{l}.wv"].t()
@@ -114,9 +117,9 @@ class OracleDecoder:
             k = k + w[f"l{l}.bk"]
             v = v + w[f"l{l}.bv"]
         cs, sn = self.cos[pos][:, None, :], self.sin[pos][:, None, :]
-        q = bf(rope(q.view(T, nq, d), cs, sn))
-        k = bf(rope(k.view(T, nkv, d), cs, sn))
-        v = bf(v.view(T, nkv, d))
+        q = self.rnd(rope(q.view(T, nq, d), cs, sn))
+        k = self.rnd(rope(k.view(T, nkv, d), cs, sn))
+        v = self.rnd(v.view(T, nkv, d))
         K = torch.cat([kcache[l], k], 0) if kcache[l] is not None else k
         V = torch.cat([vcache[l], v], 0) if vcache[l] is not None else v
         kcache[l], vcache[l] = K, V
@@ -128,12 +131,12 @@ class OracleDecoder:
             causal = torch.arange(K.shape[0])[None, :] > (n_past + torch.arange(T))[:, None]
             sc = sc.masked_fill(causal, float("-inf"))
             out[:, h, :] = torch.softmax(sc, dim=-1) @ V[:, h // G, :]
-        attn = bf(out.reshape(T, nq * d))
+        attn = self.rnd(out.reshape(T, nq * d))
         resid = resid + attn @ w[f"l{l}.wo"].t()
-        xn = rmsnorm(resid, w[f"l{l}.ffn_norm"], s.rms_eps)
+        xn = rmsnorm(resid, w[f"l{l}.ffn_norm"], s.rms_eps, self.rnd)
         g = xn @ w[f"l{l}.wg"].t()
         u = xn @ w[f"l{l}.wu"].t()
-        act = bf(g / (1.0 + torch.exp(-g)) * u)
+        act = self.rnd(g / (1.0 + torch.exp(-g)) * u)
         return resid + act @ w[f"l{l}.wd"].t()
 
     def forward(self, tokens: list[int], start: int, cache: dict | None):
@@ -149,7 +152,7 @@ class OracleDecoder:
         resid = w["embed"][torch.tensor(tokens)].clone()
         for l in range(s.n_layers):
             resid = self._layer(l, resid, pos, cache["k"], cache["v"])
-        xn = rmsnorm(resid[-1:], w["final_norm"], s.rms_eps)
+        xn = rmsnorm(resid[-1:], w["final_norm"], s.rms_eps, self.rnd)
         logits = (xn @ w["lm_head"].t())[0]
         return logits, cache
 
