@@ -51,6 +51,16 @@ class CostParams:
         return cls(**data)
 
 
+def prefill_time(model: ModelProfile, isl: int, params: CostParams, gpu: GpuSpec) -> float:
+    """Analytic prefill price (costmodel.py:86-98): affine in prompt tokens, with
+    the dequantisation penalty when prefill weights are low-bit. The prefill
+    module is producer-side; the simulator uses this for its event times."""
+    if isl < 1:
+        raise ValueError(f"isl must be >= 1, got {isl}")
+    penalty = params.dequant_compute_penalty if model.prefill_weight_bits < 16 else 1.0
+    return params.prefill_fixed_overhead + penalty * (isl * params.prefill_flops_per_token / (params.mfu * gpu.flops))
+
+
 def decode_step_time_from_totals(total_kv_bytes: float, decoder_weight_bytes: float, params: CostParams,
                                  gpu: GpuSpec) -> float:
     """Weights read once per step + the batch's KV, over effective bandwidth."""
