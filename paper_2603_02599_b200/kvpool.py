@@ -65,5 +65,26 @@ class PageAllocator:
         out = [self._free.pop() for _ in range(n)]
         return out
 
+    def alloc_contiguous(self, n: int) -> list[int]:
+        """n consecutive page ids if such a run is free (so a hand-off payload can
+        land in place), otherwise any n pages."""
+        if n > len(self._free):
+            raise OverCapacity(f"need {n} KV pages, {len(self._free)} free")
+        free = sorted(self._free)
+        run_start, run_len = free[0], 1
+        for prev, p in zip(free, free[1:]):
+            if run_len >= n:
+                break
+            if p == prev + 1:
+                run_len += 1
+            else:
+                run_start, run_len = p, 1
+        if run_len >= n:
+            pages = list(range(run_start, run_start + n))
+            taken = set(pages)
+            self._free = [p for p in self._free if p not in taken]
+            return pages
+        return self.alloc(n)
+
     def free(self, pages: list[int]) -> None:
         self._free.extend(reversed(pages))

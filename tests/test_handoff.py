@@ -1,0 +1,76 @@
+"""KV hand-off protocol between two processes (gloo, world_size 2, CPU): the
+decode side receives exactly the prefill side's pages, into its own page ids,
+with the KvHandle fields preserved (domain.py:96-113)."""
+import os
+import socket
+
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2603_02599_b200.handoff import page_runs, recv_kv, send_kv
+from paper_2603_02599_b200.kvpool import KvPool, PageAllocator
+from paper_2603_02599_b200.spec import TINY
+from paper_2603_02599_b200.sun_types import KvHandle
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        pool = KvPool(TINY, 24, "cpu")
+        g = torch.Generator().manual_seed(100 + rank)
+        pool.tensor.copy_(torch.randn(pool.tensor.shape, generator=g).to(torch.bfloat16))
+        alloc = PageAllocator(pool.num_pages)
+        if rank == 0:  # prefill side: two requests, scattered and contiguous pages
+            out = []
+            for rid, pages in ((7, [5, 2, 9]), (8, [11, 12, 13, 14])):
+                h = KvHandle(request_id=rid, resident_tokens=len(pages) * 16 - 3, bytes_per_token=TINY.kv_bytes_per_token,
+                             pages=pages, model_id=rid % 2)
+                send_kv(h, pool, 1)
+                out.append(pool.tensor[pages].clone())
+            q.put(("sent", out))
+        else:  # decode side
+            alloc.alloc(3)  # pool partly in use already
+            got = []
+            for _ in range(2):
+                h = recv_kv(pool, alloc, 0)
+                got.append((h.request_id, h.resident_tokens, h.bytes_per_token, h.model_id, list(h.pages),
+                            pool.tensor[h.pages].clone()))
+            q.put(("recv", got, alloc.free_pages))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_kv_handoff_two_ranks_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((m[0], m[1:]) for m in (q.get(timeout=120), q.get(timeout=120)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    sent = res["sent"][0]
+    got, free_after = res["recv"]
+    assert [g[0] for g in got] == [7, 8]
+    assert got[0][1] == 3 * 16 - 3 and got[0][2] == TINY.kv_bytes_per_token and got[0][3] == 1
+    for (payload, g) in zip(sent, got):
+        assert torch.equal(payload, g[5])
+        assert len(page_runs(g[4])) == 1  # landed in a contiguous run of the receiver's pool
+    assert free_after == 24 - 3 - 3 - 4
+
+
+def test_page_runs():
+    assert page_runs([3, 4, 5, 9, 10, 2]) == [(3, 3), (9, 2), (2, 1)]
+    assert page_runs([]) == []
