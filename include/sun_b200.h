@@ -143,7 +143,7 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
 
 /* Same step, serialised, with a CUDA event after every kernel: kernel_ms[i] is the
  * device time of the i-th launch (order: embed+norm, then per layer [norm], qkv,
- * attention, combine, o, norm, gate_up, down; final norm, lm_head, argmax).
+ * attention (split combine fused), o, norm, gate_up, down; final norm, lm_head, argmax).
  * Synchronises the stream. For measurement only. */
 SunStatus sun_decode_step_profile(SunDecoder* dec, const int32_t* tokens, const int32_t* positions,
                                   const int32_t* block_tables, int32_t bt_stride, int32_t batch,
@@ -163,9 +163,9 @@ SunStatus sun_gemm_bf16(const void* w, int64_t n_out, int64_t k, const void* x, 
                         int32_t batch, float* out, int64_t ldo, int32_t accumulate, void* workspace,
                         size_t workspace_bytes, void* stream);
 
-/* sun_gemm_bf16 with per-CTA %globaltimer stamps (stamps: uint64 [148][8]; slots:
+/* sun_gemm_bf16 with per-CTA %globaltimer stamps (stamps: uint64 [grid][16]; slots:
  * 0 start, 1 setup done, 2 first stage landed, 3 last MMA issued, 4 first
- * accumulator ready, 5 epilogue done, 6 exit). Profiling aid. */
+ * accumulator ready, 5 epilogue done, 6 exit, 8-11 cluster reduction phases). Profiling aid. */
 SunStatus sun_gemm_bf16_stamped(const void* w, int64_t n_out, int64_t k, const void* x, int64_t ldx,
                                 int64_t x_rows, int32_t batch, float* out, int64_t ldo, int32_t accumulate,
                                 void* workspace, size_t workspace_bytes, void* stream, uint64_t* stamps);

@@ -6,8 +6,9 @@
 // K/V pages are staged by TMA (3-D tensor map over the page pool, SWIZZLE_128B,
 // 16-token x 128 B boxes) into per-warp mbarrier rings; each warp consumes every
 // NWARPS-th page with ldmatrix + mma.sync, online softmax in fp32 with
-// quad-shuffle reductions, then the warps merge through shared memory and the
-// unit's (m, l, O) partial goes to global memory for the split combine.
+// quad-shuffle reductions, then the warps merge through shared memory. A
+// single-split sequence writes its output directly; otherwise each split
+// publishes (m, l, O) and the last-arriving split merges them (fused combine).
 //
 // Replaces the KV term `sum(resident_tokens * kv_bytes_per_token)` of the
 // reference step price (poolsim costmodel.py:112, 139; engine.py:427-428).
@@ -34,7 +35,18 @@ struct AttnArgs {
   __nv_bfloat16* out;      // [B][n_q_heads * D]   (combine output)
   long long ld_out;
   int act_rows;            // > 0: write `out` in SUN-ACT (the O-projection operand)
+  unsigned* counters;      // [B][n_kv_heads] split arrival counters (zeroed once, self-resetting)
+  int fused_combine;       // 1: last split merges in-kernel; 0: attn_combine_kernel does it
 };
+
+template <int D>
+SUN_DEVICE void store_attn_out(const AttnArgs& a, int b, int head, int dim, float v) {
+  const __nv_bfloat16 o = __float2bfloat16_rn(v);
+  if (a.act_rows > 0)
+    *reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<uint8_t*>(a.out) + act_offset(b, head * D + dim, a.act_rows)) = o;
+  else
+    a.out[static_cast<long long>(b) * a.ld_out + head * D + dim] = o;
+}
 
 template <int D>
 struct AttnCfg {
@@ -61,6 +73,7 @@ __global__ void __launch_bounds__(128)
   const int kvh = blockIdx.y;
   const int b = blockIdx.z;
   pdl_wait();
+  pdl_launch_dependents();  // early: the next kernel may start its prologue / weight prefetch
   const int ctx = a.positions[b] + 1;
   const int n_pages = (ctx + kPageTokens - 1) / kPageTokens;
   const int p0 = split * a.pages_per_split;
@@ -219,6 +232,7 @@ __global__ void __launch_bounds__(128)
     }
   }
   __syncthreads();
+  const int n_splits = a.fused_combine ? (n_pages + a.pages_per_split - 1) / a.pages_per_split : 0;
   for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
     const int gg = idx / D;
     const int dim = idx % D;
@@ -234,6 +248,10 @@ __global__ void __launch_bounds__(128)
       ll += merge_ml[(w * 8 + gg) * 2 + 1] * sc;
     }
     const int head = kvh * G + gg;
+    if (n_splits == 1) {  // whole context in this CTA: emit the output directly
+      store_attn_out<D>(a, b, head, dim, acc / ll);
+      continue;
+    }
     const long long u = (static_cast<long long>(b) * a.n_q_heads + head) * a.max_splits + split;
     a.part_o[u * D + dim] = acc;
     if (dim == 0) {
@@ -241,13 +259,46 @@ __global__ void __launch_bounds__(128)
       a.part_ml[u * 2 + 1] = ll;
     }
   }
-  pdl_launch_dependents();
+  if (a.fused_combine && n_splits > 1) {
+    // split-K combine fused in: the last-arriving split of (b, kv head) merges
+    // all splits in split order (deterministic) and writes the GQA group's output
+    __shared__ int is_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned* cnt = a.counters + static_cast<long long>(b) * a.n_kv_heads + kvh;
+      const unsigned prev = atomicAdd(cnt, 1u);
+      is_last = prev == static_cast<unsigned>(n_splits - 1);
+      if (is_last) *cnt = 0u;
+    }
+    __syncthreads();
+    if (is_last) {
+      __threadfence();
+      for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
+        const int gg = idx / D;
+        const int dim = idx % D;
+        const int head = kvh * G + gg;
+        const long long u0 = (static_cast<long long>(b) * a.n_q_heads + head) * a.max_splits;
+        float mm = -INFINITY;
+        for (int s2 = 0; s2 < n_splits; ++s2) mm = fmaxf(mm, __ldcg(&a.part_ml[(u0 + s2) * 2]));
+        float acc = 0.f, ll = 0.f;
+        for (int s2 = 0; s2 < n_splits; ++s2) {
+          const float sc = exp2f(__ldcg(&a.part_ml[(u0 + s2) * 2]) - mm);
+          acc += __ldcg(&a.part_o[(u0 + s2) * D + dim]) * sc;
+          ll += __ldcg(&a.part_ml[(u0 + s2) * 2 + 1]) * sc;
+        }
+        store_attn_out<D>(a, b, head, dim, acc / ll);
+      }
+    }
+  }
 }
 
-// Merge the split partials of one (sequence, query head) and emit bf16 output.
+// Merge the split partials of one (sequence, query head) and emit the bf16
+// output (used when fused_combine == 0: all (b, head) merged in parallel).
 template <int D>
 __global__ void __launch_bounds__(128) attn_combine_kernel(const AttnArgs a) {
   pdl_wait();
+  pdl_launch_dependents();
   const int head = blockIdx.x;
   const int b = blockIdx.y;
   const int ctx = a.positions[b] + 1;
@@ -263,13 +314,8 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(const AttnArgs a) {
       acc += a.part_o[(u0 + s) * D + dim] * sc;
       ll += a.part_ml[(u0 + s) * 2 + 1] * sc;
     }
-    const __nv_bfloat16 o = __float2bfloat16_rn(acc / ll);
-    if (a.act_rows > 0)
-      *reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<uint8_t*>(a.out) + act_offset(b, head * D + dim, a.act_rows)) = o;
-    else
-      a.out[static_cast<long long>(b) * a.ld_out + head * D + dim] = o;
+    store_attn_out<D>(a, b, head, dim, acc / ll);
   }
-  pdl_launch_dependents();
 }
 
 }  // namespace sun

@@ -30,6 +30,7 @@ __global__ void __launch_bounds__(kRowThreads)
                    __nv_bfloat16* __restrict__ out, int h, long long ld_out, float eps, int act_rows) {
   __shared__ float red[kRowThreads / 32];
   pdl_wait();
+  pdl_launch_dependents();
   const int b = blockIdx.x;
   float* x = resid + static_cast<long long>(b) * h;
   if (tokens != nullptr) {
@@ -61,7 +62,6 @@ __global__ void __launch_bounds__(kRowThreads)
     *reinterpret_cast<__nv_bfloat162*>(dst) = o01;  // 4 consecutive columns stay in one 16-byte chunk
     *reinterpret_cast<__nv_bfloat162*>(dst + 2) = o23;
   }
-  pdl_launch_dependents();
 }
 
 // next[b] = argmax over lm_head tiles (ties -> lowest vocabulary index). With
@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(kRowThreads)
   __shared__ float sv[kRowThreads / 32];
   __shared__ int si[kRowThreads / 32];
   pdl_wait();
+  pdl_launch_dependents();
   const int b = blockIdx.x;
   float bv = -INFINITY;
   int bi = 0x7fffffff;
@@ -110,7 +111,6 @@ __global__ void __launch_bounds__(kRowThreads)
       positions[b] += 1;
     }
   }
-  pdl_launch_dependents();
 }
 
 }  // namespace sun

@@ -88,7 +88,7 @@ SUN_DEVICE unsigned long long gtimer() {
   return t;
 }
 #define SUN_STAMP(i) \
-  do { if (a.stamps) a.stamps[blockIdx.x * 8 + (i)] = gtimer(); } while (0)
+  do { if (a.stamps) a.stamps[blockIdx.x * 16 + (i)] = gtimer(); } while (0)
 
 constexpr int kGemmThreads = 192;
 constexpr int kW4Threads = 320;
@@ -421,6 +421,10 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) SUN_STAMP(1);
+  // Early trigger: the next kernel may launch now and run its prologue (and, for
+  // a GEMM, its weight prefetch) as SMs free up; its griddepcontrol.wait still
+  // orders every dependent memory access after this grid completes.
+  pdl_launch_dependents();
 
   auto nblk_of = [&](int ks) { return min(2, a.kb64 - 2 * ks); };
 
@@ -516,15 +520,17 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
         epi_bar();
         if (threadIdx.x == 64) mbar_arrive(&tempty[buf]);
       } else {
-        // park the partial in (now idle) shared memory: [128 rows][bn + 4] fp32
+        // park the partial in (now idle) shared memory, chunk-major
+        // [bn/16][128 rows][16] fp32: a warp's DSMEM reads of one chunk are then
+        // 2 KB contiguous (row-major rows 272 B apart made them 16-byte gathers)
         float* part = reinterpret_cast<float*>(smem);
-        const int ld = a.bn + 4;
         float v[16];
         for (int c0 = 0; c0 < a.bn; c0 += 16) {
           tmem_ld16(taddr + c0, v);
+          float* dst = part + ((c0 >> 4) * kTileM + row_local) * 16;
 #pragma unroll
           for (int j = 0; j < 16; j += 4)
-            *reinterpret_cast<float4*>(part + row_local * ld + c0 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
         }
       }
     }
@@ -547,12 +553,13 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
   }
 
   if (clustered) {
+    if (threadIdx.x == 64) SUN_STAMP(8);
     cluster_sync_all();  // every rank's partial is visible cluster-wide
+    if (threadIdx.x == 64) SUN_STAMP(9);
     if (warp >= 2 && warp < 6) {
       const int q = warp & 3;
       const int row_local = q * 32 + (threadIdx.x & 31);
       float* part = reinterpret_cast<float*>(smem);
-      const int ld = a.bn + 4;
       float* red_val = epi + 16 * kTileM;
       int* red_idx = reinterpret_cast<int*>(red_val + 64);
       for (int c0 = static_cast<int>(rank) * 16; c0 < a.bn; c0 += static_cast<int>(S) * 16) {
@@ -565,7 +572,7 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
           for (int u = 0; u < 4; ++u)
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-              x[u][j] = (r0 + u < S) ? ld_dsmem_f4(dsmem_addr(part + row_local * ld + c0 + 4 * j, r0 + u))
+              x[u][j] = (r0 + u < S) ? ld_dsmem_f4(dsmem_addr(part + ((c0 >> 4) * kTileM + row_local) * 16 + 4 * j, r0 + u))
                                      : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
           for (int u = 0; u < 4; ++u)
@@ -577,13 +584,14 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
               v[4 * j + 3] += x[u][j].w;
             }
         }
+        if (threadIdx.x == 64) SUN_STAMP(10);
         epi_chunk<EPI>(a, t_lo, row_local, c0, v, epi, red_val, red_idx);
+        if (threadIdx.x == 64) SUN_STAMP(11);
       }
     }
     cluster_sync_all();  // nobody exits while a peer may still read its partial
   }
   if (threadIdx.x == 64) SUN_STAMP(5);
-  pdl_launch_dependents();
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {

@@ -8,6 +8,7 @@
 // previous kernel's tail). Declared in include/sun_b200.h.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -115,10 +116,23 @@ GemmPlan plan_gemm(int64_t n_out, int64_t k) {
   return p;
 }
 
-constexpr int kSmemBudget = 220 * 1024;
+constexpr int kSmemPerSm = 226 * 1024;  // usable dynamic smem per SM (227 KB minus reserve)
 
-int gemm_stages(int bn, bool w4) {
-  const int avail = kSmemBudget - 1024 - (w4 ? 2 * int(kW4DeqBytes) : 0) - int(kEpiSmemBytes) - 512;
+// CTAs per SM for a GEMM. 1 (deep pipeline, ~200 KB smem) measured faster than
+// 2 x ~108 KB on B200 for C3 (5.62 vs 5.83 ms/step); SUN_GEMM_CTAS_PER_SM=2
+// selects the two-CTA variant (needs two double-buffered TMEM accumulators).
+int gemm_ctas_per_sm(int bn, bool w4) {
+  static int forced = [] {
+    const char* e = getenv("SUN_GEMM_CTAS_PER_SM");
+    return e ? atoi(e) : 1;
+  }();
+  if (forced == 2 && !w4 && 2 * tmem_cols_for(bn) <= 512) return 2;
+  return 1;
+}
+
+int gemm_stages(int bn, bool w4, int per_sm) {
+  const int budget = kSmemPerSm / per_sm - 2048;
+  const int avail = budget - 1024 - (w4 ? 2 * int(kW4DeqBytes) : 0) - int(kEpiSmemBytes) - 512;
   int st = avail / int(gemm_stage_bytes(bn, w4));
   return std::max(2, std::min(6, st));
 }
@@ -129,7 +143,14 @@ int round16(int b) { return (b + 15) / 16 * 16; }
 
 template <typename K>
 void set_max_smem(K kern) {
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  cudaFuncAttributes fa;
+  size_t static_bytes = 0;
+  if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess) static_bytes = fa.sharedSizeBytes;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(227 * 1024 - static_bytes)) !=
+      cudaSuccess) {
+    fprintf(stderr, "sun_b200: cudaFuncSetAttribute(max dynamic smem) failed\n");
+    cudaGetLastError();
+  }
 }
 
 std::once_flag g_attr_once;
@@ -146,6 +167,7 @@ void init_kernel_attrs() {
     set_max_smem(gemm_kernel<EPI_SWIGLU, true>);
     set_max_smem(attn_decode_kernel<64>);
     set_max_smem(attn_decode_kernel<128>);
+    (void)0;
   });
 }
 
@@ -237,10 +259,11 @@ cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, c
 
 // Workspace layout shared by sizing and creation.
 struct WsLayout {
-  size_t resid, xn, q, attn, act, part_o, part_ml, amax_val, amax_idx, logits, total;
+  size_t resid, xn, q, attn, act, part_o, part_ml, attn_cnt, amax_val, amax_idx, logits, total;
   int max_splits;
 };
 
+int d_cnt_heads(const SunDecoderDims& d) { return d.n_kv_heads; }
 int gu_rows(const SunDecoderDims& d) { return (d.ffn + 63) / 64 * 128; }
 int qkv_rows(const SunDecoderDims& d) { return (d.n_q_heads + 2 * d.n_kv_heads) * d.head_dim; }
 
@@ -264,6 +287,7 @@ WsLayout layout_ws(const SunDecoderDims& d, int max_batch) {
   w.act = take(act_bytes(d.ffn));
   w.part_o = take(size_t(max_batch) * d.n_q_heads * w.max_splits * d.head_dim * 4);
   w.part_ml = take(size_t(max_batch) * d.n_q_heads * w.max_splits * 2 * 4);
+  w.attn_cnt = take(size_t(max_batch) * d.n_kv_heads * 4);
   const int lm_tiles = (d.vocab + kTileM - 1) / kTileM;
   w.amax_val = take(size_t(lm_tiles) * bmp * 4);
   w.amax_idx = take(size_t(lm_tiles) * bmp * 4);
@@ -308,6 +332,7 @@ struct SunDecoder {
   float* resid;
   __nv_bfloat16 *xn, *q, *attn, *act;  // xn / attn / act in SUN-ACT (GEMM operands)
   float *part_o, *part_ml, *amax_val, *logits;
+  unsigned* attn_cnt;
   int* amax_idx;
   GemmPlan p_qkv, p_o, p_gu, p_down, p_lm;
 };
@@ -330,9 +355,9 @@ GemmArgs base_args(const GemmPlan& p, int64_t n_out, int64_t k, int batch, int b
 
 // Cluster split factor for a GEMM with <= 148 tiles: the largest S <= 8 (and
 // <= k-steps) whose m_tiles clusters of S CTAs are co-resident in one wave.
-int cluster_splits(const GemmPlan& p, size_t smem, bool w4) {
-  if (p.m_tiles > kNumSms) return 1;
-  int s = std::min(std::min(8, kNumSms / std::max(1, p.m_tiles)), p.ksteps);
+int cluster_splits(const GemmPlan& p, size_t smem, bool w4, int slots) {
+  if (p.m_tiles > slots) return 1;
+  int s = std::min(std::min(8, slots / std::max(1, p.m_tiles)), p.ksteps);
   while (s > 1 && max_active_clusters(unsigned(s), smem, w4) < p.m_tiles) --s;
   return std::max(1, s);
 }
@@ -345,11 +370,13 @@ SunStatus run_gemm(const void* wblk, const void* packed, const void* scales, Gem
   a.wblk = static_cast<const uint8_t*>(wblk);
   a.w4_packed = static_cast<const uint8_t*>(packed);
   a.w4_scales = static_cast<const __nv_bfloat16*>(scales);
-  a.stages = gemm_stages(a.bn, w4);
+  const int per_sm = gemm_ctas_per_sm(a.bn, w4);
+  const int slots = kNumSms * per_sm;
+  a.stages = gemm_stages(a.bn, w4, per_sm);
   const size_t smem = gemm_smem_bytes(a.bn, a.stages, w4);
-  const int S = cluster_splits(p, smem, w4);
+  const int S = cluster_splits(p, smem, w4, slots);
   a.splits = S;
-  const int grid = S > 1 ? p.m_tiles * S : std::min(p.m_tiles, kNumSms);
+  const int grid = S > 1 ? p.m_tiles * S : std::min(p.m_tiles, slots);
   g_cluster = unsigned(S);
   if (w4) {
     if constexpr (EPI == EPI_LOGITS) return fail(SUN_ERR_UNSUPPORTED, "lm_head is bf16");
@@ -358,6 +385,17 @@ SunStatus run_gemm(const void* wblk, const void* packed, const void* scales, Gem
     SUN_CUDA(launch(gemm_kernel<EPI, false>, dim3(grid), dim3(kGemmThreads), smem, st, pdl, a));
   }
   return SUN_OK;
+}
+
+// Split combine inside the attention kernel (last split merges) or as a separate
+// grid (default: measured faster on B200 for C3, the parallel merge has no
+// serial tail). Env SUN_ATTN_FUSED_COMBINE=1 selects the fused variant.
+int attn_fused_combine() {
+  static int v = [] {
+    const char* e = getenv("SUN_ATTN_FUSED_COMBINE");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
 }
 
 int auto_pages_per_split(const SunDecoderDims& d, int batch) {
@@ -380,10 +418,12 @@ SunStatus run_attention(const SunDecoderDims& d, const CUtensorMap& tm_kv, const
   dim3 grid(aa.max_splits, d.n_kv_heads, batch);
   if (d.head_dim == 128) {
     SUN_CUDA(launch(attn_decode_kernel<128>, grid, dim3(128), AttnCfg<128>::kSmem, st, pdl, tm_kv, aa));
-    SUN_CUDA(launch(attn_combine_kernel<128>, dim3(d.n_q_heads, batch), dim3(128), 0, st, pdl, aa));
+    if (!aa.fused_combine)
+      SUN_CUDA(launch(attn_combine_kernel<128>, dim3(d.n_q_heads, batch), dim3(128), 0, st, pdl, aa));
   } else {
     SUN_CUDA(launch(attn_decode_kernel<64>, grid, dim3(128), AttnCfg<64>::kSmem, st, pdl, tm_kv, aa));
-    SUN_CUDA(launch(attn_combine_kernel<64>, dim3(d.n_q_heads, batch), dim3(128), 0, st, pdl, aa));
+    if (!aa.fused_combine)
+      SUN_CUDA(launch(attn_combine_kernel<64>, dim3(d.n_q_heads, batch), dim3(128), 0, st, pdl, aa));
   }
   return SUN_OK;
 }
@@ -435,6 +475,7 @@ SunStatus sun_decoder_create(const SunDecoderDims* dims, const SunWeights* weigh
   dec->act = reinterpret_cast<__nv_bfloat16*>(ws + dec->L.act);
   dec->part_o = reinterpret_cast<float*>(ws + dec->L.part_o);
   dec->part_ml = reinterpret_cast<float*>(ws + dec->L.part_ml);
+  dec->attn_cnt = reinterpret_cast<unsigned*>(ws + dec->L.attn_cnt);
   dec->amax_val = reinterpret_cast<float*>(ws + dec->L.amax_val);
   dec->amax_idx = reinterpret_cast<int*>(ws + dec->L.amax_idx);
   dec->logits = reinterpret_cast<float*>(ws + dec->L.logits);
@@ -447,8 +488,10 @@ SunStatus sun_decoder_create(const SunDecoderDims* dims, const SunWeights* weigh
   dec->p_down = plan_gemm(d.hidden, d.ffn);
   dec->p_lm = plan_gemm(d.vocab, d.hidden);
   if ((st = make_map_kv(&dec->tm_kv, d, *kv)) != SUN_OK) { delete dec; return st; }
-  // zero the activation buffers once (K padding of SUN-ACT is never written)
+  // zero the activation buffers once (K padding of SUN-ACT is never written) and
+  // the attention split counters (self-resetting afterwards)
   cudaError_t e = cudaMemset(ws, 0, dec->L.part_o);
+  if (e == cudaSuccess) e = cudaMemset(ws + dec->L.attn_cnt, 0, size_t(max_batch) * d_cnt_heads(*dims) * 4);
   if (e != cudaSuccess) {
     delete dec;
     return fail(SUN_ERR_CUDA, "cudaMemset ws: %s", cudaGetErrorString(e));
@@ -497,6 +540,8 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
   aa.out = dec->attn;
   aa.ld_out = qd;
   aa.act_rows = bn;
+  aa.counters = dec->attn_cnt;
+  aa.fused_combine = attn_fused_combine();
 
   // embedding gather + first attention RMSNorm
   SUN_CUDA(launch(rmsnorm_kernel, dim3(batch), dim3(kRowThreads), 0, st, pdl, tokens,
@@ -700,9 +745,13 @@ SunStatus sun_attention_decode(const SunDecoderDims* dims, const SunKvPool* kv, 
   aa.scale_log2 = 1.4426950408889634f / sqrtf(float(d.head_dim));
   const size_t po = size_t(batch) * d.n_q_heads * aa.max_splits * d.head_dim * 4;
   const size_t pm = size_t(batch) * d.n_q_heads * aa.max_splits * 2 * 4;
-  if (workspace_bytes < align_up(po, 1024) + pm) return fail(SUN_ERR_CAPACITY, "attention workspace too small");
+  const size_t pc = size_t(batch) * d.n_kv_heads * 4;
+  if (workspace_bytes < align_up(po, 1024) + align_up(pm, 1024) + pc)
+    return fail(SUN_ERR_CAPACITY, "attention workspace too small");
   aa.part_o = static_cast<float*>(workspace);
   aa.part_ml = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + align_up(po, 1024));
+  aa.counters = reinterpret_cast<unsigned*>(static_cast<uint8_t*>(workspace) + align_up(po, 1024) + align_up(pm, 1024));
+  aa.fused_combine = attn_fused_combine();
   aa.out = static_cast<__nv_bfloat16*>(out);
   aa.ld_out = d.n_q_heads * d.head_dim;
   CUtensorMap tm;

@@ -46,6 +46,8 @@ class _StepRunner:
                                           self.max_batch, int(use_pdl), ctypes.byref(h)), "sun_decoder_create")
         self._h = h
         self._lib = lib
+        import os as _os
+        self.fused_combine = _os.environ.get("SUN_ATTN_FUSED_COMBINE", "0") == "1"
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -88,7 +90,8 @@ class _StepRunner:
         for l in range(self.spec.n_layers):
             if l > 0:
                 names.append("rmsnorm")
-            names += ["gemm_qkv_rope_kv", "attention", "attn_combine", "gemm_o_resid", "rmsnorm",
+            names += ["gemm_qkv_rope_kv", "attention"] + ([] if self.fused_combine else ["attn_combine"]) + [
+                "gemm_o_resid", "rmsnorm",
                       "gemm_gate_up_swiglu", "gemm_down_resid"]
         return names + ["rmsnorm", "gemm_lm_head_argmax", "argmax"]
 
