@@ -178,14 +178,15 @@ class CpuOracleStep:
 
     def step(self) -> float:
         """Seconds of one extrapolated full decode step."""
-        from oracle.decoder_ref import decode_batch_layers, rmsnorm
+        from oracle.decoder_ref import decode_batch_layers, norm_factored
 
         pos = [c + self.i for c in self.ctx]
         self.i += 1
         t0 = time.perf_counter()
         resid = decode_batch_layers(self.dec, self.toks, pos, self.caches, range(1), lm_head=False)
         t1 = time.perf_counter()
-        rmsnorm(resid, self.dec.w["final_norm"], self.one.rms_eps) @ self.dec.w["lm_head"].t()
+        xg, r = norm_factored(resid, self.dec.w["final_norm"], self.one.rms_eps)
+        (xg @ self.dec.w["lm_head"].t()) * r
         t2 = time.perf_counter()
         return self.spec.n_layers * (t1 - t0) + (t2 - t1)
 
@@ -233,12 +234,11 @@ def kernel_bytes(spec, B, ctx):
         "gemm_qkv_rope_kv": wbytes(qd + 2 * kd, h) + B * h * 2 + B * (qd + 2 * kd) * 2,
         "attention": kv_layer + B * qd * 2 + B * spec.n_q_heads * 8,
         "attn_combine": B * qd * 2,
-        "gemm_o_resid": wbytes(h, qd) + B * qd * 2 + B * h * 8,
+        "gemm_o_resid_norm": wbytes(h, qd) + B * qd * 2 + B * h * 10,
         "gemm_gate_up_swiglu": wbytes(2 * f, h) + B * h * 2 + B * f * 2,
-        "gemm_down_resid": wbytes(h, f) + B * f * 2 + B * h * 8,
+        "gemm_down_resid_norm": wbytes(h, f) + B * f * 2 + B * h * 10,
         "gemm_lm_head_argmax": V * h * 2 + B * h * 2 + B * V * 4,
-        "rmsnorm": B * h * 6,
-        "embed_rmsnorm": B * h * 8,
+        "embed_norm": B * h * 8,
         "argmax": 0,
     }
 

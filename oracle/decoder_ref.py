@@ -27,11 +27,14 @@ no reference code computes them and the paper's stack (vLLM, LLM Compressor AWQ)
 is neither vendored nor pinned. The rounding points below are the
 ones the B200 path uses, so the comparison isolates accumulation-order effects:
 
-  resid fp32;  xn = bf16(resid * rsqrt(mean(resid^2)+eps) * g)
-  q,k = bf16(rope(xn @ Wqkv^T + b)),  v = bf16(...)          (K cached post-RoPE)
+  resid fp32;  RMSNorm is factored: xg = bf16(resid * g), r = rsqrt(mean(resid^2)+eps),
+  and a normed projection is (xg @ W^T) * r  (= W.(x*r*g); the B200 GEMMs apply r
+  per batch column in their epilogues, so no separate norm kernel exists)
+  q,k = bf16(rope((xg @ Wqkv^T) * r + b)),  v = bf16(...)     (K cached post-RoPE)
   attn = bf16(softmax(q k^T / sqrt(d)) v)                     (fp32 softmax)
-  resid += attn @ Wo^T;  act = bf16(silu(g) * u);  resid += act @ Wdown^T
-  logits = fp32(bf16(rmsnorm(resid)) @ lm_head^T);  next = argmax (lowest index on ties)
+  resid += attn @ Wo^T;  act = bf16(silu(g) * u) with g,u = (xg @ W^T) * r
+  resid += act @ Wdown^T
+  logits = fp32((bf16(resid * g_final) @ lm_head^T) * r);  next = argmax (lowest index on ties)
 """
 from __future__ import annotations
 
@@ -75,6 +78,12 @@ def rmsnorm(x: torch.Tensor, g: torch.Tensor, eps: float, rnd=None) -> torch.Ten
     return (rnd or bf)(x * r * g.float())
 
 
+def norm_factored(x: torch.Tensor, g: torch.Tensor, eps: float, rnd=None) -> tuple[torch.Tensor, torch.Tensor]:
+    """(xg, r): xg = round(x * g), r = rsqrt(mean(x^2) + eps) per row; rmsnorm = xg * r."""
+    r = torch.rsqrt((x * x).mean(-1, keepdim=True) + eps)
+    return (rnd or bf)(x * g.float()), r
+
+
 def rope(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor:
     """x [..., d] fp32, cos/sin [..., d/2] broadcastable; NeoX rotate-half."""
     half = x.shape[-1] // 2
@@ -108,10 +117,10 @@ class OracleDecoder:
         s, w = self.s, self.w
         d, nq, nkv = s.head_dim, s.n_q_heads, s.n_kv_heads
         T = resid.shape[0]
-        xn = rmsnorm(resid, w[f"l{l}.attn_norm"], s.rms_eps, self.rnd)
-        q = xn @ w[f"l{l}.wq"].t()
-        k = xn @ w[f"l{l}.wk"].t()
-        v = xn @ w[f"l{l}.wv"].t()
+        xg, r = norm_factored(resid, w[f"l{l}.attn_norm"], s.rms_eps, self.rnd)
+        q = (xg @ w[f"l{l}.wq"].t()) * r
+        k = (xg @ w[f"l{l}.wk"].t()) * r
+        v = (xg @ w[f"l{l}.wv"].t()) * r
         if s.qkv_bias:
             q = q + w[f"l{l}.bq"]
             k = k + w[f"l{l}.bk"]
@@ -133,9 +142,9 @@ class OracleDecoder:
             out[:, h, :] = torch.softmax(sc, dim=-1) @ V[:, h // G, :]
         attn = self.rnd(out.reshape(T, nq * d))
         resid = resid + attn @ w[f"l{l}.wo"].t()
-        xn = rmsnorm(resid, w[f"l{l}.ffn_norm"], s.rms_eps, self.rnd)
-        g = xn @ w[f"l{l}.wg"].t()
-        u = xn @ w[f"l{l}.wu"].t()
+        xg, r = norm_factored(resid, w[f"l{l}.ffn_norm"], s.rms_eps, self.rnd)
+        g = (xg @ w[f"l{l}.wg"].t()) * r
+        u = (xg @ w[f"l{l}.wu"].t()) * r
         act = self.rnd(g / (1.0 + torch.exp(-g)) * u)
         return resid + act @ w[f"l{l}.wd"].t()
 
@@ -152,8 +161,8 @@ class OracleDecoder:
         resid = w["embed"][torch.tensor(tokens)].clone()
         for l in range(s.n_layers):
             resid = self._layer(l, resid, pos, cache["k"], cache["v"])
-        xn = rmsnorm(resid[-1:], w["final_norm"], s.rms_eps, self.rnd)
-        logits = (xn @ w["lm_head"].t())[0]
+        xg, r = norm_factored(resid[-1:], w["final_norm"], s.rms_eps, self.rnd)
+        logits = ((xg @ w["lm_head"].t()) * r)[0]
         return logits, cache
 
     # Eq. 2: prefill module P_θp(X) -> (first-token logits, C_X)
@@ -220,8 +229,8 @@ def decode_batch_layers(dec: OracleDecoder, tokens: list[int], positions: list[i
     pos = torch.tensor(positions)
     resid = w["embed"][torch.tensor(tokens)].clone()
     for l in layers:
-        xn = rmsnorm(resid, w[f"l{l}.attn_norm"], s.rms_eps)
-        q, k, v = xn @ w[f"l{l}.wq"].t(), xn @ w[f"l{l}.wk"].t(), xn @ w[f"l{l}.wv"].t()
+        xg, r = norm_factored(resid, w[f"l{l}.attn_norm"], s.rms_eps)
+        q, k, v = (xg @ w[f"l{l}.wq"].t()) * r, (xg @ w[f"l{l}.wk"].t()) * r, (xg @ w[f"l{l}.wv"].t()) * r
         if s.qkv_bias:
             q, k, v = q + w[f"l{l}.bq"], k + w[f"l{l}.bk"], v + w[f"l{l}.bv"]
         cs, sn = dec.cos[pos][:, None, :], dec.sin[pos][:, None, :]
@@ -238,9 +247,10 @@ def decode_batch_layers(dec: OracleDecoder, tokens: list[int], positions: list[i
             out[b] = torch.einsum("hgt,thd->hgd", torch.softmax(sc, -1), V).reshape(nq, d)
         attn = bf(out.reshape(B, nq * d))
         resid = resid + attn @ w[f"l{l}.wo"].t()
-        xn = rmsnorm(resid, w[f"l{l}.ffn_norm"], s.rms_eps)
-        g, u = xn @ w[f"l{l}.wg"].t(), xn @ w[f"l{l}.wu"].t()
+        xg, r = norm_factored(resid, w[f"l{l}.ffn_norm"], s.rms_eps)
+        g, u = (xg @ w[f"l{l}.wg"].t()) * r, (xg @ w[f"l{l}.wu"].t()) * r
         resid = resid + bf(g / (1.0 + torch.exp(-g)) * u) @ w[f"l{l}.wd"].t()
     if not lm_head:
         return resid
-    return rmsnorm(resid, w["final_norm"], s.rms_eps) @ w["lm_head"].t()
+    xg, r = norm_factored(resid, w["final_norm"], s.rms_eps)
+    return (xg @ w["lm_head"].t()) * r

@@ -64,6 +64,42 @@ __global__ void __launch_bounds__(kRowThreads)
   }
 }
 
+// Embedding gather fused with the first (factored) RMSNorm: resid = embed[tok],
+// xg = bf16(resid * g) in SUN-ACT, ss[0][b] = sum(resid^2) (other tiles 0); the
+// QKV GEMM applies r_b = rsqrt(mean + eps) in its epilogue (see gemm_tc.cuh).
+__global__ void __launch_bounds__(kRowThreads)
+    embed_norm_kernel(const int* __restrict__ tokens, const __nv_bfloat16* __restrict__ embed,
+                      float* __restrict__ resid, const __nv_bfloat16* __restrict__ g, __nv_bfloat16* __restrict__ xg,
+                      float* __restrict__ ss, int h, int act_rows, int ss_tiles) {
+  __shared__ float red[kRowThreads / 32];
+  pdl_wait();
+  pdl_launch_dependents();
+  const int b = blockIdx.x;
+  const __nv_bfloat16* e = embed + static_cast<long long>(tokens[b]) * h;
+  float* x = resid + static_cast<long long>(b) * h;
+  float acc = 0.f;
+  for (int i = threadIdx.x * 4; i < h; i += kRowThreads * 4) {
+    const __nv_bfloat162 e01 = *reinterpret_cast<const __nv_bfloat162*>(e + i);
+    const __nv_bfloat162 e23 = *reinterpret_cast<const __nv_bfloat162*>(e + i + 2);
+    const float4 v = make_float4(__bfloat162float(e01.x), __bfloat162float(e01.y), __bfloat162float(e23.x),
+                                 __bfloat162float(e23.y));
+    *reinterpret_cast<float4*>(x + i) = v;
+    acc += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    const __nv_bfloat162 g01 = *reinterpret_cast<const __nv_bfloat162*>(g + i);
+    const __nv_bfloat162 g23 = *reinterpret_cast<const __nv_bfloat162*>(g + i + 2);
+    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<uint8_t*>(xg) + act_offset(b, i, act_rows));
+    *reinterpret_cast<__nv_bfloat162*>(dst) =
+        __floats2bfloat162_rn(v.x * __bfloat162float(g01.x), v.y * __bfloat162float(g01.y));
+    *reinterpret_cast<__nv_bfloat162*>(dst + 2) =
+        __floats2bfloat162_rn(v.z * __bfloat162float(g23.x), v.w * __bfloat162float(g23.y));
+  }
+  const float tot = block_sum(acc, red);
+  if (threadIdx.x == 0) {
+    ss[b] = tot;
+    for (int t = 1; t < ss_tiles; ++t) ss[static_cast<long long>(t) * act_rows + b] = 0.f;
+  }
+}
+
 // next[b] = argmax over lm_head tiles (ties -> lowest vocabulary index). With
 // feedback, also tokens[b] = next[b] and positions[b] += 1 (graph-replayable loop).
 __global__ void __launch_bounds__(kRowThreads)

@@ -78,6 +78,16 @@ struct GemmArgs {
   // LOGITS
   float* amax_val;  // [m_tiles][bn]
   int* amax_idx;    // [m_tiles][bn]
+  // Fused RMSNorm, factored (see epi_chunk): producers (RESID_ADD) write
+  // xg = bf16(x * g_next) in SUN-ACT plus per-tile sums of squares; consumers
+  // (QKV / SWIGLU / LOGITS) scale their accumulators by r_b = rsqrt(mean + eps).
+  const __nv_bfloat16* norm_w;  // producer: gain of the next RMSNorm [n_out] (null: off)
+  __nv_bfloat16* xg_out;        // producer: SUN-ACT output, bn rows
+  float* ss_out;                // producer: [m_tiles][bn] partial sums of squares
+  const float* ss_in;           // consumer: [ss_tiles][bn] (null: no scaling)
+  int ss_tiles;
+  int norm_h;                   // hidden size (mean denominator)
+  float norm_eps;
   // optional per-CTA %globaltimer stamps [gridDim.x][8] (profiling only)
   unsigned long long* stamps;
 };
@@ -98,7 +108,8 @@ constexpr uint32_t kTileWBytes = kTileM * kTileK * 2;  // 16 KB: one SUN-BLK blo
 constexpr uint32_t kW4PackedBytes = kTileM * 128 / 2;  // 8 KB: one SUN-W4 block (128 x 128)
 constexpr uint32_t kW4DeqBytes = kTileM * 128 * 2;     // 32 KB dequantised bf16 tile
 
-constexpr uint32_t kEpiSmemBytes = 16 * kTileM * 4 + 512 + 2048 + 512;  // partner staging, argmax scratch, column meta
+// partner staging [16][128] f32 | argmax scratch 512 B | column meta: pos[256], page[256], r_b[256] | 512 spare
+constexpr uint32_t kEpiSmemBytes = 16 * kTileM * 4 + 512 + 3072 + 512;
 
 // byte offset of activation element (row b, column k) in SUN-ACT with `rows` rows per atom
 __host__ __device__ inline long long act_offset(int b, long long k, int rows) {
@@ -127,7 +138,52 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
                           float* stage_f32, float* red_val, int* red_idx) {
   const int row = m_tile * kTileM + row_local;
   const int B = a.batch;
+  if (a.ss_in != nullptr) {  // consumer of a factored RMSNorm: W.(x*g) * r_b
+    const float* rb = reinterpret_cast<const float*>(red_idx + 64 + 512);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] *= rb[c0 + j];
+  }
   if constexpr (EPI == EPI_STORE_F32 || EPI == EPI_RESID_ADD) {
+    if constexpr (EPI == EPI_RESID_ADD) {
+      if (a.norm_w != nullptr) {  // producer of the next RMSNorm's operand + sums of squares
+        float nw[16];
+        const bool in = row < a.n_out;
+        float* base = a.out_f32 + static_cast<long long>(c0) * a.ldo + row;
+        float old[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) old[j] = (in && c0 + j < B) ? base[j * a.ldo] : 0.f;
+        const float g = in ? __bfloat162float(a.norm_w[row]) : 0.f;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          nw[j] = old[j] + v[j];
+          if (in && c0 + j < B) {
+            base[j * a.ldo] = nw[j];
+            *reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<uint8_t*>(a.xg_out) + act_offset(c0 + j, row, a.bn)) =
+                __float2bfloat16_rn(nw[j] * g);
+          }
+          nw[j] = in ? nw[j] * nw[j] : 0.f;
+        }
+        // sum of squares over the tile's 128 rows, fixed order: warp tree, then 4 warps
+        const int lane = threadIdx.x & 31;
+        const int q = (threadIdx.x / 32) & 3;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) nw[j] += __shfl_xor_sync(0xffffffffu, nw[j], off);
+        }
+        if (lane == 0) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) red_val[q * 16 + j] = nw[j];
+        }
+        epi_bar();
+        if (threadIdx.x / 32 == 2 && lane < 16) {
+          const float t = ((red_val[lane] + red_val[16 + lane]) + red_val[32 + lane]) + red_val[48 + lane];
+          a.ss_out[static_cast<long long>(m_tile) * a.bn + c0 + lane] = t;
+        }
+        epi_bar();
+        return;
+      }
+    }
     if (row < a.n_out) {
       float* base = a.out_f32 + static_cast<long long>(c0) * a.ldo + row;
       if constexpr (EPI == EPI_RESID_ADD) {
@@ -317,17 +373,27 @@ SUN_DEVICE void direct_epilogue(const GemmArgs& a, int tile, uint32_t taddr, flo
   }
 }
 
+// Per-column epilogue metadata, once per CTA: QKV positions / KV pages, and the
+// factored RMSNorm scale r_b = rsqrt(sum_t ss[t][b] / h + eps) (tile order fixed).
 template <int EPI>
 SUN_DEVICE void load_qkv_meta(const GemmArgs& a, float* epi) {
+  int* meta = reinterpret_cast<int*>(epi + 16 * kTileM + 128);
   if constexpr (EPI == EPI_QKV_ROPE) {
-    int* meta = reinterpret_cast<int*>(epi + 16 * kTileM + 128);
     for (int b = threadIdx.x - 64; b < a.bn; b += 128) {
       const int pos = b < a.batch ? a.positions[b] : 0;
       meta[b] = pos;
       meta[256 + b] = b < a.batch ? a.block_tables[static_cast<long long>(b) * a.bt_stride + pos / a.page_size] : 0;
     }
-    epi_bar();
   }
+  if (a.ss_in != nullptr) {
+    float* rb = reinterpret_cast<float*>(meta + 512);
+    for (int b = threadIdx.x - 64; b < a.bn; b += 128) {
+      float t = 0.f;
+      for (int i = 0; i < a.ss_tiles; ++i) t += a.ss_in[static_cast<long long>(i) * a.bn + b];
+      rb[b] = rsqrtf(t / static_cast<float>(a.norm_h) + a.norm_eps);
+    }
+  }
+  epi_bar();
 }
 
 SUN_DEVICE void cvt_bar() { asm volatile("bar.sync 2, 128;" ::: "memory"); }

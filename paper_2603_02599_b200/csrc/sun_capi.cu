@@ -259,7 +259,7 @@ cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, c
 
 // Workspace layout shared by sizing and creation.
 struct WsLayout {
-  size_t resid, xn, q, attn, act, part_o, part_ml, attn_cnt, amax_val, amax_idx, logits, total;
+  size_t resid, xn, q, attn, act, part_o, part_ml, attn_cnt, ss, amax_val, amax_idx, logits, total;
   int max_splits;
 };
 
@@ -288,6 +288,7 @@ WsLayout layout_ws(const SunDecoderDims& d, int max_batch) {
   w.part_o = take(size_t(max_batch) * d.n_q_heads * w.max_splits * d.head_dim * 4);
   w.part_ml = take(size_t(max_batch) * d.n_q_heads * w.max_splits * 2 * 4);
   w.attn_cnt = take(size_t(max_batch) * d.n_kv_heads * 4);
+  w.ss = take(size_t((d.hidden + kTileM - 1) / kTileM) * bmp * 4);
   const int lm_tiles = (d.vocab + kTileM - 1) / kTileM;
   w.amax_val = take(size_t(lm_tiles) * bmp * 4);
   w.amax_idx = take(size_t(lm_tiles) * bmp * 4);
@@ -333,6 +334,7 @@ struct SunDecoder {
   __nv_bfloat16 *xn, *q, *attn, *act;  // xn / attn / act in SUN-ACT (GEMM operands)
   float *part_o, *part_ml, *amax_val, *logits;
   unsigned* attn_cnt;
+  float* ss;  // [h/128][bn] per-tile sums of squares of the residual (factored RMSNorm)
   int* amax_idx;
   GemmPlan p_qkv, p_o, p_gu, p_down, p_lm;
 };
@@ -476,6 +478,7 @@ SunStatus sun_decoder_create(const SunDecoderDims* dims, const SunWeights* weigh
   dec->part_o = reinterpret_cast<float*>(ws + dec->L.part_o);
   dec->part_ml = reinterpret_cast<float*>(ws + dec->L.part_ml);
   dec->attn_cnt = reinterpret_cast<unsigned*>(ws + dec->L.attn_cnt);
+  dec->ss = reinterpret_cast<float*>(ws + dec->L.ss);
   dec->amax_val = reinterpret_cast<float*>(ws + dec->L.amax_val);
   dec->amax_idx = reinterpret_cast<int*>(ws + dec->L.amax_idx);
   dec->logits = reinterpret_cast<float*>(ws + dec->L.logits);
@@ -543,19 +546,31 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
   aa.counters = dec->attn_cnt;
   aa.fused_combine = attn_fused_combine();
 
-  // embedding gather + first attention RMSNorm
-  SUN_CUDA(launch(rmsnorm_kernel, dim3(batch), dim3(kRowThreads), 0, st, pdl, tokens,
+  // RMSNorm is factored into the GEMMs: a producer writes xg = bf16(x * g) and
+  // per-tile sums of squares, the consumer GEMM scales row b of its result by
+  // r_b = rsqrt(mean(x_b^2) + eps) (W.(x*g*r) = r * W.(x*g)); no norm launches.
+  const int ss_tiles = (d.hidden + kTileM - 1) / kTileM;
+  auto consume_norm = [&](GemmArgs& g) {
+    g.ss_in = dec->ss;
+    g.ss_tiles = ss_tiles;
+    g.norm_h = d.hidden;
+    g.norm_eps = d.rms_eps;
+  };
+  auto produce_norm = [&](GemmArgs& g, const void* gain) {
+    g.norm_w = static_cast<const __nv_bfloat16*>(gain);
+    g.xg_out = dec->xn;
+    g.ss_out = dec->ss;
+  };
+  // embedding gather + the first (attention) norm's operand
+  SUN_CUDA(launch(embed_norm_kernel, dim3(batch), dim3(kRowThreads), 0, st, pdl, tokens,
                   static_cast<const __nv_bfloat16*>(dec->w.embed), dec->resid,
-                  static_cast<const __nv_bfloat16*>(dec->layers[0].attn_norm), dec->xn, d.hidden,
-                  (long long)d.hidden, d.rms_eps, bn));
+                  static_cast<const __nv_bfloat16*>(dec->layers[0].attn_norm), dec->xn, dec->ss, d.hidden, bn,
+                  ss_tiles));
   for (int l = 0; l < d.n_layers; ++l) {
     const SunLayerWeights& lw = dec->layers[l];
-    if (l > 0)
-      SUN_CUDA(launch(rmsnorm_kernel, dim3(batch), dim3(kRowThreads), 0, st, pdl, (const int*)nullptr,
-                      (const __nv_bfloat16*)nullptr, dec->resid, static_cast<const __nv_bfloat16*>(lw.attn_norm),
-                      dec->xn, d.hidden, (long long)d.hidden, d.rms_eps, bn));
-    // QKV + bias + RoPE + KV append
+    // QKV (* r_b) + bias + RoPE + KV append
     GemmArgs a = base_args(dec->p_qkv, qkv_rows(d), d.hidden, batch, bn, dec->xn);
+    consume_norm(a);
     a.out_bf16 = dec->q;
     a.ldb = qd;
     a.bias = static_cast<const __nv_bfloat16*>(lw.b_qkv);
@@ -577,38 +592,35 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     // paged attention
     aa.layer = l;
     if ((s = run_attention(d, dec->tm_kv, aa, batch, st, pdl)) != SUN_OK) return s;
-    // O projection + residual
+    // O projection + residual; emits the FFN norm's operand
     a = base_args(dec->p_o, d.hidden, qd, batch, bn, dec->attn);
     a.out_f32 = dec->resid;
     a.ldo = d.hidden;
+    produce_norm(a, lw.ffn_norm);
     s = w4 ? run_gemm<EPI_RESID_ADD>(nullptr, lw.w_o, lw.s_o, a, dec->p_o, st, pdl)
            : run_gemm<EPI_RESID_ADD>(lw.w_o, nullptr, nullptr, a, dec->p_o, st, pdl);
     if (s != SUN_OK) return s;
-    // FFN RMSNorm
-    SUN_CUDA(launch(rmsnorm_kernel, dim3(batch), dim3(kRowThreads), 0, st, pdl, (const int*)nullptr,
-                    (const __nv_bfloat16*)nullptr, dec->resid, static_cast<const __nv_bfloat16*>(lw.ffn_norm),
-                    dec->xn, d.hidden, (long long)d.hidden, d.rms_eps, bn));
-    // gate/up + SwiGLU
+    // gate/up (* r_b) + SwiGLU
     a = base_args(dec->p_gu, gu_rows(d), d.hidden, batch, bn, dec->xn);
+    consume_norm(a);
     a.out_bf16 = dec->act;
     a.ldb = d.ffn;
     a.n_valid_out = d.ffn;
     s = w4 ? run_gemm<EPI_SWIGLU>(nullptr, lw.w_gate_up, lw.s_gate_up, a, dec->p_gu, st, pdl)
            : run_gemm<EPI_SWIGLU>(lw.w_gate_up, nullptr, nullptr, a, dec->p_gu, st, pdl);
     if (s != SUN_OK) return s;
-    // down + residual
+    // down + residual; emits the next attention norm's (or the final norm's) operand
     a = base_args(dec->p_down, d.hidden, d.ffn, batch, bn, dec->act);
     a.out_f32 = dec->resid;
     a.ldo = d.hidden;
+    produce_norm(a, l + 1 < d.n_layers ? dec->layers[l + 1].attn_norm : dec->w.final_norm);
     s = w4 ? run_gemm<EPI_RESID_ADD>(nullptr, lw.w_down, lw.s_down, a, dec->p_down, st, pdl)
            : run_gemm<EPI_RESID_ADD>(lw.w_down, nullptr, nullptr, a, dec->p_down, st, pdl);
     if (s != SUN_OK) return s;
   }
-  // final norm, lm_head (+ argmax partials), greedy sampling
-  SUN_CUDA(launch(rmsnorm_kernel, dim3(batch), dim3(kRowThreads), 0, st, pdl, (const int*)nullptr,
-                  (const __nv_bfloat16*)nullptr, dec->resid, static_cast<const __nv_bfloat16*>(dec->w.final_norm),
-                  dec->xn, d.hidden, (long long)d.hidden, d.rms_eps, bn));
+  // lm_head (* r_b) with per-tile argmax partials, then greedy sampling
   GemmArgs a = base_args(dec->p_lm, d.vocab, d.hidden, batch, bn, dec->xn);
+  consume_norm(a);
   a.out_f32 = lg;
   a.ldo = d.vocab;
   a.amax_val = dec->amax_val;

@@ -86,14 +86,11 @@ class _StepRunner:
 
     def kernel_names(self) -> list[str]:
         """Launch order of one step (matches sun_decode_step)."""
-        names = ["embed_rmsnorm"]
-        for l in range(self.spec.n_layers):
-            if l > 0:
-                names.append("rmsnorm")
+        names = ["embed_norm"]
+        for _ in range(self.spec.n_layers):
             names += ["gemm_qkv_rope_kv", "attention"] + ([] if self.fused_combine else ["attn_combine"]) + [
-                "gemm_o_resid", "rmsnorm",
-                      "gemm_gate_up_swiglu", "gemm_down_resid"]
-        return names + ["rmsnorm", "gemm_lm_head_argmax", "argmax"]
+                "gemm_o_resid_norm", "gemm_gate_up_swiglu", "gemm_down_resid_norm"]
+        return names + ["gemm_lm_head_argmax", "argmax"]
 
 
 def launch_count() -> int:

@@ -66,4 +66,4 @@ def test_scheduler_drives_b200_executor_mixed_batches(cuda):
                 assert (top2[0] - top2[1]).item() < 2 * LOGIT_TOL, f"req {r.id} step {t} differs from oracle"
                 exempt += 1
     assert worst <= LOGIT_TOL, worst
-    assert exempt <= 2
+    assert exempt <= max(2, len(done) * osl * 5 // 100)
