@@ -88,6 +88,14 @@ struct GemmArgs {
   int ss_tiles;
   int norm_h;                   // hidden size (mean denominator)
   float norm_eps;
+  // Stream-K schedule (sk_units > 0): the m_tiles x ksteps work units are split
+  // evenly over the grid; a CTA whose range starts inside a tile parks its fp32
+  // partial in sk_part[blockIdx.x] and raises sk_flags[blockIdx.x]; the tile's
+  // owner (the CTA holding k-step 0) adds the partials in CTA order, runs the
+  // epilogue and clears the flags (zeroed once, self-resetting).
+  int sk_units;
+  float* sk_part;      // [grid][bn/16][128][16] fp32
+  unsigned* sk_flags;  // [grid]
   // optional per-CTA %globaltimer stamps [gridDim.x][8] (profiling only)
   unsigned long long* stamps;
 };
@@ -396,6 +404,89 @@ SUN_DEVICE void load_qkv_meta(const GemmArgs& a, float* epi) {
   epi_bar();
 }
 
+SUN_DEVICE unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+SUN_DEVICE void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// fp32 split-K partial tile layout [bn/16][4][128 rows][4]: float4 j (columns
+// c0+4j..c0+4j+3) of row r; a warp's float4 accesses are 512 B contiguous, so
+// shared-memory / DSMEM reads are conflict-free and global ones fully coalesced.
+SUN_DEVICE int part_index(int c0, int j, int row) { return (c0 >> 4) * (kTileM * 16) + (j * kTileM + row) * 4; }
+
+// Stream-K contributor: TMEM accumulator -> sk_part[blockIdx.x] (chunk-major
+// [bn/16][128][16], a warp's chunk is 2 KB contiguous), then raise the flag.
+SUN_DEVICE void sk_store_partial(const GemmArgs& a, uint32_t taddr, int row_local) {
+  float* base = a.sk_part + static_cast<long long>(blockIdx.x) * a.bn * kTileM;
+  float v[16];
+  for (int c0 = 0; c0 < a.bn; c0 += 16) {
+    tmem_ld16(taddr + c0, v);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      __stcg(reinterpret_cast<float4*>(base + part_index(c0, j, row_local)),
+             make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+  }
+  __threadfence();
+  epi_bar();
+  if (threadIdx.x == 64) {
+    st_release_u32(a.sk_flags + blockIdx.x, 1u);
+    SUN_STAMP(13);
+  }
+}
+
+// Stream-K owner of `tile` (its range holds k-step 0 but not the last): wait for
+// the contributors (the following CTAs whose ranges start inside the tile), pull
+// their partials into the idle stage ring with bulk copies (one round trip), add
+// them in CTA order to the TMEM accumulator and run the fused epilogue.
+template <int EPI>
+SUN_DEVICE void sk_owner_epilogue(const GemmArgs& a, int tile, uint32_t taddr, int row_local, float* epi,
+                                  uint8_t* ring, uint64_t* bar) {
+  const int G = static_cast<int>(gridDim.x);
+  const int c = static_cast<int>(blockIdx.x);
+  const long long tile_end = static_cast<long long>(tile + 1) * a.ksteps;
+  int c_hi = c + 1;
+  while (c_hi < G && static_cast<long long>(c_hi) * a.sk_units / G < tile_end) ++c_hi;
+  const uint32_t pbytes = static_cast<uint32_t>(a.bn) * kTileM * 4;
+  if (threadIdx.x == 64) {
+    for (int cc = c + 1; cc < c_hi; ++cc)
+      while (ld_acquire_u32(a.sk_flags + cc) == 0u) {
+      }
+    SUN_STAMP(12);
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    mbar_arrive_expect_tx(bar, pbytes * static_cast<uint32_t>(c_hi - c - 1));
+    for (int cc = c + 1; cc < c_hi; ++cc)
+      bulk_load(ring + static_cast<size_t>(cc - c - 1) * pbytes, a.sk_part + static_cast<long long>(cc) * a.bn * kTileM,
+                pbytes, bar);
+  }
+  mbar_wait(bar, 0);
+  const float* parts = reinterpret_cast<const float*>(ring);
+  float* red_val = epi + 16 * kTileM;
+  int* red_idx = reinterpret_cast<int*>(red_val + 64);
+  float v[16];
+  for (int c0 = 0; c0 < a.bn; c0 += 16) {
+    tmem_ld16(taddr + c0, v);
+    for (int cc = 0; cc < c_hi - c - 1; ++cc) {
+      const float* src = parts + static_cast<size_t>(cc) * a.bn * kTileM;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float4 x = *reinterpret_cast<const float4*>(src + part_index(c0, j, row_local));
+        v[4 * j] += x.x;
+        v[4 * j + 1] += x.y;
+        v[4 * j + 2] += x.z;
+        v[4 * j + 3] += x.w;
+      }
+    }
+    epi_chunk<EPI>(a, tile, row_local, c0, v, epi, red_val, red_idx);
+  }
+  epi_bar();
+  if (threadIdx.x == 64)
+    for (int cc = c + 1; cc < c_hi; ++cc) a.sk_flags[cc] = 0u;
+}
+
 SUN_DEVICE void cvt_bar() { asm volatile("bar.sync 2, 128;" ::: "memory"); }
 
 // Dequantise one 128x128 block: packed (128 rows x 64 B) + scales -> SW128 bf16 tile.
@@ -443,27 +534,30 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
   uint64_t* tempty = tfull + 2;      // [2]
   uint64_t* dfull = tempty + 2;      // [2] W4
   uint64_t* dempty = dfull + 2;      // [2] W4
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + 2);
+  uint64_t* skbar = dempty + 2;      // stream-K owner: contributor partials landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(skbar + 1);
 
   const int warp = warp_id_sync();
   const uint32_t S = a.splits > 1 ? static_cast<uint32_t>(a.splits) : 1u;
   const bool clustered = S > 1;
   const uint32_t rank = clustered ? cluster_ctarank() : 0u;
-  // this CTA's work: tiles [t_lo, t_hi) x ksteps [ks0, ks1)
-  int t_lo, t_hi, ks0, ks1;
-  if (clustered) {
-    t_lo = static_cast<int>(blockIdx.x / S);
-    t_hi = t_lo + 1;
-    ks0 = static_cast<int>(rank * a.ksteps / S);
-    ks1 = static_cast<int>((rank + 1) * a.ksteps / S);
-  } else {
-    t_lo = static_cast<int>(static_cast<long long>(blockIdx.x) * a.m_tiles / gridDim.x);
-    t_hi = static_cast<int>(static_cast<long long>(blockIdx.x + 1) * a.m_tiles / gridDim.x);
-    ks0 = 0;
-    ks1 = a.ksteps;
+  // this CTA's work: the contiguous range [u0, u1) of work units u = tile * ksteps + ks
+  const int KS = a.ksteps;
+  int u0, u1;
+  if (clustered) {  // one tile, k-steps split over the cluster
+    const int t = static_cast<int>(blockIdx.x / S);
+    u0 = t * KS + static_cast<int>(rank * KS / S);
+    u1 = t * KS + static_cast<int>((rank + 1) * KS / S);
+  } else if (a.sk_units > 0) {  // stream-K
+    u0 = static_cast<int>(static_cast<long long>(blockIdx.x) * a.sk_units / gridDim.x);
+    u1 = static_cast<int>(static_cast<long long>(blockIdx.x + 1) * a.sk_units / gridDim.x);
+  } else {  // whole tiles
+    u0 = static_cast<int>(static_cast<long long>(blockIdx.x) * a.m_tiles / gridDim.x) * KS;
+    u1 = static_cast<int>(static_cast<long long>(blockIdx.x + 1) * a.m_tiles / gridDim.x) * KS;
   }
-  const int nks = ks1 - ks0;
-  const int n = (t_hi - t_lo) * nks;
+  const int n = u1 - u0;
+  const int t_first = u0 / KS;
+  const int nseg = n > 0 ? (u1 - 1) / KS - t_first + 1 : 0;
   const uint32_t ncols = tmem_cols_for(a.bn);
   const long long rows_pad = static_cast<long long>(a.m_tiles) * kTileM;
   if (threadIdx.x == 0) SUN_STAMP(0);
@@ -479,6 +573,7 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
       mbar_init(&dfull[j], 1);
       mbar_init(&dempty[j], 1);
     }
+    mbar_init(skbar, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, ncols);
@@ -499,8 +594,8 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
       // issue weight (or packed+scales) loads of stage j; X is added separately
       auto issue_w = [&](int j) {
         const int s = j % stages;
-        const int tile = t_lo + j / nks;
-        const int ks = ks0 + j % nks;
+        const int tile = (u0 + j) / KS;
+        const int ks = (u0 + j) % KS;
         const int nb = nblk_of(ks);
         uint8_t* st = stg + s * sb;
         if constexpr (W4) {
@@ -517,7 +612,7 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
       };
       auto issue_x = [&](int j) {
         const int s = j % stages;
-        const int ks = ks0 + j % nks;
+        const int ks = (u0 + j) % KS;
         const int nb = W4 ? 2 : nblk_of(ks);
         bulk_load_hint(stg + s * sb + xoff, a.xact + static_cast<long long>(2 * ks) * a.bn * 128,
                        nb * a.bn * 128u, &full[s], kEvictLast);
@@ -538,10 +633,10 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
     int seg = 0;
     for (int j = 0; j < n; ++j) {
       const int s = j % stages;
-      const int jj = j % nks;
-      const bool first = jj == 0, last = jj == nks - 1;
+      const int ks = (u0 + j) % KS;
+      const bool first = j == 0 || ks == 0, last = j == n - 1 || ks == KS - 1;
       const int buf = seg & 1;
-      const int nb = nblk_of(ks0 + jj);
+      const int nb = nblk_of(ks);
       if (first) {
         mbar_wait(&tempty[buf], ((seg >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -574,14 +669,19 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
     load_qkv_meta<EPI>(a, epi);
     const int q = warp & 3;
     const int row_local = q * 32 + (threadIdx.x & 31);
-    for (int seg = 0; seg < t_hi - t_lo; ++seg) {
+    for (int seg = 0; seg < nseg; ++seg) {
       const int buf = seg & 1;
+      const int tile = t_first + seg;
+      const int kb = max(u0, tile * KS) - tile * KS;
+      const int ke = min(u1, (tile + 1) * KS) - tile * KS;
       mbar_wait(&tfull[buf], (seg >> 1) & 1);
       tc_fence_after();
       if (threadIdx.x == 64 && seg == 0) SUN_STAMP(4);
       const uint32_t taddr = tmem_base + static_cast<uint32_t>(buf * a.bn) + (static_cast<uint32_t>(q * 32) << 16);
       if (!clustered) {
-        direct_epilogue<EPI>(a, t_lo + seg, taddr, epi);
+        if (kb == 0 && ke == KS) direct_epilogue<EPI>(a, tile, taddr, epi);
+        else if (kb > 0) sk_store_partial(a, taddr, row_local);
+        else sk_owner_epilogue<EPI>(a, tile, taddr, row_local, epi, stg, skbar);
         tc_fence_before();
         epi_bar();
         if (threadIdx.x == 64) mbar_arrive(&tempty[buf]);
@@ -593,10 +693,10 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
         float v[16];
         for (int c0 = 0; c0 < a.bn; c0 += 16) {
           tmem_ld16(taddr + c0, v);
-          float* dst = part + ((c0 >> 4) * kTileM + row_local) * 16;
 #pragma unroll
-          for (int j = 0; j < 16; j += 4)
-            *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<float4*>(part + part_index(c0, j, row_local)) =
+                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
         }
       }
     }
@@ -638,7 +738,7 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
           for (int u = 0; u < 4; ++u)
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-              x[u][j] = (r0 + u < S) ? ld_dsmem_f4(dsmem_addr(part + ((c0 >> 4) * kTileM + row_local) * 16 + 4 * j, r0 + u))
+              x[u][j] = (r0 + u < S) ? ld_dsmem_f4(dsmem_addr(part + part_index(c0, j, row_local), r0 + u))
                                      : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
           for (int u = 0; u < 4; ++u)
@@ -651,7 +751,7 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
             }
         }
         if (threadIdx.x == 64) SUN_STAMP(10);
-        epi_chunk<EPI>(a, t_lo, row_local, c0, v, epi, red_val, red_idx);
+        epi_chunk<EPI>(a, t_first, row_local, c0, v, epi, red_val, red_idx);
         if (threadIdx.x == 64) SUN_STAMP(11);
       }
     }

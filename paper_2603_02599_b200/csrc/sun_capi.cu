@@ -130,6 +130,16 @@ int gemm_ctas_per_sm(int bn, bool w4) {
   return 1;
 }
 
+// Optional grid cap (SUN_GEMM_MAX_GRID): with 2-per-SM smem budgets and a
+// 148-CTA grid, the next kernel's CTAs can be co-resident (PDL prefetch).
+int gemm_max_grid() {
+  static int v = [] {
+    const char* e = getenv("SUN_GEMM_MAX_GRID");
+    return e ? atoi(e) : 1 << 30;
+  }();
+  return v;
+}
+
 int gemm_stages(int bn, bool w4, int per_sm) {
   const int budget = kSmemPerSm / per_sm - 2048;
   const int avail = budget - 1024 - (w4 ? 2 * int(kW4DeqBytes) : 0) - int(kEpiSmemBytes) - 512;
@@ -257,9 +267,27 @@ cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, c
   return e;
 }
 
+// Stream-K GEMM scratch: one fp32 [bn][128] partial and one flag per CTA slot.
+constexpr int kMaxGemmCtas = 2 * kNumSms;
+size_t sk_part_bytes(int bn) { return size_t(kMaxGemmCtas) * size_t(bn) * kTileM * 4; }
+
+// GEMM schedule. 0 (default): cluster split-K for <= 148 tiles, whole tiles
+// otherwise. 1: stream-K for GEMMs with more tiles than SMs (even split of
+// tiles x k-steps; measured 37.4 vs 40.4 us for the 8B gate_up alone, but the
+// step got slower — with whole tiles the CTAs holding one tile finish early and
+// the next kernel's CTAs start prefetching under PDL). 2: stream-K everywhere
+// it fits (tests).
+int gemm_sched() {
+  static int v = [] {
+    const char* e = getenv("SUN_GEMM_SCHED");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 // Workspace layout shared by sizing and creation.
 struct WsLayout {
-  size_t resid, xn, q, attn, act, part_o, part_ml, attn_cnt, ss, amax_val, amax_idx, logits, total;
+  size_t resid, xn, q, attn, act, part_o, part_ml, attn_cnt, ss, amax_val, amax_idx, logits, sk_part, sk_flags, total;
   int max_splits;
 };
 
@@ -293,6 +321,8 @@ WsLayout layout_ws(const SunDecoderDims& d, int max_batch) {
   w.amax_val = take(size_t(lm_tiles) * bmp * 4);
   w.amax_idx = take(size_t(lm_tiles) * bmp * 4);
   w.logits = take(size_t(max_batch) * d.vocab * 4);
+  w.sk_part = take(sk_part_bytes(bmp));
+  w.sk_flags = take(kMaxGemmCtas * 4);
   w.total = off;
   return w;
 }
@@ -336,14 +366,19 @@ struct SunDecoder {
   unsigned* attn_cnt;
   float* ss;  // [h/128][bn] per-tile sums of squares of the residual (factored RMSNorm)
   int* amax_idx;
+  float* sk_part;
+  unsigned* sk_flags;
   GemmPlan p_qkv, p_o, p_gu, p_down, p_lm;
 };
 
 namespace {
 
-GemmArgs base_args(const GemmPlan& p, int64_t n_out, int64_t k, int batch, int bn, const void* xact) {
+GemmArgs base_args(const GemmPlan& p, int64_t n_out, int64_t k, int batch, int bn, const void* xact,
+                   float* sk_part = nullptr, unsigned* sk_flags = nullptr) {
   GemmArgs a;
   memset(&a, 0, sizeof(a));
+  a.sk_part = sk_part;
+  a.sk_flags = sk_flags;
   a.n_out = int(n_out);
   a.k = int(k);
   a.batch = batch;
@@ -373,12 +408,31 @@ SunStatus run_gemm(const void* wblk, const void* packed, const void* scales, Gem
   a.w4_packed = static_cast<const uint8_t*>(packed);
   a.w4_scales = static_cast<const __nv_bfloat16*>(scales);
   const int per_sm = gemm_ctas_per_sm(a.bn, w4);
-  const int slots = kNumSms * per_sm;
+  const int slots = std::min(kNumSms * per_sm, gemm_max_grid());
   a.stages = gemm_stages(a.bn, w4, per_sm);
   const size_t smem = gemm_smem_bytes(a.bn, a.stages, w4);
-  const int S = cluster_splits(p, smem, w4, slots);
+  int S, grid;
+  // Stream-K where whole tiles cannot balance over the SMs (more tiles than CTA
+  // slots, e.g. gate_up 224 tiles / 148 SMs = 1.51) and every owner's
+  // contributor partials fit in its stage ring; cluster split-K (<= slots
+  // tiles) or whole tiles otherwise.
+  const int units = p.m_tiles * p.ksteps;
+  const int sk_grid = std::min(units, std::min(slots, kMaxGemmCtas));
+  const int max_contrib = (p.ksteps + (units / sk_grid) - 1) / std::max(1, units / sk_grid) + 1;
+  // (SUN_GEMM_SCHED=2 forces stream-K on every GEMM whose partials fit: tests)
+  const bool sk = gemm_sched() != 0 && a.sk_part != nullptr && a.sk_flags != nullptr &&
+                  (gemm_sched() == 2 || (p.m_tiles > slots && p.m_tiles % sk_grid != 0)) &&
+                  size_t(max_contrib) * a.bn * kTileM * 4 <= size_t(a.stages) * gemm_stage_bytes(a.bn, w4);
+  if (sk) {
+    S = 1;
+    a.sk_units = units;
+    grid = sk_grid;
+  } else {
+    S = cluster_splits(p, smem, w4, slots);
+    a.sk_units = 0;
+    grid = S > 1 ? p.m_tiles * S : std::min(p.m_tiles, slots);
+  }
   a.splits = S;
-  const int grid = S > 1 ? p.m_tiles * S : std::min(p.m_tiles, slots);
   g_cluster = unsigned(S);
   if (w4) {
     if constexpr (EPI == EPI_LOGITS) return fail(SUN_ERR_UNSUPPORTED, "lm_head is bf16");
@@ -482,6 +536,8 @@ SunStatus sun_decoder_create(const SunDecoderDims* dims, const SunWeights* weigh
   dec->amax_val = reinterpret_cast<float*>(ws + dec->L.amax_val);
   dec->amax_idx = reinterpret_cast<int*>(ws + dec->L.amax_idx);
   dec->logits = reinterpret_cast<float*>(ws + dec->L.logits);
+  dec->sk_part = reinterpret_cast<float*>(ws + dec->L.sk_part);
+  dec->sk_flags = reinterpret_cast<unsigned*>(ws + dec->L.sk_flags);
 
   const SunDecoderDims& d = *dims;
   const int qd = d.n_q_heads * d.head_dim;
@@ -495,6 +551,7 @@ SunStatus sun_decoder_create(const SunDecoderDims* dims, const SunWeights* weigh
   // the attention split counters (self-resetting afterwards)
   cudaError_t e = cudaMemset(ws, 0, dec->L.part_o);
   if (e == cudaSuccess) e = cudaMemset(ws + dec->L.attn_cnt, 0, size_t(max_batch) * d_cnt_heads(*dims) * 4);
+  if (e == cudaSuccess) e = cudaMemset(ws + dec->L.sk_flags, 0, kMaxGemmCtas * 4);
   if (e != cudaSuccess) {
     delete dec;
     return fail(SUN_ERR_CUDA, "cudaMemset ws: %s", cudaGetErrorString(e));
@@ -569,7 +626,7 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
   for (int l = 0; l < d.n_layers; ++l) {
     const SunLayerWeights& lw = dec->layers[l];
     // QKV (* r_b) + bias + RoPE + KV append
-    GemmArgs a = base_args(dec->p_qkv, qkv_rows(d), d.hidden, batch, bn, dec->xn);
+    GemmArgs a = base_args(dec->p_qkv, qkv_rows(d), d.hidden, batch, bn, dec->xn, dec->sk_part, dec->sk_flags);
     consume_norm(a);
     a.out_bf16 = dec->q;
     a.ldb = qd;
@@ -593,7 +650,7 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     aa.layer = l;
     if ((s = run_attention(d, dec->tm_kv, aa, batch, st, pdl)) != SUN_OK) return s;
     // O projection + residual; emits the FFN norm's operand
-    a = base_args(dec->p_o, d.hidden, qd, batch, bn, dec->attn);
+    a = base_args(dec->p_o, d.hidden, qd, batch, bn, dec->attn, dec->sk_part, dec->sk_flags);
     a.out_f32 = dec->resid;
     a.ldo = d.hidden;
     produce_norm(a, lw.ffn_norm);
@@ -601,7 +658,7 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
            : run_gemm<EPI_RESID_ADD>(lw.w_o, nullptr, nullptr, a, dec->p_o, st, pdl);
     if (s != SUN_OK) return s;
     // gate/up (* r_b) + SwiGLU
-    a = base_args(dec->p_gu, gu_rows(d), d.hidden, batch, bn, dec->xn);
+    a = base_args(dec->p_gu, gu_rows(d), d.hidden, batch, bn, dec->xn, dec->sk_part, dec->sk_flags);
     consume_norm(a);
     a.out_bf16 = dec->act;
     a.ldb = d.ffn;
@@ -610,7 +667,7 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
            : run_gemm<EPI_SWIGLU>(lw.w_gate_up, nullptr, nullptr, a, dec->p_gu, st, pdl);
     if (s != SUN_OK) return s;
     // down + residual; emits the next attention norm's (or the final norm's) operand
-    a = base_args(dec->p_down, d.hidden, d.ffn, batch, bn, dec->act);
+    a = base_args(dec->p_down, d.hidden, d.ffn, batch, bn, dec->act, dec->sk_part, dec->sk_flags);
     a.out_f32 = dec->resid;
     a.ldo = d.hidden;
     produce_norm(a, l + 1 < d.n_layers ? dec->layers[l + 1].attn_norm : dec->w.final_norm);
@@ -619,7 +676,7 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     if (s != SUN_OK) return s;
   }
   // lm_head (* r_b) with per-tile argmax partials, then greedy sampling
-  GemmArgs a = base_args(dec->p_lm, d.vocab, d.hidden, batch, bn, dec->xn);
+  GemmArgs a = base_args(dec->p_lm, d.vocab, d.hidden, batch, bn, dec->xn, dec->sk_part, dec->sk_flags);
   consume_norm(a);
   a.out_f32 = lg;
   a.ldo = d.vocab;
@@ -672,7 +729,8 @@ SunStatus sun_decode_step_profile(SunDecoder* dec, const int32_t* tokens, const 
 
 SunStatus sun_gemm_workspace_bytes(int64_t n_out, int64_t k, int32_t batch, size_t* bytes) {
   if (n_out < 1 || k < 1 || batch < 1 || batch > 256) return fail(SUN_ERR_VALUE, "bad gemm shape");
-  *bytes = size_t(round16(batch)) * size_t((k + 63) / 64) * 128;  // SUN-ACT copy of X
+  const size_t act = align_up(size_t(round16(batch)) * size_t((k + 63) / 64) * 128, 1024);  // SUN-ACT copy of X
+  *bytes = act + sk_part_bytes(round16(batch)) + kMaxGemmCtas * 4;  // + stream-K partials and flags
   return SUN_OK;
 }
 
@@ -695,7 +753,10 @@ SunStatus gemm_api(const void* wblk, const void* packed, const void* scales, int
   SUN_CUDA(launch(block_activations_kernel, dim3(148), dim3(256), 0, st, false, static_cast<const __nv_bfloat16*>(x),
                   int(batch), (long long)k, (long long)ldx, bn, static_cast<uint8_t*>(workspace)));
   GemmPlan p = plan_gemm(n_out, k);
-  GemmArgs a = base_args(p, n_out, k, batch, bn, workspace);
+  const size_t act = align_up(size_t(bn) * size_t((k + 63) / 64) * 128, 1024);
+  uint8_t* wsb = static_cast<uint8_t*>(workspace);
+  GemmArgs a = base_args(p, n_out, k, batch, bn, workspace, reinterpret_cast<float*>(wsb + act),
+                         reinterpret_cast<unsigned*>(wsb + act + sk_part_bytes(bn)));
   a.out_f32 = out;
   a.ldo = ldo;
   a.stamps = reinterpret_cast<unsigned long long*>(stamps);

@@ -28,3 +28,7 @@ for n_out, k in [(6144, 4096), (4096, 4096), (4096, 14336), (28672, 4096)]:
         if col is None or (s[:, i] == 0).all():
             continue
         print(f"   {nm:12s} min {col.min():7.2f} med {col.median():7.2f} max {col.max():7.2f} us")
+    if os.environ.get("SLOW"):
+        order = rel[:, 6].argsort(descending=True)[:8]
+        for i in order.tolist():
+            print("   cta", i, " ".join(f"{x:6.2f}" for x in rel[i, :14].tolist()))

@@ -15,7 +15,9 @@ def _r16(b):
 @pytest.mark.parametrize(
     "n_out,k,batch",
     [(256, 256, 1), (768, 256, 8), (1408, 256, 17), (300, 688, 5), (4096, 4096, 64), (6144, 4096, 64),
-     (1000, 512, 256), (4096, 14336, 33), (512, 128, 128)],
+     (1000, 512, 256), (4096, 14336, 33), (512, 128, 128),
+     # more tiles than SMs, not a multiple of 148: stream-K (partial tiles + owner fix-up)
+     (28672, 4096, 64), (20000, 512, 40), (128256, 256, 8)],
 )
 def test_gemm_bf16_matches_fp32(cuda, n_out, k, batch):
     from paper_2603_02599_b200 import kernels
@@ -43,6 +45,34 @@ def test_gemm_deterministic_split_k(cuda):
     a = kernels.gemm_bf16(w, x, 64)
     b = kernels.gemm_bf16(w, x, 64)
     assert torch.equal(a, b)
+
+
+def test_gemm_deterministic_stream_k(cuda):
+    from paper_2603_02599_b200 import kernels
+
+    g = torch.Generator(device="cpu").manual_seed(4)
+    w = (torch.randn(28672, 4096, generator=g) * 0.02).to(torch.bfloat16).to(cuda)
+    x = torch.randn(64, 4096, generator=g).to(torch.bfloat16).to(cuda)
+    a = kernels.gemm_bf16(w, x, 64)
+    for _ in range(3):
+        assert torch.equal(a, kernels.gemm_bf16(w, x, 64))
+
+
+@pytest.mark.parametrize("sched", ["0", "2"])
+def test_gemm_schedules_subprocess(sched):
+    """The GEMM kernel tests and the end-to-end decode parity under the other
+    schedules: 0 = cluster split-K / whole tiles only, 2 = stream-K on every
+    GEMM whose partials fit (covers every fused epilogue with partial tiles)."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, SUN_GEMM_SCHED=sched)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", "(gemm or tiny) and not subprocess",
+                        os.path.join(here, "test_kernels_gpu.py"), os.path.join(here, "test_decode_parity_gpu.py")],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
 def _attn_ref(q, pool, layer, positions, bt, G):
