@@ -75,8 +75,10 @@ SunStatus sun_block_weights_bf16(const void* w, int64_t rows, int64_t k, void* o
  *  w_gate_up  [ceil(f/64) * 128][hidden]           64-row blocks: gate rows j..j+63 then
  *                                                  up rows j..j+63 (zero rows pad f)
  *  w_down     [hidden][f]
- * For weight_bits == 4, w_* hold packed int4 (two per byte, low nibble = even k,
- * row-major [rows][K/2]) and s_* the bf16 scales [rows][K/group]. */
+ * For weight_bits == 4, w_* hold SUN-W4 packed int4 (8 KB per 128-row x 128-k block,
+ * blocks [row tile][K block], each [4 chunks of 32 k][128 rows][16 B], offset-binary
+ * nibbles in order [0,2,4,6,1,3,5,7] per 8-k word) and s_* the bf16 group scales
+ * tile-major [row tile][K/128][128] (oracle/quant_ref.py restates both). */
 typedef struct SunLayerWeights {
   const void* attn_norm;
   const void* w_qkv;
@@ -175,6 +177,11 @@ SunStatus sun_gemm_bf16_stamped(const void* w, int64_t n_out, int64_t k, const v
 SunStatus sun_gemm_w4(const void* packed, const void* scales, int64_t n_out, int64_t k, const void* x, int64_t ldx,
                       int64_t x_rows, int32_t batch, float* out, int64_t ldo, int32_t accumulate, void* workspace,
                       size_t workspace_bytes, void* stream);
+/* sun_gemm_w4 (store) with per-CTA %globaltimer stamps [grid][16] (profiling only;
+ * slots as sun_gemm_bf16_stamped). */
+SunStatus sun_gemm_w4_stamped(const void* packed, const void* scales, int64_t n_out, int64_t k, const void* x,
+                              int64_t ldx, int64_t x_rows, int32_t batch, float* out, int64_t ldo, void* workspace,
+                              size_t workspace_bytes, void* stream, uint64_t* stamps);
 
 /* Paged split-K decode attention for one layer: q bf16 [batch][nq][d] (post-RoPE),
  * KV from the pool, out bf16 [batch][nq*d]. */
@@ -186,8 +193,9 @@ SunStatus sun_attention_decode(const SunDecoderDims* dims, const SunKvPool* kv, 
 /* y[b] = bf16(x[b] * rsqrt(mean(x[b]^2) + eps) * w), x fp32 [batch][h]. */
 SunStatus sun_rmsnorm(const float* x, const void* w, void* y, int32_t batch, int32_t h, float eps, void* stream);
 
-/* QSUN: quantize bf16 W[rows][K] to packed int4 + bf16 scales (group along K),
- * symmetric, q = clamp(round_half_even(w / s), -8, 7), s = bf16(amax / 7). */
+/* QSUN: quantize bf16 W[rows][K] to SUN-W4 packed int4 + bf16 scales (group 128
+ * along K), symmetric, q = clamp(round_half_even(w / s), -8, 7), s = bf16(amax / 7.5);
+ * packed must be zeroed (padding rows are not written). */
 SunStatus sun_quantize_w4(const void* w, int64_t rows, int64_t k, int32_t group, void* packed, void* scales,
                           void* stream);
 

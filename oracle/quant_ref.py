@@ -13,8 +13,10 @@ SUN-W4 (matches paper_2603_02599_b200/csrc/gemm_w4.cuh):
   s   = bf16(absmax(group) / 7.5)            per (row, 128-wide K group)
   q   = clamp(rint(w / s), -8, 7)  (q = 0 if s == 0), rint = half-to-even
   deq = bf16(q * s)                          (the tcgen05 operand)
-  scales stored [K/128][round_up(rows,128)] bf16
-  packed: block (row//128, k//128) is 128 rows x 64 B contiguous (8 KB); in each
+  scales stored tile-major [round_up(rows,128)/128][K/128][128] bf16 (a weight stage's
+  scales for consecutive K blocks are one contiguous run)
+  packed: block (row//128, k//128) is 8 KB contiguous, laid out [chunk 4][row 128][16 B]:
+  chunk c of row r holds k = 32c .. 32c+31 of that row as 4 words; in each
   32-bit little-endian word the 8 consecutive k elements e0..e7 sit in nibbles
   [e0,e2,e4,e6,e1,e3,e5,e7] (nibble 0 = bits 0..3) as offset-binary q + 8.
 """
@@ -46,7 +48,7 @@ def dequantize(q: torch.Tensor, s: torch.Tensor, group: int = 128) -> torch.Tens
 
 
 def pack(q: torch.Tensor, s: torch.Tensor) -> tuple[np.ndarray, np.ndarray]:
-    """(q [rows,K], s [rows,K/128]) -> (packed uint8 flat, scales bf16-bits uint16 [K/128, rows_pad])."""
+    """(q [rows,K], s [rows,K/128]) -> (packed uint8 flat, scales bf16-bits uint16 [rows_pad/128, K/128, 128])."""
     rows, k = q.shape
     rows_pad = (rows + 127) // 128 * 128
     u = np.zeros((rows_pad, k), dtype=np.uint32)
@@ -55,19 +57,21 @@ def pack(q: torch.Tensor, s: torch.Tensor) -> tuple[np.ndarray, np.ndarray]:
     words = np.zeros((rows_pad, k // 8), dtype=np.uint32)
     for e in range(8):
         words |= u[:, e::8] << np.uint32(4 * NIBBLE_OF_ELEM[e])
-    # tile-contiguous: [row_tile][k_block][128 rows][16 words]
+    # tile-contiguous: [row_tile][k_block][chunk 4][128 rows][4 words]
     kb = k // 128
-    t = words.reshape(rows_pad // 128, 128, kb, 16).transpose(0, 2, 1, 3)
+    t = words.reshape(rows_pad // 128, 128, kb, 4, 4).transpose(0, 2, 3, 1, 4)
     packed = np.ascontiguousarray(t).view(np.uint8).reshape(-1)
-    sc = np.zeros((kb, rows_pad), dtype=np.uint16)
-    sc[:, :rows] = s.view(torch.int16).numpy().astype(np.uint16).T
+    sc = np.zeros((rows_pad, kb), dtype=np.uint16)
+    sc[:rows] = s.view(torch.int16).numpy().astype(np.uint16)
+    sc = np.ascontiguousarray(sc.reshape(rows_pad // 128, 128, kb).transpose(0, 2, 1))
     return packed, sc
 
 
 def unpack(packed: np.ndarray, rows: int, k: int) -> torch.Tensor:
     rows_pad = (rows + 127) // 128 * 128
     kb = k // 128
-    words = packed.view(np.uint32).reshape(rows_pad // 128, kb, 128, 16).transpose(0, 2, 1, 3).reshape(rows_pad, k // 8)
+    words = (packed.view(np.uint32).reshape(rows_pad // 128, kb, 4, 128, 4).transpose(0, 3, 1, 2, 4)
+             .reshape(rows_pad, k // 8))
     u = np.zeros((rows_pad, k), dtype=np.int32)
     for e in range(8):
         u[:, e::8] = (words >> np.uint32(4 * NIBBLE_OF_ELEM[e])) & np.uint32(0xF)

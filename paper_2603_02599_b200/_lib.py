@@ -78,6 +78,8 @@ SIGNATURES = {
                                       c_size, c_vp, c_vp]),
     "sun_gemm_w4": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i32, c_vp, c_i64, c_i32, c_vp,
                             c_size, c_vp]),
+    "sun_gemm_w4_stamped": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i32, c_vp, c_i64, c_vp,
+                                    c_size, c_vp, c_vp]),
     "sun_attention_decode": (c_i32, [ctypes.POINTER(SunDecoderDims), ctypes.POINTER(SunKvPool), c_i32, c_vp,
                                      c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_size, c_vp]),
     "sun_blocked_bytes": (c_i32, [c_i64, c_i64, ctypes.POINTER(c_size)]),

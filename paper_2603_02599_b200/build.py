@@ -46,7 +46,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not needs_build():
         return LIB
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(tmp), *map(str, SOURCES)]
+    extra = os.environ.get("SUN_NVCC_EXTRA", "").split()  # experiments only (e.g. -DSUN_W4_CONV_WARPS=16)
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", str(tmp), *map(str, SOURCES)]
     proc = subprocess.run(cmd, cwd=str(CSRC), capture_output=True, text=True)
     log = proc.stdout + proc.stderr
     (PKG / "build.log").write_text(" ".join(cmd) + "\n" + log)

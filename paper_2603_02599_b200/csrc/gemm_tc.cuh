@@ -53,7 +53,10 @@ struct GemmArgs {
   int ksteps;        // ceil(kb64 / 2): 128-wide pipeline stages per tile
   int m_tiles;       // ceil(n_out / 128)
   int splits;        // cluster split-K factor S (> 1: cluster schedule)
-  int stages;        // smem pipeline depth
+  int stages;        // smem pipeline depth (W4: weight stages of wgroup K blocks)
+  int xstages;       // W4: activation stages of xk K blocks
+  int wgroup;        // W4: K blocks per weight stage (packed [wgroup][8 KB] | scales [wgroup][256 B])
+  int xk;            // W4: K blocks per activation stage
   // STORE / RESID / LOGITS
   float* out_f32;
   long long ldo;
@@ -109,12 +112,22 @@ SUN_DEVICE unsigned long long gtimer() {
   do { if (a.stamps) a.stamps[blockIdx.x * 16 + (i)] = gtimer(); } while (0)
 
 constexpr int kGemmThreads = 192;
-constexpr int kW4Threads = 320;
+#ifndef SUN_W4_CONV_WARPS
+#define SUN_W4_CONV_WARPS 8
+#endif
+// converter warps: 4 per SM sub-partition (lane group) hide ALU / TMEM-store latency;
+// each takes 128 / (warps / 4) K elements of its 32 rows per 128-wide K block
+constexpr int kW4ConvThreads = SUN_W4_CONV_WARPS * 32;
+constexpr int kW4KParts = SUN_W4_CONV_WARPS / 4;
+constexpr int kW4Chunks = 4 / kW4KParts;  // 16-byte packed chunks (32 k) per converter thread
+constexpr int kW4Threads = 192 + kW4ConvThreads + 32;  // + the activation-producer warp
 constexpr int kTileM = 128;
 constexpr int kTileK = 64;
 constexpr uint32_t kTileWBytes = kTileM * kTileK * 2;  // 16 KB: one SUN-BLK block
 constexpr uint32_t kW4PackedBytes = kTileM * 128 / 2;  // 8 KB: one SUN-W4 block (128 x 128)
-constexpr uint32_t kW4DeqBytes = kTileM * 128 * 2;     // 32 KB dequantised bf16 tile
+__host__ __device__ inline uint32_t w4_wstage_bytes(int wgroup) { return static_cast<uint32_t>(wgroup) * (kW4PackedBytes + 256u); }
+constexpr int kMaxWStages = 16, kMaxXStages = 8;
+constexpr int kW4MaxABufs = 6;  // W4: dequantised 128x128 A tiles (64 TMEM columns each) at the top of TMEM
 
 // partner staging [16][128] f32 | argmax scratch 512 B | column meta: pos[256], page[256], r_b[256] | 512 spare
 constexpr uint32_t kEpiSmemBytes = 16 * kTileM * 4 + 512 + 3072 + 512;
@@ -129,14 +142,25 @@ __host__ __device__ inline uint32_t gemm_stage_bytes(int bn, bool w4) {
   return (w4 ? kW4PackedBytes + 1024u : 2u * kTileWBytes) + static_cast<uint32_t>(bn) * 256u;
 }
 __host__ __device__ inline size_t gemm_smem_bytes(int bn, int stages, bool w4) {
-  return 1024 + (w4 ? 2 * size_t(kW4DeqBytes) : 0) + static_cast<size_t>(stages) * gemm_stage_bytes(bn, w4) +
-         kEpiSmemBytes + 512;
+  return 1024 + static_cast<size_t>(stages) * gemm_stage_bytes(bn, w4) + kEpiSmemBytes + 1024;
+}
+__host__ __device__ inline uint32_t w4_xstage_bytes(int bn, int xk) { return static_cast<uint32_t>(xk * bn) * 256u; }
+__host__ __device__ inline size_t gemm_smem_bytes_w4(int bn, int wgroup, int wstages, int xk, int xstages) {
+  return 1024 + (static_cast<size_t>(wstages) * w4_wstage_bytes(wgroup) + 1023) / 1024 * 1024 +
+         static_cast<size_t>(xstages) * w4_xstage_bytes(bn, xk) + kEpiSmemBytes + 1024;
 }
 
 __host__ __device__ inline uint32_t tmem_cols_for(int bn) {
   uint32_t c = 32;
   while (c < static_cast<uint32_t>(2 * bn)) c <<= 1;
   return c;
+}
+// accumulator buffers: 2 (epilogue of tile i overlaps tile i+1) unless W4's A tiles leave no room
+__host__ __device__ inline int acc_buffers(int bn, bool w4) { return (w4 && 2 * bn > 512 - 2 * 64) ? 1 : 2; }
+// W4 A-tile ring depth: what the 512 TMEM columns leave after the accumulators
+__host__ __device__ inline int w4_abufs(int bn) {
+  const int n = (512 - acc_buffers(bn, true) * bn) / 64;
+  return n < kW4MaxABufs ? n : kW4MaxABufs;
 }
 
 SUN_DEVICE void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
@@ -487,32 +511,41 @@ SUN_DEVICE void sk_owner_epilogue(const GemmArgs& a, int tile, uint32_t taddr, i
     for (int cc = c + 1; cc < c_hi; ++cc) a.sk_flags[cc] = 0u;
 }
 
-SUN_DEVICE void cvt_bar() { asm volatile("bar.sync 2, 128;" ::: "memory"); }
 
-// Dequantise one 128x128 block: packed (128 rows x 64 B) + scales -> SW128 bf16 tile.
-SUN_DEVICE void w4_dequant_block(const uint8_t* pk, const __nv_bfloat16* sc, uint8_t* dq, int ct) {
+SUN_DEVICE uint32_t lop3_and_or(uint32_t a, uint32_t mask, uint32_t magic) {  // (a & mask) | magic
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(mask), "r"(magic));
+  return d;
+}
+
+// QSUN dequantisation for one converter thread and one 128x128 K block: its TMEM
+// lane `row`, K part `part` (kW4Chunks packed 16-byte chunks of the SUN-W4 block
+// [4 chunks][128 rows][16 B], so a warp's 16-byte loads are 512 B contiguous).
+// Per packed word (8 k): 3 shifts, 4 LOP3 (mask | magic -> bf16 128 + u), 4 HSUB2
+// (exact), 4 HMUL2 (one rounding) -> bf16(q * s); output column c of the A tile
+// holds k = (2c, 2c + 1), written with one tcgen05.st of 32 columns.
+SUN_DEVICE void w4_dequant_row(uint32_t pk, uint32_t sc, int row, int part, uint32_t (&o)[16 * kW4Chunks]) {
+  const uint32_t magic = 0x43004300u;
   const __nv_bfloat162 off = __floats2bfloat162_rn(136.f, 136.f);
+  uint32_t words[4 * kW4Chunks];
 #pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    const int r = p * 32 + (ct >> 2);
-    const int c4 = ct & 3;  // 16-byte packed chunk = 32 k elements
-    const uint4 w = *reinterpret_cast<const uint4*>(pk + r * 64 + c4 * 16);
-    const __nv_bfloat162 s2 = __bfloat162bfloat162(sc[r]);
-    const uint32_t words[4] = {w.x, w.y, w.z, w.w};
+  for (int c = 0; c < kW4Chunks; ++c)
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(words[4 * c]), "=r"(words[4 * c + 1]), "=r"(words[4 * c + 2]), "=r"(words[4 * c + 3])
+                 : "r"(pk + ((kW4Chunks * part + c) * kTileM + row) * 16));
+  unsigned short sraw;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sraw) : "r"(sc + row * 2));
+  __nv_bfloat16 sb;
+  *reinterpret_cast<unsigned short*>(&sb) = sraw;
+  const __nv_bfloat162 s2 = __bfloat162bfloat162(sb);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint32_t o[4];
+  for (int q = 0; q < 4 * kW4Chunks; ++q) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const uint32_t u = ((words[q] >> (4 * e)) & 0x000F000Fu) | 0x43004300u;
-        __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(&u);
-        v = __hmul2(__hsub2(v, off), s2);
-        o[e] = *reinterpret_cast<uint32_t*>(&v);
-      }
-      const int c = c4 * 4 + q;  // 16-byte bf16 chunk index within the 128-wide k block
-      const int atom = c >> 3;
-      const int phys = (c & 7) ^ (r & 7);
-      *reinterpret_cast<uint4*>(dq + atom * (kTileM * 128) + r * 128 + phys * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t u = lop3_and_or(words[q] >> (4 * e), 0x000F000Fu, magic);
+      __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(&u);
+      v = __hmul2(__hsub2(v, off), s2);
+      o[q * 4 + e] = *reinterpret_cast<uint32_t*>(&v);
     }
   }
 }
@@ -523,18 +556,23 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int stages = a.stages;
-  const uint32_t sb = gemm_stage_bytes(a.bn, W4);
-  const uint32_t xoff = W4 ? kW4PackedBytes + 1024u : 2u * kTileWBytes;  // X offset inside a stage
-  uint8_t* deq = smem;                                                    // W4: [2][32 KB]
-  uint8_t* stg = smem + (W4 ? 2 * kW4DeqBytes : 0);
-  float* epi = reinterpret_cast<float*>(stg + stages * sb);
+  const uint32_t sb = W4 ? w4_wstage_bytes(a.wgroup) : gemm_stage_bytes(a.bn, W4);
+  const uint32_t xoff = 2u * kTileWBytes;  // bf16: X offset inside a stage
+  const int xstages = W4 ? a.xstages : 0;
+  const uint32_t xsb = W4 ? w4_xstage_bytes(a.bn, a.xk) : 0u;
+  const int wg = a.wgroup;
+  uint8_t* stg = smem;
+  uint8_t* xstg = stg + ((stages * sb + 1023u) & ~1023u);  // W4 activation ring (SW128 atoms: 1 KB aligned)
+  float* epi = reinterpret_cast<float*>(xstg + xstages * xsb);
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(epi) + kEpiSmemBytes);
-  uint64_t* empty = full + stages;
-  uint64_t* tfull = empty + stages;  // [2]
-  uint64_t* tempty = tfull + 2;      // [2]
-  uint64_t* dfull = tempty + 2;      // [2] W4
-  uint64_t* dempty = dfull + 2;      // [2] W4
-  uint64_t* skbar = dempty + 2;      // stream-K owner: contributor partials landed
+  uint64_t* empty = full + kMaxWStages;
+  uint64_t* xfull = empty + kMaxWStages;       // [kMaxXStages] W4
+  uint64_t* xempty = xfull + kMaxXStages;      // [kMaxXStages] W4
+  uint64_t* tfull = xempty + kMaxXStages;      // [2]
+  uint64_t* tempty = tfull + 2;                // [2]
+  uint64_t* dfull = tempty + 2;                // [kW4MaxABufs] W4: A tile dequantised
+  uint64_t* dempty = dfull + kW4MaxABufs;      // [kW4MaxABufs] W4: A tile consumed by the MMA
+  uint64_t* skbar = dempty + kW4MaxABufs;      // stream-K owner: contributor partials landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(skbar + 1);
 
   const int warp = warp_id_sync();
@@ -558,19 +596,27 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
   const int n = u1 - u0;
   const int t_first = u0 / KS;
   const int nseg = n > 0 ? (u1 - 1) / KS - t_first + 1 : 0;
-  const uint32_t ncols = tmem_cols_for(a.bn);
+  const uint32_t ncols = W4 ? 512u : tmem_cols_for(a.bn);
+  const int nbuf = acc_buffers(a.bn, W4);
+  const int na = W4 ? w4_abufs(a.bn) : 1;  // A tile i at TMEM column 512 - 64 (i + 1)
   const long long rows_pad = static_cast<long long>(a.m_tiles) * kTileM;
   if (threadIdx.x == 0) SUN_STAMP(0);
 
   if (warp == 0 && elect_one()) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], W4 ? 2 : 1);
+      mbar_init(&empty[s], W4 ? kW4ConvThreads / 32 : 1);  // W4: every converter warp; bf16: MMA commit
+    }
+    for (int s = 0; s < xstages; ++s) {
+      mbar_init(&xfull[s], 1);
+      mbar_init(&xempty[s], 1);
     }
     for (int j = 0; j < 2; ++j) {
       mbar_init(&tfull[j], 1);
       mbar_init(&tempty[j], 1);
-      mbar_init(&dfull[j], 1);
+    }
+    for (int j = 0; j < kW4MaxABufs; ++j) {
+      mbar_init(&dfull[j], kW4ConvThreads / 32);
       mbar_init(&dempty[j], 1);
     }
     mbar_init(skbar, 1);
@@ -589,7 +635,101 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
 
   auto nblk_of = [&](int ks) { return min(2, a.kb64 - 2 * ks); };
 
-  if (warp == 0) {
+  if (W4 && (warp == 0 || warp == 6 + kW4ConvThreads / 32)) {
+    // ---------------- W4 producers (blocking, one per ring): warp 0 streams the
+    // weight stages (wgroup K blocks: packed + scales, two bulk requests), the
+    // last warp the activation stages (xk K blocks, one request), so the weight
+    // ring runs ahead of the MMA by its whole depth whatever the activation ring's.
+    if (elect_one()) {
+      const bool wprod = warp == 0;
+      const int grp = wprod ? wg : a.xk;
+      const int depth = wprod ? stages : xstages;
+      uint64_t* fb = wprod ? full : xfull;
+      uint64_t* eb = wprod ? empty : xempty;
+      if (!wprod) pdl_wait();  // activations are the previous kernel's output
+      int ks = u0 % KS, seg_left = min(KS - ks, n), slot = 0, phase = 0;
+      for (int j = 0; j < n;) {
+        const int len = min(grp, seg_left);
+        if (j >= depth) mbar_wait(&eb[slot], phase ^ 1);
+        if (wprod) {
+          const long long blk = static_cast<long long>(u0 + j);  // = tile * KS + ks
+          uint8_t* st = stg + slot * sb;
+          mbar_arrive_expect_tx(&fb[slot], static_cast<uint32_t>(len) * (kW4PackedBytes + 256u));
+          bulk_load_hint(st, a.w4_packed + blk * kW4PackedBytes, len * kW4PackedBytes, &fb[slot], kEvictFirst);
+          bulk_load_hint(st + wg * kW4PackedBytes, a.w4_scales + blk * kTileM, len * 256u, &fb[slot], kEvictFirst);
+        } else {
+          mbar_arrive_expect_tx(&fb[slot], static_cast<uint32_t>(len) * a.bn * 256u);
+          bulk_load_hint(xstg + slot * xsb, a.xact + static_cast<long long>(2 * ks) * a.bn * 128, len * a.bn * 256u,
+                         &fb[slot], kEvictLast);
+        }
+        j += len;
+        ks += len;
+        seg_left -= len;
+        if (seg_left == 0) {
+          ks = 0;
+          seg_left = min(KS, n - j);
+        }
+        if (++slot == depth) {
+          slot = 0;
+          phase ^= 1;
+        }
+      }
+      if (wprod) pdl_wait();
+    }
+  } else if (W4 && warp == 1) {
+    // ---------------- W4 MMA issuer: A (dequantised weights) from TMEM, X from smem
+    const uint32_t idesc = make_idesc_bf16(kTileM, a.bn);
+    int ks = u0 % KS, seg_left = min(KS - ks, n);
+    int xslot = 0, xphase = 0, xpos = 0, aslot = 0, aphase = 0, buf = 0, tphase = 0;
+    for (int j = 0; j < n; ++j) {
+      const bool first = j == 0 || ks == 0, last = seg_left == 1;
+      const bool xlast = xpos + 1 == a.xk || last;
+      if (first) {
+        mbar_wait(&tempty[buf], tphase ^ 1);
+        tc_fence_after();
+      }
+      if (xpos == 0) mbar_wait(&xfull[xslot], xphase);
+      mbar_wait(&dfull[aslot], aphase);
+      tc_fence_after();
+      if (j == 0 && threadIdx.x == 32) SUN_STAMP(2);
+      if (elect_one()) {
+        const uint32_t xa = smem_u32(xstg + xslot * xsb) + static_cast<uint32_t>(xpos) * 2u * a.bn * 128u;
+        const uint32_t tacc = tmem_base + static_cast<uint32_t>(buf * a.bn);
+        const uint32_t ta = tmem_base + static_cast<uint32_t>(512 - 64 * (aslot + 1));
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_bf16_ta(tacc, ta + kk * 8, make_sw128_desc(xa + (kk >> 2) * (a.bn * 128u) + (kk & 3) * 32), idesc,
+                       (first && kk == 0) ? 0u : 1u);
+        umma_commit(&dempty[aslot]);
+        if (xlast) umma_commit(&xempty[xslot]);
+        if (last) umma_commit(&tfull[buf]);
+      }
+      __syncwarp();
+      if (++aslot == na) {
+        aslot = 0;
+        aphase ^= 1;
+      }
+      if (xlast) {
+        xpos = 0;
+        if (++xslot == xstages) {
+          xslot = 0;
+          xphase ^= 1;
+        }
+      } else {
+        ++xpos;
+      }
+      ++ks;
+      if (--seg_left == 0) {
+        ks = 0;
+        seg_left = min(KS, n - j - 1);
+        if (++buf == nbuf) {
+          buf = 0;
+          tphase ^= 1;
+        }
+      }
+    }
+    if (threadIdx.x == 32) SUN_STAMP(3);
+  } else if (warp == 0) {
     if (elect_one()) {
       // issue weight (or packed+scales) loads of stage j; X is added separately
       auto issue_w = [&](int j) {
@@ -597,23 +737,14 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
         const int tile = (u0 + j) / KS;
         const int ks = (u0 + j) % KS;
         const int nb = nblk_of(ks);
-        uint8_t* st = stg + s * sb;
-        if constexpr (W4) {
-          mbar_arrive_expect_tx(&full[s], kW4PackedBytes + 256u + 2u * a.bn * 128u);
-          bulk_load_hint(st, a.w4_packed + (static_cast<long long>(tile) * a.ksteps + ks) * kW4PackedBytes,
-                         kW4PackedBytes, &full[s], kEvictFirst);
-          bulk_load_hint(st + kW4PackedBytes, a.w4_scales + ks * rows_pad + static_cast<long long>(tile) * kTileM,
-                         256u, &full[s], kEvictFirst);
-        } else {
-          mbar_arrive_expect_tx(&full[s], nb * (kTileWBytes + a.bn * 128u));
-          bulk_load_hint(st, a.wblk + (static_cast<long long>(tile) * a.kb64 + 2 * ks) * kTileWBytes,
-                         nb * kTileWBytes, &full[s], kEvictFirst);
-        }
+        mbar_arrive_expect_tx(&full[s], nb * (kTileWBytes + a.bn * 128u));
+        bulk_load_hint(stg + s * sb, a.wblk + (static_cast<long long>(tile) * a.kb64 + 2 * ks) * kTileWBytes,
+                       nb * kTileWBytes, &full[s], kEvictFirst);
       };
       auto issue_x = [&](int j) {
         const int s = j % stages;
         const int ks = (u0 + j) % KS;
-        const int nb = W4 ? 2 : nblk_of(ks);
+        const int nb = nblk_of(ks);
         bulk_load_hint(stg + s * sb + xoff, a.xact + static_cast<long long>(2 * ks) * a.bn * 128,
                        nb * a.bn * 128u, &full[s], kEvictLast);
       };
@@ -622,33 +753,31 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
       pdl_wait();
       for (int j = 0; j < pre; ++j) issue_x(j);
       for (int j = pre; j < n; ++j) {
-        const int s = j % stages;
-        mbar_wait(&empty[s], ((j / stages) & 1) ^ 1);
+        mbar_wait(&empty[j % stages], ((j / stages) & 1) ^ 1);
         issue_w(j);
         issue_x(j);
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && !W4) {
     const uint32_t idesc = make_idesc_bf16(kTileM, a.bn);
     int seg = 0;
     for (int j = 0; j < n; ++j) {
       const int s = j % stages;
       const int ks = (u0 + j) % KS;
       const bool first = j == 0 || ks == 0, last = j == n - 1 || ks == KS - 1;
-      const int buf = seg & 1;
+      const int buf = seg % nbuf;
       const int nb = nblk_of(ks);
       if (first) {
-        mbar_wait(&tempty[buf], ((seg >> 1) & 1) ^ 1);
+        mbar_wait(&tempty[buf], ((seg / nbuf) & 1) ^ 1);
         tc_fence_after();
       }
       mbar_wait(&full[s], (j / stages) & 1);
-      if constexpr (W4) mbar_wait(&dfull[j & 1], (j >> 1) & 1);
       tc_fence_after();
       if (j == 0 && threadIdx.x == 32) SUN_STAMP(2);
       if (elect_one()) {
-        const uint32_t wa = W4 ? smem_u32(deq + (j & 1) * kW4DeqBytes) : smem_u32(stg + s * sb);
         const uint32_t xa = smem_u32(stg + s * sb + xoff);
         const uint32_t tacc = tmem_base + static_cast<uint32_t>(buf * a.bn);
+        const uint32_t wa = smem_u32(stg + s * sb);
         for (int kk = 0; kk < nb * 4; ++kk) {
           const uint32_t atom = kk >> 2;
           const uint32_t koff = (kk & 3) * 32;
@@ -656,7 +785,6 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
                     make_sw128_desc(xa + atom * (a.bn * 128u) + koff), idesc, (first && kk == 0) ? 0u : 1u);
         }
         umma_commit(&empty[s]);
-        if constexpr (W4) umma_commit(&dempty[j & 1]);
         if (last) umma_commit(&tfull[buf]);
       }
       __syncwarp();
@@ -670,11 +798,11 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
     const int q = warp & 3;
     const int row_local = q * 32 + (threadIdx.x & 31);
     for (int seg = 0; seg < nseg; ++seg) {
-      const int buf = seg & 1;
+      const int buf = seg % nbuf;
       const int tile = t_first + seg;
       const int kb = max(u0, tile * KS) - tile * KS;
       const int ke = min(u1, (tile + 1) * KS) - tile * KS;
-      mbar_wait(&tfull[buf], (seg >> 1) & 1);
+      mbar_wait(&tfull[buf], (seg / nbuf) & 1);
       tc_fence_after();
       if (threadIdx.x == 64 && seg == 0) SUN_STAMP(4);
       const uint32_t taddr = tmem_base + static_cast<uint32_t>(buf * a.bn) + (static_cast<uint32_t>(q * 32) << 16);
@@ -700,21 +828,42 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
         }
       }
     }
-  } else if constexpr (W4) {
-    // ---------------- converters: warps 6..9 ----------------
-    const int ct = threadIdx.x - 192;
+  } else if (W4 && warp < 6 + kW4ConvThreads / 32) {
+    // ---------------- converters: lane group warp % 4, K part (warp - 6) / 4 ----------------
+    const int lg = warp & 3;  // TMEM lanes this warp may access
+    const int row = lg * 32 + (threadIdx.x & 31);
+    const int part = (warp - 6) >> 2;  // columns [16 * kW4Chunks * part, +16 * kW4Chunks) of each A tile
+    const uint32_t lane_off = static_cast<uint32_t>(lg * 32) << 16;
+    int ks = u0 % KS, seg_left = min(KS - ks, n);
+    int wslot = 0, wphase = 0, wpos = 0, aslot = 0, aphase = 0;
     for (int j = 0; j < n; ++j) {
-      const int s = j % stages;
-      mbar_wait(&full[s], (j / stages) & 1);
-      if (j >= 2) mbar_wait(&dempty[j & 1], ((j >> 1) & 1) ^ 1);
-      const uint8_t* pk = stg + s * sb;
-      w4_dequant_block(pk, reinterpret_cast<const __nv_bfloat16*>(pk + kW4PackedBytes), deq + (j & 1) * kW4DeqBytes, ct);
-      fence_proxy_async_smem();
-      cvt_bar();
-      if (ct == 0) {
-        mbar_arrive(&dfull[j & 1]);
-        mbar_arrive(&empty[s]);
+      if (wpos == 0) mbar_wait(&full[wslot], wphase);
+      const bool wlast = wpos + 1 == wg || seg_left == 1;
+      const uint32_t st = smem_u32(stg + wslot * sb);
+      uint32_t o[16 * kW4Chunks];
+      w4_dequant_row(st + wpos * kW4PackedBytes, st + wg * kW4PackedBytes + wpos * 256u, row, part, o);
+      if (wlast) {  // this warp is done reading the weight stage
+        __syncwarp();
+        if (elect_one()) mbar_arrive(&empty[wslot]);
+        wpos = 0;
+        if (++wslot == stages) {
+          wslot = 0;
+          wphase ^= 1;
+        }
+      } else {
+        ++wpos;
       }
+      if (j >= na) mbar_wait(&dempty[aslot], aphase ^ 1);  // MMA j-na done with this A tile
+      tc_fence_after();
+      tmem_st(tmem_base + lane_off + static_cast<uint32_t>(512 - 64 * (aslot + 1) + 16 * kW4Chunks * part), o);
+      tc_fence_before();
+      __syncwarp();
+      if (elect_one()) mbar_arrive(&dfull[aslot]);
+      if (++aslot == na) {
+        aslot = 0;
+        aphase ^= 1;
+      }
+      if (--seg_left == 0) seg_left = min(KS, n - j - 1);
     }
   }
 
@@ -781,10 +930,10 @@ __global__ void quantize_w4_kernel(const __nv_bfloat16* __restrict__ w, long lon
   for (int i = 0; i < 128; ++i) amax = fmaxf(amax, fabsf(__bfloat162float(src[i])));
   const __nv_bfloat16 sb = __float2bfloat16_rn(amax / 7.5f);
   const float s = __bfloat162float(sb);
-  scales[g * rows_pad + r] = sb;
+  scales[((r / 128) * (k / 128) + g) * 128 + (r % 128)] = sb;  // tile-major [row tile][K block][128]
   const long long kb_total = k / 128;
-  uint8_t* dst = packed + ((r / 128) * kb_total + g) * 8192 + (r % 128) * 64;
-  for (int wd = 0; wd < 16; ++wd) {  // 16 words of 8 elements
+  uint8_t* blk = packed + ((r / 128) * kb_total + g) * 8192;
+  for (int wd = 0; wd < 16; ++wd) {  // 16 words of 8 elements; word wd lives in chunk wd / 4
     uint32_t word = 0;
     for (int e = 0; e < 8; ++e) {
       const float x = __bfloat162float(src[wd * 8 + e]);
@@ -797,7 +946,7 @@ __global__ void quantize_w4_kernel(const __nv_bfloat16* __restrict__ w, long lon
       const int nib = (e & 1) ? 4 + (e >> 1) : (e >> 1);  // order [0,2,4,6,1,3,5,7]
       word |= u << (4 * nib);
     }
-    reinterpret_cast<uint32_t*>(dst)[wd] = word;
+    reinterpret_cast<uint32_t*>(blk + ((wd >> 2) * 128 + (r % 128)) * 16)[wd & 3] = word;
   }
 }
 

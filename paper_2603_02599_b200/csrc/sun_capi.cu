@@ -142,9 +142,9 @@ int gemm_max_grid() {
 
 int gemm_stages(int bn, bool w4, int per_sm) {
   const int budget = kSmemPerSm / per_sm - 2048;
-  const int avail = budget - 1024 - (w4 ? 2 * int(kW4DeqBytes) : 0) - int(kEpiSmemBytes) - 512;
+  const int avail = budget - 1024 - int(kEpiSmemBytes) - 512;
   int st = avail / int(gemm_stage_bytes(bn, w4));
-  return std::max(2, std::min(6, st));
+  return std::max(2, std::min(w4 ? 16 : 6, st));  // barrier region (512 B) holds <= 16 stages
 }
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -409,8 +409,26 @@ SunStatus run_gemm(const void* wblk, const void* packed, const void* scales, Gem
   a.w4_scales = static_cast<const __nv_bfloat16*>(scales);
   const int per_sm = gemm_ctas_per_sm(a.bn, w4);
   const int slots = std::min(kNumSms * per_sm, gemm_max_grid());
-  a.stages = gemm_stages(a.bn, w4, per_sm);
-  const size_t smem = gemm_smem_bytes(a.bn, a.stages, w4);
+  size_t smem, ring;
+  if (w4) {
+    // weight stages of wgroup K blocks (one packed + one scales request each),
+    // activation stages of xk K blocks; 3 activation stages, weights fill the rest
+    static const int env_wg = [] { const char* e = getenv("SUN_W4_WGROUP"); return e ? atoi(e) : 0; }();
+    static const int env_xk = [] { const char* e = getenv("SUN_W4_XK"); return e ? atoi(e) : 0; }();
+    static const int env_xs = [] { const char* e = getenv("SUN_W4_XSTAGES"); return e ? atoi(e) : 0; }();
+    a.wgroup = env_wg > 0 ? env_wg : 4;
+    a.xk = env_xk > 0 ? env_xk : (a.bn <= 32 ? 4 : (a.bn <= 64 ? 2 : 1));
+    a.xstages = env_xs > 0 ? env_xs : (a.bn > 128 ? 2 : 3);
+    const int budget = kSmemPerSm - 2048 - 2048 - int(kEpiSmemBytes) - 1024 -
+                       a.xstages * int(w4_xstage_bytes(a.bn, a.xk));
+    a.stages = std::max(2, std::min(16, budget / int(w4_wstage_bytes(a.wgroup))));
+    smem = gemm_smem_bytes_w4(a.bn, a.wgroup, a.stages, a.xk, a.xstages);
+    ring = size_t(a.stages) * w4_wstage_bytes(a.wgroup) + size_t(a.xstages) * w4_xstage_bytes(a.bn, a.xk);
+  } else {
+    a.stages = gemm_stages(a.bn, w4, per_sm);
+    smem = gemm_smem_bytes(a.bn, a.stages, w4);
+    ring = size_t(a.stages) * gemm_stage_bytes(a.bn, w4);
+  }
   int S, grid;
   // Stream-K where whole tiles cannot balance over the SMs (more tiles than CTA
   // slots, e.g. gate_up 224 tiles / 148 SMs = 1.51) and every owner's
@@ -422,7 +440,7 @@ SunStatus run_gemm(const void* wblk, const void* packed, const void* scales, Gem
   // (SUN_GEMM_SCHED=2 forces stream-K on every GEMM whose partials fit: tests)
   const bool sk = gemm_sched() != 0 && a.sk_part != nullptr && a.sk_flags != nullptr &&
                   (gemm_sched() == 2 || (p.m_tiles > slots && p.m_tiles % sk_grid != 0)) &&
-                  size_t(max_contrib) * a.bn * kTileM * 4 <= size_t(a.stages) * gemm_stage_bytes(a.bn, w4);
+                  size_t(max_contrib) * a.bn * kTileM * 4 <= ring;
   if (sk) {
     S = 1;
     a.sk_units = units;
@@ -791,6 +809,14 @@ SunStatus sun_gemm_w4(const void* packed, const void* scales, int64_t n_out, int
                                               workspace, workspace_bytes, stream, nullptr)
                     : gemm_api<EPI_STORE_F32>(nullptr, packed, scales, n_out, k, x, ldx, x_rows, batch, out, ldo,
                                               workspace, workspace_bytes, stream, nullptr);
+}
+
+SunStatus sun_gemm_w4_stamped(const void* packed, const void* scales, int64_t n_out, int64_t k, const void* x,
+                              int64_t ldx, int64_t x_rows, int32_t batch, float* out, int64_t ldo, void* workspace,
+                              size_t workspace_bytes, void* stream, uint64_t* stamps) {
+  if (k % 128 != 0) return fail(SUN_ERR_UNSUPPORTED, "W4 needs k multiple of 128");
+  return gemm_api<EPI_STORE_F32>(nullptr, packed, scales, n_out, k, x, ldx, x_rows, batch, out, ldo, workspace,
+                                 workspace_bytes, stream, stamps);
 }
 
 SunStatus sun_attention_decode(const SunDecoderDims* dims, const SunKvPool* kv, int32_t layer, const void* q,

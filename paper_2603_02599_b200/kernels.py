@@ -74,12 +74,13 @@ def gemm_bf16(w: torch.Tensor, x: torch.Tensor, batch: int, out: torch.Tensor | 
 
 
 def gemm_w4(packed: torch.Tensor, scales: torch.Tensor, n_out: int, k: int, x: torch.Tensor, batch: int,
-            out: torch.Tensor | None = None, accumulate: bool = False) -> torch.Tensor:
+            out: torch.Tensor | None = None, accumulate: bool = False,
+            workspace: torch.Tensor | None = None) -> torch.Tensor:
     """QSUN W4A16 GEMM: out[b, n] (=|+=) sum_k deq(w)[n, k] x[b, k]."""
     _need_cuda(packed, scales, x)
     if out is None:
         out = torch.zeros(batch, n_out, dtype=torch.float32, device=x.device)
-    ws = gemm_workspace(n_out, k, batch, x.device)
+    ws = gemm_workspace(n_out, k, batch, x.device) if workspace is None else workspace
     lib = _lib.load()
     _lib.check(lib.sun_gemm_w4(packed.data_ptr(), scales.data_ptr(), n_out, k, x.data_ptr(), x.stride(0), x.shape[0],
                                batch, out.data_ptr(), out.stride(0), int(accumulate), ws.data_ptr(), ws.numel(),
@@ -117,12 +118,12 @@ def rmsnorm(x: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
 
 
 def quantize_w4(w: torch.Tensor, group: int = 128) -> tuple[torch.Tensor, torch.Tensor]:
-    """QSUN SUN-W4 quantisation on the GPU -> (packed uint8, scales bf16 [K/g, rows_pad])."""
+    """QSUN SUN-W4 quantisation on the GPU -> (packed uint8, scales bf16 [rows_pad/128, K/g, 128])."""
     _need_cuda(w)
     rows, k = w.shape
     rows_pad = (rows + 127) // 128 * 128
     packed = torch.zeros(rows_pad * k // 2, dtype=torch.uint8, device=w.device)
-    scales = torch.zeros(k // group, rows_pad, dtype=torch.bfloat16, device=w.device)
+    scales = torch.zeros(rows_pad // 128, k // group, 128, dtype=torch.bfloat16, device=w.device)
     lib = _lib.load()
     _lib.check(lib.sun_quantize_w4(w.contiguous().data_ptr(), rows, k, group, packed.data_ptr(), scales.data_ptr(),
                                    _stream()), "sun_quantize_w4")

@@ -148,10 +148,14 @@ def test_w4_quantizer_bit_exact_vs_oracle(cuda, rows, k):
     q, s = quant_ref.quantize(w)
     p_ref, s_ref = quant_ref.pack(q, s)
     rows_pad = (rows + 127) // 128 * 128
-    pg = packed.cpu().numpy().reshape(rows_pad // 128, k // 128, 128, 64).transpose(0, 2, 1, 3).reshape(rows_pad, -1)
-    pr = p_ref.reshape(rows_pad // 128, k // 128, 128, 64).transpose(0, 2, 1, 3).reshape(rows_pad, -1)
+    def by_row(p):  # SUN-W4 block [chunk 4][row 128][16 B] -> [rows_pad][k/2]
+        return p.reshape(rows_pad // 128, k // 128, 4, 128, 16).transpose(0, 3, 1, 2, 4).reshape(rows_pad, -1)
+
+    pg, pr = by_row(packed.cpu().numpy()), by_row(p_ref)
     assert np.array_equal(pg[:rows], pr[:rows])
-    assert np.array_equal(scales.cpu().view(torch.int16).numpy().astype(np.uint16)[:, :rows], s_ref[:, :rows])
+    sg = scales.cpu().view(torch.int16).numpy().astype(np.uint16)  # [rows_pad/128, K/128, 128]
+    by_row_s = lambda a: a.transpose(0, 2, 1).reshape(rows_pad, -1)  # noqa: E731
+    assert np.array_equal(by_row_s(sg)[:rows], by_row_s(s_ref)[:rows])
     assert torch.equal(quant_ref.unpack(packed.cpu().numpy(), rows, k), q)
 
 

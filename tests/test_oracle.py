@@ -96,7 +96,7 @@ def test_sun_w4_pack_roundtrip_and_bounds():
     assert int(q.min()) >= -8 and int(q.max()) <= 7
     assert float(s[3, 1]) == 0.0 and int(q[3, 128:256].abs().max()) == 0
     packed, scales = quant_ref.pack(q, s)
-    assert packed.size == 256 * 512 // 2 and scales.shape == (4, 256)
+    assert packed.size == 256 * 512 // 2 and scales.shape == (2, 4, 128)
     assert torch.equal(quant_ref.unpack(packed, 200, 512), q)
     deq = quant_ref.dequantize(q, s).float()
     rel = ((deq - w.float()).norm() / w.float().norm()).item()
