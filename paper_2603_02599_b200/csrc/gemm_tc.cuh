@@ -99,6 +99,10 @@ struct GemmArgs {
   int sk_units;
   float* sk_part;      // [grid][bn/16][128][16] fp32
   unsigned* sk_flags;  // [grid]
+  // L2 prefetch of the next GEMM's first weight stages, issued by this kernel's
+  // producer once its own loads are out (fills HBM during the epilogue/launch gap)
+  const uint8_t* pf_w;  // next weights (SUN-BLK or SUN-W4 packed); null = off
+  int pf_w4, pf_m_tiles, pf_ksteps, pf_kb64, pf_splits, pf_grid, pf_sk_units, pf_bytes;
   // optional per-CTA %globaltimer stamps [gridDim.x][8] (profiling only)
   unsigned long long* stamps;
 };
@@ -428,6 +432,43 @@ SUN_DEVICE void load_qkv_meta(const GemmArgs& a, float* epi) {
   epi_bar();
 }
 
+// Prefetch into L2 the first pf_bytes of the weight stream of every next-GEMM
+// CTA c == blockIdx.x (mod gridDim.x), using the next launch's schedule.
+SUN_DEVICE void prefetch_next_weights(const GemmArgs& a) {
+  if (a.pf_w == nullptr) return;
+  const int KS = a.pf_ksteps;
+  for (int c = blockIdx.x; c < a.pf_grid; c += gridDim.x) {
+    long long u0, u1;
+    if (a.pf_splits > 1) {
+      const int S = a.pf_splits, t = c / S, r = c % S;
+      u0 = static_cast<long long>(t) * KS + r * KS / S;
+      u1 = static_cast<long long>(t) * KS + (r + 1) * KS / S;
+    } else if (a.pf_sk_units > 0) {
+      u0 = static_cast<long long>(c) * a.pf_sk_units / a.pf_grid;
+      u1 = static_cast<long long>(c + 1) * a.pf_sk_units / a.pf_grid;
+    } else {
+      u0 = static_cast<long long>(c) * a.pf_m_tiles / a.pf_grid * KS;
+      u1 = static_cast<long long>(c + 1) * a.pf_m_tiles / a.pf_grid * KS;
+    }
+    long long off, len;
+    if (a.pf_w4) {  // 8 KB packed per K block, contiguous along the range
+      off = u0 * kW4PackedBytes;
+      len = (u1 - u0) * kW4PackedBytes;
+    } else {  // SUN-BLK: 16 KB blocks, unit = two blocks (one for an odd tail)
+      const long long t0 = u0 / KS, t1 = (u1 - 1) / KS;
+      const long long b0 = t0 * a.pf_kb64 + 2 * (u0 % KS);
+      const long long b1 = t1 * a.pf_kb64 + min(2 * ((u1 - 1) % KS) + 2, static_cast<long long>(a.pf_kb64));
+      off = b0 * kTileWBytes;
+      len = (b1 - b0) * kTileWBytes;
+    }
+    const uint32_t bytes = static_cast<uint32_t>(min(len, static_cast<long long>(a.pf_bytes))) & ~15u;
+    if (bytes > 0)
+      asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(a.pf_w + off), "r"(bytes),
+                   "l"(kEvictLast)
+                   : "memory");
+  }
+}
+
 SUN_DEVICE unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -674,7 +715,7 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
           phase ^= 1;
         }
       }
-      if (wprod) pdl_wait();
+      if (wprod) prefetch_next_weights(a);
     }
   } else if (W4 && warp == 1) {
     // ---------------- W4 MMA issuer: A (dequantised weights) from TMEM, X from smem
@@ -757,6 +798,7 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
         issue_w(j);
         issue_x(j);
       }
+      prefetch_next_weights(a);
     }
   } else if (warp == 1 && !W4) {
     const uint32_t idesc = make_idesc_bf16(kTileM, a.bn);

@@ -400,36 +400,36 @@ int cluster_splits(const GemmPlan& p, size_t smem, bool w4, int slots) {
 }
 
 // Launch one GEMM: bf16 SUN-BLK weights (wblk) or QSUN SUN-W4 (packed, scales).
-template <int EPI>
-SunStatus run_gemm(const void* wblk, const void* packed, const void* scales, GemmArgs a, const GemmPlan& p,
-                   cudaStream_t st, bool pdl) {
-  const bool w4 = packed != nullptr;
-  a.wblk = static_cast<const uint8_t*>(wblk);
-  a.w4_packed = static_cast<const uint8_t*>(packed);
-  a.w4_scales = static_cast<const __nv_bfloat16*>(scales);
-  const int per_sm = gemm_ctas_per_sm(a.bn, w4);
+// Launch configuration of one GEMM (also used to aim the previous GEMM's L2
+// prefetch at the CTAs that will start streaming first).
+struct LaunchCfg {
+  int grid, splits, sk_units, stages, xstages, wgroup, xk;
+  size_t smem;
+};
+
+LaunchCfg launch_cfg(const GemmPlan& p, int bn, bool w4, bool have_sk) {
+  LaunchCfg c{};
+  const int per_sm = gemm_ctas_per_sm(bn, w4);
   const int slots = std::min(kNumSms * per_sm, gemm_max_grid());
-  size_t smem, ring;
+  size_t ring;
   if (w4) {
     // weight stages of wgroup K blocks (one packed + one scales request each),
     // activation stages of xk K blocks; 3 activation stages, weights fill the rest
     static const int env_wg = [] { const char* e = getenv("SUN_W4_WGROUP"); return e ? atoi(e) : 0; }();
     static const int env_xk = [] { const char* e = getenv("SUN_W4_XK"); return e ? atoi(e) : 0; }();
     static const int env_xs = [] { const char* e = getenv("SUN_W4_XSTAGES"); return e ? atoi(e) : 0; }();
-    a.wgroup = env_wg > 0 ? env_wg : 4;
-    a.xk = env_xk > 0 ? env_xk : (a.bn <= 32 ? 4 : (a.bn <= 64 ? 2 : 1));
-    a.xstages = env_xs > 0 ? env_xs : (a.bn > 128 ? 2 : 3);
-    const int budget = kSmemPerSm - 2048 - 2048 - int(kEpiSmemBytes) - 1024 -
-                       a.xstages * int(w4_xstage_bytes(a.bn, a.xk));
-    a.stages = std::max(2, std::min(16, budget / int(w4_wstage_bytes(a.wgroup))));
-    smem = gemm_smem_bytes_w4(a.bn, a.wgroup, a.stages, a.xk, a.xstages);
-    ring = size_t(a.stages) * w4_wstage_bytes(a.wgroup) + size_t(a.xstages) * w4_xstage_bytes(a.bn, a.xk);
+    c.wgroup = env_wg > 0 ? env_wg : 4;
+    c.xk = env_xk > 0 ? env_xk : (bn <= 32 ? 4 : (bn <= 64 ? 2 : 1));
+    c.xstages = env_xs > 0 ? env_xs : (bn > 128 ? 2 : 3);
+    const int budget = kSmemPerSm - 2048 - 2048 - int(kEpiSmemBytes) - 1024 - c.xstages * int(w4_xstage_bytes(bn, c.xk));
+    c.stages = std::max(2, std::min(16, budget / int(w4_wstage_bytes(c.wgroup))));
+    c.smem = gemm_smem_bytes_w4(bn, c.wgroup, c.stages, c.xk, c.xstages);
+    ring = size_t(c.stages) * w4_wstage_bytes(c.wgroup) + size_t(c.xstages) * w4_xstage_bytes(bn, c.xk);
   } else {
-    a.stages = gemm_stages(a.bn, w4, per_sm);
-    smem = gemm_smem_bytes(a.bn, a.stages, w4);
-    ring = size_t(a.stages) * gemm_stage_bytes(a.bn, w4);
+    c.stages = gemm_stages(bn, w4, per_sm);
+    c.smem = gemm_smem_bytes(bn, c.stages, w4);
+    ring = size_t(c.stages) * gemm_stage_bytes(bn, w4);
   }
-  int S, grid;
   // Stream-K where whole tiles cannot balance over the SMs (more tiles than CTA
   // slots, e.g. gate_up 224 tiles / 148 SMs = 1.51) and every owner's
   // contributor partials fit in its stage ring; cluster split-K (<= slots
@@ -438,25 +438,69 @@ SunStatus run_gemm(const void* wblk, const void* packed, const void* scales, Gem
   const int sk_grid = std::min(units, std::min(slots, kMaxGemmCtas));
   const int max_contrib = (p.ksteps + (units / sk_grid) - 1) / std::max(1, units / sk_grid) + 1;
   // (SUN_GEMM_SCHED=2 forces stream-K on every GEMM whose partials fit: tests)
-  const bool sk = gemm_sched() != 0 && a.sk_part != nullptr && a.sk_flags != nullptr &&
+  const bool sk = gemm_sched() != 0 && have_sk &&
                   (gemm_sched() == 2 || (p.m_tiles > slots && p.m_tiles % sk_grid != 0)) &&
-                  size_t(max_contrib) * a.bn * kTileM * 4 <= ring;
+                  size_t(max_contrib) * bn * kTileM * 4 <= ring;
   if (sk) {
-    S = 1;
-    a.sk_units = units;
-    grid = sk_grid;
+    c.splits = 1;
+    c.sk_units = units;
+    c.grid = sk_grid;
   } else {
-    S = cluster_splits(p, smem, w4, slots);
-    a.sk_units = 0;
-    grid = S > 1 ? p.m_tiles * S : std::min(p.m_tiles, slots);
+    c.splits = cluster_splits(p, c.smem, w4, slots);
+    c.sk_units = 0;
+    c.grid = c.splits > 1 ? p.m_tiles * c.splits : std::min(p.m_tiles, slots);
   }
-  a.splits = S;
-  g_cluster = unsigned(S);
+  return c;
+}
+
+// L2 prefetch budget per next-GEMM CTA (SUN_GEMM_PREFETCH_KB). Default off:
+// measured on C3 (8B bf16, B=64) 5.375 ms/step without, 5.347 at 64 KB, 5.47 at
+// 128 KB, 5.75 at 512 KB; C4 unchanged — the HBM is not idle enough between
+// GEMMs for a prefetch to pay, and larger ones compete with the live stream.
+int gemm_prefetch_bytes() {
+  static int v = [] {
+    const char* e = getenv("SUN_GEMM_PREFETCH_KB");
+    return (e ? atoi(e) : 0) * 1024;
+  }();
+  return v;
+}
+
+// Aim this GEMM's tail-time L2 prefetch at the first weight stages of `next`.
+void set_prefetch(GemmArgs& a, const void* next_w, const GemmPlan& np, int bn, bool w4) {
+  const int bytes = gemm_prefetch_bytes();
+  if (!next_w || bytes <= 0) return;
+  const LaunchCfg c = launch_cfg(np, bn, w4, a.sk_part != nullptr && a.sk_flags != nullptr);
+  a.pf_w = static_cast<const uint8_t*>(next_w);
+  a.pf_w4 = w4 ? 1 : 0;
+  a.pf_m_tiles = np.m_tiles;
+  a.pf_ksteps = np.ksteps;
+  a.pf_kb64 = np.kb64;
+  a.pf_splits = c.splits;
+  a.pf_grid = c.grid;
+  a.pf_sk_units = c.sk_units;
+  a.pf_bytes = bytes;
+}
+
+template <int EPI>
+SunStatus run_gemm(const void* wblk, const void* packed, const void* scales, GemmArgs a, const GemmPlan& p,
+                   cudaStream_t st, bool pdl) {
+  const bool w4 = packed != nullptr;
+  a.wblk = static_cast<const uint8_t*>(wblk);
+  a.w4_packed = static_cast<const uint8_t*>(packed);
+  a.w4_scales = static_cast<const __nv_bfloat16*>(scales);
+  const LaunchCfg c = launch_cfg(p, a.bn, w4, a.sk_part != nullptr && a.sk_flags != nullptr);
+  a.stages = c.stages;
+  a.xstages = c.xstages;
+  a.wgroup = c.wgroup;
+  a.xk = c.xk;
+  a.splits = c.splits;
+  a.sk_units = c.sk_units;
+  g_cluster = unsigned(c.splits);
   if (w4) {
     if constexpr (EPI == EPI_LOGITS) return fail(SUN_ERR_UNSUPPORTED, "lm_head is bf16");
-    else SUN_CUDA(launch(gemm_kernel<EPI, true>, dim3(grid), dim3(kW4Threads), smem, st, pdl, a));
+    else SUN_CUDA(launch(gemm_kernel<EPI, true>, dim3(c.grid), dim3(kW4Threads), c.smem, st, pdl, a));
   } else {
-    SUN_CUDA(launch(gemm_kernel<EPI, false>, dim3(grid), dim3(kGemmThreads), smem, st, pdl, a));
+    SUN_CUDA(launch(gemm_kernel<EPI, false>, dim3(c.grid), dim3(kGemmThreads), c.smem, st, pdl, a));
   }
   return SUN_OK;
 }
@@ -661,6 +705,7 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     a.n_kv_heads = d.n_kv_heads;
     a.head_dim = d.head_dim;
     a.page_size = d.page_size;
+    set_prefetch(a, w4 ? lw.w_o : lw.w_o, dec->p_o, bn, w4);  // O-proj weights, through the attention kernel
     s = w4 ? run_gemm<EPI_QKV_ROPE>(nullptr, lw.w_qkv, lw.s_qkv, a, dec->p_qkv, st, pdl)
            : run_gemm<EPI_QKV_ROPE>(lw.w_qkv, nullptr, nullptr, a, dec->p_qkv, st, pdl);
     if (s != SUN_OK) return s;
@@ -672,6 +717,7 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     a.out_f32 = dec->resid;
     a.ldo = d.hidden;
     produce_norm(a, lw.ffn_norm);
+    set_prefetch(a, lw.w_gate_up, dec->p_gu, bn, w4);
     s = w4 ? run_gemm<EPI_RESID_ADD>(nullptr, lw.w_o, lw.s_o, a, dec->p_o, st, pdl)
            : run_gemm<EPI_RESID_ADD>(lw.w_o, nullptr, nullptr, a, dec->p_o, st, pdl);
     if (s != SUN_OK) return s;
@@ -681,6 +727,7 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     a.out_bf16 = dec->act;
     a.ldb = d.ffn;
     a.n_valid_out = d.ffn;
+    set_prefetch(a, lw.w_down, dec->p_down, bn, w4);
     s = w4 ? run_gemm<EPI_SWIGLU>(nullptr, lw.w_gate_up, lw.s_gate_up, a, dec->p_gu, st, pdl)
            : run_gemm<EPI_SWIGLU>(lw.w_gate_up, nullptr, nullptr, a, dec->p_gu, st, pdl);
     if (s != SUN_OK) return s;
@@ -689,6 +736,8 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     a.out_f32 = dec->resid;
     a.ldo = d.hidden;
     produce_norm(a, l + 1 < d.n_layers ? dec->layers[l + 1].attn_norm : dec->w.final_norm);
+    if (l + 1 < d.n_layers) set_prefetch(a, dec->layers[l + 1].w_qkv, dec->p_qkv, bn, w4);
+    else set_prefetch(a, dec->w.lm_head, dec->p_lm, bn, false);
     s = w4 ? run_gemm<EPI_RESID_ADD>(nullptr, lw.w_down, lw.s_down, a, dec->p_down, st, pdl)
            : run_gemm<EPI_RESID_ADD>(lw.w_down, nullptr, nullptr, a, dec->p_down, st, pdl);
     if (s != SUN_OK) return s;
