@@ -10,7 +10,7 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/b
 if [ "$1" == "ncu" ]; then
   for cfg in c3 c4; do
     # one decode step = 195 launches (embed + 32 x 6 + lm_head + argmax): skip the first step, capture the second
-    timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 195 -c 195 --csv --log-file gpurun_out/launches_$cfg.csv python scripts/profile_step.py --config $cfg --steps 2 > gpurun_out/ncu1_$cfg.log 2>&1
+    timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"gemm_kernel|attn_|embed_norm|argmax" -s 195 -c 195 --csv --log-file gpurun_out/launches_$cfg.csv python scripts/profile_step.py --config $cfg --steps 2 > gpurun_out/ncu1_$cfg.log 2>&1
     # one layer (layer 2): QKV, attention, O, gate_up, down
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gemm_kernel|attn_decode" -s 10 -c 5 -o gpurun_out/full_$cfg python scripts/profile_step.py --config $cfg --steps 1 > gpurun_out/ncu2_$cfg.log 2>&1
   done
