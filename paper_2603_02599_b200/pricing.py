@@ -7,8 +7,11 @@ boundary of the shared decode path; ``DecodeBackend`` names it:
 
 * ``AnalyticBackend`` — the reference formula (same signatures, same
   ``MixedDecoderError`` / ``ValueError`` behaviour);
-* ``paper_2603_02599_b200.scheduler.B200Backend`` — runs the real step on a B200
-  and returns its measured duration.
+* ``MeasuredBackend`` — the B200's measured step time over a (batch, context)
+  grid (scripts/measure_step_grid.py, tests/golden/b200_steps_*.json), so the
+  simulator predicts the new system (harness closure, SURVEY.md §8(f)4);
+* ``calibrate_decode`` — the decode half of the reference's ``calibrate``
+  (costmodel.py:257-358) refit to B200-measured concurrency-1 TPOT.
 
 ``step_bytes`` is the algorithmic-bytes model used for every roofline number
 this package reports.
@@ -18,7 +21,12 @@ from __future__ import annotations
 from dataclasses import asdict, dataclass
 from typing import Iterable, Protocol
 
-from .errors import MixedDecoderError
+import bisect
+import json
+
+import numpy as np
+
+from .errors import CalibrationInfeasible, MixedDecoderError
 from .spec import DecoderSpec
 from .sun_types import GpuSpec, KvHandle, ModelProfile, WorkerRole
 
@@ -117,9 +125,10 @@ def step_bytes(spec: DecoderSpec, contexts: Iterable[int]) -> int:
 
 
 class DecodeBackend(Protocol):
-    """What a decode worker calls once per step (engine.py:427-429)."""
+    """What a decode worker calls once per step (engine.py:427-429). ``batch``
+    (the post-admission batch size) is extra information a backend may use."""
 
-    def step_time(self, total_kv_bytes: float, decoder_weight_bytes: float) -> float: ...
+    def step_time(self, total_kv_bytes: float, decoder_weight_bytes: float, batch: int | None = None) -> float: ...
 
 
 class AnalyticBackend:
@@ -128,5 +137,96 @@ class AnalyticBackend:
     def __init__(self, params: CostParams, gpu: GpuSpec):
         self.params, self.gpu = params, gpu
 
-    def step_time(self, total_kv_bytes: float, decoder_weight_bytes: float) -> float:
+    def step_time(self, total_kv_bytes: float, decoder_weight_bytes: float, batch: int | None = None) -> float:
         return decode_step_time_from_totals(total_kv_bytes, decoder_weight_bytes, self.params, self.gpu)
+
+
+# --------------------------------------------------------------------------- harness closure
+@dataclass(frozen=True)
+class StepPoint:
+    """One measured B200 decode step: `batch` members, each with `context`
+    resident tokens before the step, took `step_s` seconds."""
+
+    batch: int
+    context: int
+    step_s: float
+
+
+def load_step_points(path: str) -> tuple[dict, list[StepPoint]]:
+    """tests/golden/b200_steps_*.json (scripts/measure_step_grid.py) -> (header, points)."""
+    with open(path) as f:
+        data = json.load(f)
+    pts = [StepPoint(int(p["batch"]), int(p["context"]), float(p["step_s"])) for p in data["points"]]
+    return {k: v for k, v in data.items() if k != "points"}, pts
+
+
+def calibrate_decode(points: list[StepPoint], decoder_weight_bytes: float, kv_bytes_per_token: float, gpu: GpuSpec,
+                     rel_tol: float = 0.03) -> tuple[float, float, list[tuple[str, float]]]:
+    """Decode half of the reference's ``calibrate`` (costmodel.py:306-317, 335-358):
+    least squares of tpot = D + beta * (W + resident KV bytes) over the targets,
+    mbu = 1 / (beta * BW). Returns (decode_fixed_overhead, mbu, residuals);
+    raises ``CalibrationInfeasible`` like the reference (too few targets, beta <= 0,
+    mbu > 1, or a target missed by more than rel_tol). The reference fits
+    concurrency-1 targets; points here are whole decode steps at any batch."""
+    if len(points) < 2:
+        raise CalibrationInfeasible("need at least 2 decode targets")
+    a = np.zeros((len(points), 2))
+    y = np.zeros(len(points))
+    for i, p in enumerate(points):
+        a[i] = (1.0, decoder_weight_bytes + p.batch * p.context * kv_bytes_per_token)
+        y[i] = p.step_s
+    (d, beta), *_ = np.linalg.lstsq(a, y, rcond=None)
+    if beta <= 0:
+        raise CalibrationInfeasible("targets imply non-positive seconds per byte")
+    mbu = 1.0 / (beta * gpu.hbm_bandwidth)
+    if mbu > 1.0:
+        raise CalibrationInfeasible(f"decode targets imply {1.0 / beta:.3e} B/s effective bandwidth, above "
+                                    f"the GPU peak {gpu.hbm_bandwidth:.3e} B/s")
+    res = []
+    for p in points:
+        pred = d + beta * (decoder_weight_bytes + p.batch * p.context * kv_bytes_per_token)
+        res.append((f"B{p.batch}@ctx{p.context}.tpot", (pred - p.step_s) / p.step_s))
+    worst = max(abs(e) for _, e in res)
+    if worst > rel_tol:
+        raise CalibrationInfeasible(f"best fit misses tolerance {rel_tol:.1%} (worst {worst:.2%})",
+                                    residuals=sorted(res, key=lambda r: -abs(r[1])))
+    return float(d), float(mbu), res
+
+
+class MeasuredBackend:
+    """Decode-step price from the B200's own measurements: bilinear in (batch,
+    mean resident context) over a measured grid, linear extrapolation in context
+    beyond it (KV bytes are linear in context), clamped to the batch range.
+    Drop-in for ``AnalyticBackend`` at engine.py:427 when the post-admission
+    batch size is passed."""
+
+    def __init__(self, points: list[StepPoint], kv_bytes_per_token: float):
+        if not points:
+            raise ValueError("MeasuredBackend needs at least one measured point")
+        self.kvb = float(kv_bytes_per_token)
+        self.batches = sorted({p.batch for p in points})
+        self.contexts = sorted({p.context for p in points})
+        grid = {(p.batch, p.context): p.step_s for p in points}
+        missing = [(b, c) for b in self.batches for c in self.contexts if (b, c) not in grid]
+        if missing:
+            raise ValueError(f"measured grid incomplete, missing {missing[:4]}")
+        self.t = np.array([[grid[(b, c)] for c in self.contexts] for b in self.batches])
+
+    @staticmethod
+    def _bracket(xs: list[int], x: float) -> tuple[int, int, float]:
+        if len(xs) == 1:
+            return 0, 0, 0.0
+        i = min(max(bisect.bisect_right(xs, x) - 1, 0), len(xs) - 2)
+        return i, i + 1, (x - xs[i]) / (xs[i + 1] - xs[i])
+
+    def predict(self, batch: int, context: float) -> float:
+        b = min(max(float(batch), self.batches[0]), self.batches[-1])
+        i0, i1, fb = self._bracket(self.batches, b)
+        j0, j1, fc = self._bracket(self.contexts, float(context))  # fc may fall outside [0, 1]: extrapolate
+        row = lambda i: self.t[i, j0] + fc * (self.t[i, j1] - self.t[i, j0])  # noqa: E731
+        return float(max(row(i0) + fb * (row(i1) - row(i0)), 0.0))
+
+    def step_time(self, total_kv_bytes: float, decoder_weight_bytes: float, batch: int | None = None) -> float:
+        if not batch:
+            raise ValueError("MeasuredBackend needs the batch size")
+        return self.predict(batch, total_kv_bytes / (batch * self.kvb))
