@@ -290,7 +290,7 @@ def gpu_arm(args, cfg):
 
     graph = not args.no_graph
     for _ in range(args.warmup):
-        dec.step_static(B, 0, graph=graph, feedback=True)
+        dec.step_static(B, args.pps, graph=graph, feedback=True)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -302,7 +302,7 @@ def gpu_arm(args, cfg):
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     evs[0].record()
     for i in range(args.steps):
-        dec.step_static(B, 0, graph=graph, feedback=True)
+        dec.step_static(B, args.pps, graph=graph, feedback=True)
         evs[i + 1].record()
     torch.cuda.synchronize()
     if world > 1:
@@ -323,13 +323,15 @@ def gpu_arm(args, cfg):
 
     # launches inside the timed region: graph replays do not pass through the
     # library's host launch counter, so count the kernels of one captured step
-    per_step_launches = len(dec.kernel_names())
+    prof = dec.profile(dec.tokens, dec.positions, dec.block_tables, B, dec.next_tokens, None, args.pps)
+    names = dec.kernel_names()
+    if len(names) != len(prof):  # unsplit attention: no combine launches
+        names = dec.kernel_names(combine=False)
+    per_step_launches = len(names)
     gpu_launches = per_step_launches * args.steps
 
     # ---- per-kernel attribution (serialised, events after every launch) ----
     pos_now = [c + args.warmup + args.steps for c in ctx]
-    prof = dec.profile(dec.tokens, dec.positions, dec.block_tables, B, dec.next_tokens, None, 0)
-    names = dec.kernel_names()
     by = {}
     for n_, ms in zip(names, prof):
         t = by.setdefault(n_, [0.0, 0])
@@ -360,7 +362,7 @@ def gpu_arm(args, cfg):
         h_pos = pin(torch.tensor(pos_now, dtype=torch.int32))
         out = pin(torch.zeros(B, dtype=torch.int32))
         for i in range(2):  # warm the non-feedback graph
-            dec.decode(h_tok, h_pos, h_bt, graph=graph)
+            dec.decode(h_tok, h_pos, h_bt, pages_per_split=args.pps, graph=graph)
             out.copy_(dec.next_tokens[:B])
             h_pos += 1
         torch.cuda.synchronize()
@@ -368,7 +370,7 @@ def gpu_arm(args, cfg):
             dist.barrier()
         te = time.perf_counter()
         for i in range(args.steps):
-            nt = dec.decode(h_tok, h_pos, h_bt, graph=graph)
+            nt = dec.decode(h_tok, h_pos, h_bt, pages_per_split=args.pps, graph=graph)
             out.copy_(nt)  # D2H read of the step's result (synchronises)
             h_tok.copy_(out)
             h_pos += 1
@@ -429,6 +431,7 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="sun", choices=["sun", "reference"])
     ap.add_argument("--routing", default="lot", choices=["lot", "pinned"])
+    ap.add_argument("--pps", type=int, default=0, help="attention pages per split (0 = auto)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-pdl", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(128)
     }
   }
   __syncthreads();
-  const int n_splits = a.fused_combine ? (n_pages + a.pages_per_split - 1) / a.pages_per_split : 0;
+  const int n_splits = (n_pages + a.pages_per_split - 1) / a.pages_per_split;
   for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
     const int gg = idx / D;
     const int dim = idx % D;
@@ -304,6 +304,7 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(const AttnArgs a) {
   const int ctx = a.positions[b] + 1;
   const int n_pages = (ctx + kPageTokens - 1) / kPageTokens;
   const int n_splits = (n_pages + a.pages_per_split - 1) / a.pages_per_split;
+  if (n_splits == 1) return;  // the attention kernel emitted this sequence's output directly
   const long long u0 = (static_cast<long long>(b) * a.n_q_heads + head) * a.max_splits;
   float mm = -INFINITY;
   for (int s = 0; s < n_splits; ++s) mm = fmaxf(mm, a.part_ml[(u0 + s) * 2]);

@@ -84,11 +84,13 @@ class _StepRunner:
             ctypes.byref(n)), "sun_decode_step_profile")
         return [buf[i] for i in range(min(n.value, cap))]
 
-    def kernel_names(self) -> list[str]:
-        """Launch order of one step (matches sun_decode_step)."""
+    def kernel_names(self, combine: bool | None = None) -> list[str]:
+        """Launch order of one step (matches sun_decode_step). The split combine
+        is launched unless fused or the attention ran unsplit (combine=False)."""
+        combine = (not self.fused_combine) if combine is None else combine
         names = ["embed_norm"]
         for _ in range(self.spec.n_layers):
-            names += ["gemm_qkv_rope_kv", "attention"] + ([] if self.fused_combine else ["attn_combine"]) + [
+            names += ["gemm_qkv_rope_kv", "attention"] + (["attn_combine"] if combine else []) + [
                 "gemm_o_resid_norm", "gemm_gate_up_swiglu", "gemm_down_resid_norm"]
         return names + ["gemm_lm_head_argmax", "argmax"]
 
