@@ -37,6 +37,8 @@ struct AttnArgs {
   int act_rows;            // > 0: write `out` in SUN-ACT (the O-projection operand)
   unsigned* counters;      // [B][n_kv_heads] split arrival counters (zeroed once, self-resetting)
   int fused_combine;       // 1: last split merges in-kernel; 0: attn_combine_kernel does it
+  unsigned long long* tl;  // step timeline (profiling only)
+  int tl_idx;
 };
 
 template <int D>
@@ -72,12 +74,16 @@ __global__ void __launch_bounds__(128)
   const int split = blockIdx.x;
   const int kvh = blockIdx.y;
   const int b = blockIdx.z;
+  tl_begin(a.tl, a.tl_idx);
   pdl_wait();
   pdl_launch_dependents();  // early: the next kernel may start its prologue / weight prefetch
   const int ctx = a.positions[b] + 1;
   const int n_pages = (ctx + kPageTokens - 1) / kPageTokens;
   const int p0 = split * a.pages_per_split;
-  if (p0 >= n_pages) return;
+  if (p0 >= n_pages) {
+    tl_end(a.tl, a.tl_idx);
+    return;
+  }
   const int p1 = min(n_pages, p0 + a.pages_per_split);
 
   extern __shared__ uint8_t smem_raw[];
@@ -291,6 +297,7 @@ __global__ void __launch_bounds__(128)
       }
     }
   }
+  tl_end(a.tl, a.tl_idx);
 }
 
 // Merge the split partials of one (sequence, query head) and emit the bf16

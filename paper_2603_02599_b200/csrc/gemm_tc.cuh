@@ -52,7 +52,9 @@ struct GemmArgs {
   int kb64;          // ceil(k / 64): 64-wide k blocks per tile
   int ksteps;        // ceil(kb64 / 2): 128-wide pipeline stages per tile
   int m_tiles;       // ceil(n_out / 128)
-  int splits;        // cluster split-K factor S (> 1: cluster schedule)
+  int splits;        // split-K factor S (> 1: S CTAs per tile)
+  int vcluster;      // 1: the S CTAs of a tile are not a hardware cluster: partials and the
+                     // rank-sliced reduction go through L2 (sk_part) with a per-tile counter
   int stages;        // smem pipeline depth (W4: weight stages of wgroup K blocks)
   int xstages;       // W4: activation stages of xk K blocks
   int wgroup;        // W4: K blocks per weight stage (packed [wgroup][8 KB] | scales [wgroup][256 B])
@@ -105,6 +107,8 @@ struct GemmArgs {
   int pf_w4, pf_m_tiles, pf_ksteps, pf_kb64, pf_splits, pf_grid, pf_sk_units, pf_bytes;
   // optional per-CTA %globaltimer stamps [gridDim.x][8] (profiling only)
   unsigned long long* stamps;
+  unsigned long long* tl;  // step timeline slot array (profiling only) and this launch's index
+  int tl_idx;
 };
 
 SUN_DEVICE unsigned long long gtimer() {
@@ -424,8 +428,19 @@ SUN_DEVICE void load_qkv_meta(const GemmArgs& a, float* epi) {
   if (a.ss_in != nullptr) {
     float* rb = reinterpret_cast<float*>(meta + 512);
     for (int b = threadIdx.x - 64; b < a.bn; b += 128) {
+      // issue 16 independent loads per round trip, then add in tile order (the
+      // sum is unchanged; a load-add-load chain cost one L2 round trip per tile,
+      // ~10 us for 32 tiles — longer than the whole QKV main loop)
       float t = 0.f;
-      for (int i = 0; i < a.ss_tiles; ++i) t += a.ss_in[static_cast<long long>(i) * a.bn + b];
+      for (int i0 = 0; i0 < a.ss_tiles; i0 += 16) {
+        float x[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          x[i] = (i0 + i < a.ss_tiles) ? a.ss_in[static_cast<long long>(i0 + i) * a.bn + b] : 0.f;
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (i0 + i < a.ss_tiles) t += x[i];
+      }
       rb[b] = rsqrtf(t / static_cast<float>(a.norm_h) + a.norm_eps);
     }
   }
@@ -596,6 +611,7 @@ template <int EPI, bool W4>
 __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel(const GemmArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  tl_begin(a.tl, a.tl_idx);
   const int stages = a.stages;
   const uint32_t sb = W4 ? w4_wstage_bytes(a.wgroup) : gemm_stage_bytes(a.bn, W4);
   const uint32_t xoff = 2u * kTileWBytes;  // bf16: X offset inside a stage
@@ -618,8 +634,9 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
 
   const int warp = warp_id_sync();
   const uint32_t S = a.splits > 1 ? static_cast<uint32_t>(a.splits) : 1u;
-  const bool clustered = S > 1;
-  const uint32_t rank = clustered ? cluster_ctarank() : 0u;
+  const bool clustered = S > 1;  // split-K over S CTAs (hardware cluster or virtual)
+  const bool vcl = clustered && a.vcluster;
+  const uint32_t rank = clustered ? (vcl ? blockIdx.x % S : cluster_ctarank()) : 0u;
   // this CTA's work: the contiguous range [u0, u1) of work units u = tile * ksteps + ks
   const int KS = a.ksteps;
   int u0, u1;
@@ -856,18 +873,21 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
         epi_bar();
         if (threadIdx.x == 64) mbar_arrive(&tempty[buf]);
       } else {
-        // park the partial in (now idle) shared memory, chunk-major
-        // [bn/16][128 rows][16] fp32: a warp's DSMEM reads of one chunk are then
-        // 2 KB contiguous (row-major rows 272 B apart made them 16-byte gathers)
-        float* part = reinterpret_cast<float*>(smem);
+        // park the partial (part_index layout) in the now idle shared memory
+        // (hardware cluster: peers read it over DSMEM) or in L2 (virtual cluster)
+        float* part = vcl ? a.sk_part + static_cast<long long>(blockIdx.x) * a.bn * kTileM
+                          : reinterpret_cast<float*>(smem);
         float v[16];
         for (int c0 = 0; c0 < a.bn; c0 += 16) {
           tmem_ld16(taddr + c0, v);
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            *reinterpret_cast<float4*>(part + part_index(c0, j, row_local)) =
-                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          for (int j = 0; j < 4; ++j) {
+            const float4 f = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            if (vcl) __stcg(reinterpret_cast<float4*>(part + part_index(c0, j, row_local)), f);
+            else *reinterpret_cast<float4*>(part + part_index(c0, j, row_local)) = f;
+          }
         }
+        if (vcl) __threadfence();
       }
     }
   } else if (W4 && warp < 6 + kW4ConvThreads / 32) {
@@ -911,12 +931,24 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
 
   if (clustered) {
     if (threadIdx.x == 64) SUN_STAMP(8);
-    cluster_sync_all();  // every rank's partial is visible cluster-wide
+    unsigned* tile_cnt = vcl ? a.sk_flags + blockIdx.x / S : nullptr;
+    if (vcl) {  // every rank's partial is in L2: count arrivals of the tile's S CTAs
+      __syncthreads();
+      if (threadIdx.x == 64) {
+        atomicAdd(tile_cnt, 1u);
+        while (ld_acquire_u32(tile_cnt) < S) {
+        }
+      }
+      __syncthreads();
+    } else {
+      cluster_sync_all();  // every rank's partial is visible cluster-wide
+    }
     if (threadIdx.x == 64) SUN_STAMP(9);
     if (warp >= 2 && warp < 6) {
       const int q = warp & 3;
       const int row_local = q * 32 + (threadIdx.x & 31);
       float* part = reinterpret_cast<float*>(smem);
+      const float* gpart = vcl ? a.sk_part + static_cast<long long>(blockIdx.x - rank) * a.bn * kTileM : nullptr;
       float* red_val = epi + 16 * kTileM;
       int* red_idx = reinterpret_cast<int*>(red_val + 64);
       for (int c0 = static_cast<int>(rank) * 16; c0 < a.bn; c0 += static_cast<int>(S) * 16) {
@@ -929,8 +961,10 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
           for (int u = 0; u < 4; ++u)
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-              x[u][j] = (r0 + u < S) ? ld_dsmem_f4(dsmem_addr(part + part_index(c0, j, row_local), r0 + u))
-                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+              x[u][j] = (r0 + u >= S) ? make_float4(0.f, 0.f, 0.f, 0.f)
+                        : vcl ? __ldcg(reinterpret_cast<const float4*>(gpart + static_cast<long long>(r0 + u) * a.bn * kTileM +
+                                                                      part_index(c0, j, row_local)))
+                              : ld_dsmem_f4(dsmem_addr(part + part_index(c0, j, row_local), r0 + u));
 #pragma unroll
           for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -946,7 +980,12 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
         if (threadIdx.x == 64) SUN_STAMP(11);
       }
     }
-    cluster_sync_all();  // nobody exits while a peer may still read its partial
+    if (vcl) {  // the last of the tile's 2S arrivals rearms the counter for the next launch
+      __syncthreads();
+      if (threadIdx.x == 64 && atomicAdd(tile_cnt, 1u) == 2 * S - 1) *tile_cnt = 0u;
+    } else {
+      cluster_sync_all();  // nobody exits while a peer may still read its partial
+    }
   }
   if (threadIdx.x == 64) SUN_STAMP(5);
   tc_fence_before();
@@ -956,6 +995,7 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
     tmem_dealloc(tmem_base, ncols);
   }
   if (threadIdx.x == 0) SUN_STAMP(6);
+  tl_end(a.tl, a.tl_idx);
 }
 
 // Offline quantiser (one thread per (row, group)); produces the tile-contiguous

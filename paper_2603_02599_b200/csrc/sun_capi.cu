@@ -249,6 +249,20 @@ struct LaunchTrace {
 };
 thread_local LaunchTrace g_trace;
 
+// Step timeline (sun_decode_step_timeline): device slot array + next launch index.
+struct TimelineState {
+  unsigned long long* tl = nullptr;
+  int next = 0, capacity = 0;
+};
+thread_local TimelineState g_tl;
+template <typename A>
+void tl_assign(A& a) {
+  if (g_tl.tl != nullptr && g_tl.next < g_tl.capacity) {
+    a.tl = g_tl.tl;
+    a.tl_idx = g_tl.next++;
+  }
+}
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
                    Args&&... args) {
@@ -403,9 +417,21 @@ int cluster_splits(const GemmPlan& p, size_t smem, bool w4, int slots) {
 // Launch configuration of one GEMM (also used to aim the previous GEMM's L2
 // prefetch at the CTAs that will start streaming first).
 struct LaunchCfg {
-  int grid, splits, sk_units, stages, xstages, wgroup, xk;
+  int grid, splits, vcluster, sk_units, stages, xstages, wgroup, xk;
   size_t smem;
 };
+
+// Virtual clusters (SUN_GEMM_VCLUSTER, default on): when the hardware cannot
+// co-schedule enough S-CTA clusters (QKV: 48 tiles want S = 3 -> 144 CTAs, but
+// 3-CTA clusters do not pack the GPCs), split K over S plain CTAs that reduce
+// through L2 instead of DSMEM.
+int gemm_vcluster() {
+  static int v = [] {
+    const char* e = getenv("SUN_GEMM_VCLUSTER");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
 
 LaunchCfg launch_cfg(const GemmPlan& p, int bn, bool w4, bool have_sk) {
   LaunchCfg c{};
@@ -448,6 +474,14 @@ LaunchCfg launch_cfg(const GemmPlan& p, int bn, bool w4, bool have_sk) {
   } else {
     c.splits = cluster_splits(p, c.smem, w4, slots);
     c.sk_units = 0;
+    c.vcluster = 0;
+    const int want = p.m_tiles <= slots ? std::min(std::min(8, slots / std::max(1, p.m_tiles)), p.ksteps) : 1;
+    // (SUN_GEMM_VCLUSTER=2 uses virtual clusters wherever a split pays: tests)
+    if (gemm_vcluster() && have_sk && (want > c.splits || (gemm_vcluster() == 2 && want > 1)) &&
+        p.m_tiles * want <= kMaxGemmCtas) {
+      c.splits = want;
+      c.vcluster = 1;
+    }
     c.grid = c.splits > 1 ? p.m_tiles * c.splits : std::min(p.m_tiles, slots);
   }
   return c;
@@ -493,9 +527,11 @@ SunStatus run_gemm(const void* wblk, const void* packed, const void* scales, Gem
   a.xstages = c.xstages;
   a.wgroup = c.wgroup;
   a.xk = c.xk;
+  tl_assign(a);
   a.splits = c.splits;
+  a.vcluster = c.vcluster;
   a.sk_units = c.sk_units;
-  g_cluster = unsigned(c.splits);
+  g_cluster = c.vcluster ? 1u : unsigned(c.splits);
   if (w4) {
     if constexpr (EPI == EPI_LOGITS) return fail(SUN_ERR_UNSUPPORTED, "lm_head is bf16");
     else SUN_CUDA(launch(gemm_kernel<EPI, true>, dim3(c.grid), dim3(kW4Threads), c.smem, st, pdl, a));
@@ -534,8 +570,9 @@ int auto_pages_per_split(const SunDecoderDims& d, int batch) {
   return int(pps);
 }
 
-SunStatus run_attention(const SunDecoderDims& d, const CUtensorMap& tm_kv, const AttnArgs& aa, int batch,
+SunStatus run_attention(const SunDecoderDims& d, const CUtensorMap& tm_kv, AttnArgs aa, int batch,
                         cudaStream_t st, bool pdl) {
+  tl_assign(aa);
   dim3 grid(aa.max_splits, d.n_kv_heads, batch);
   if (d.head_dim == 128) {
     SUN_CUDA(launch(attn_decode_kernel<128>, grid, dim3(128), AttnCfg<128>::kSmem, st, pdl, tm_kv, aa));
@@ -648,6 +685,10 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
   const int pps = pages_per_split > 0 ? std::min(pages_per_split, max_pages) : auto_pages_per_split(d, batch);
   float* lg = logits ? logits : dec->logits;
   const bool w4 = d.weight_bits == 4;
+  // Timing experiments only (SUN_SKIP_KERNELS bitmask: 1 QKV, 2 attention, 8 O, 16
+  // gate_up, 32 down): leave a kernel class out of the step to read its effective
+  // cost inside the PDL-overlapped graph. Results are then meaningless.
+  static const int skip = [] { const char* e = getenv("SUN_SKIP_KERNELS"); return e ? atoi(e) : 0; }();
 
   AttnArgs aa;
   memset(&aa, 0, sizeof(aa));
@@ -709,19 +750,19 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     a.head_dim = d.head_dim;
     a.page_size = d.page_size;
     set_prefetch(a, w4 ? lw.w_o : lw.w_o, dec->p_o, bn, w4);  // O-proj weights, through the attention kernel
-    s = w4 ? run_gemm<EPI_QKV_ROPE>(nullptr, lw.w_qkv, lw.s_qkv, a, dec->p_qkv, st, pdl)
+    if (!(skip & 1)) s = w4 ? run_gemm<EPI_QKV_ROPE>(nullptr, lw.w_qkv, lw.s_qkv, a, dec->p_qkv, st, pdl)
            : run_gemm<EPI_QKV_ROPE>(lw.w_qkv, nullptr, nullptr, a, dec->p_qkv, st, pdl);
     if (s != SUN_OK) return s;
     // paged attention
     aa.layer = l;
-    if ((s = run_attention(d, dec->tm_kv, aa, batch, st, pdl)) != SUN_OK) return s;
+    if (!(skip & 2) && (s = run_attention(d, dec->tm_kv, aa, batch, st, pdl)) != SUN_OK) return s;
     // O projection + residual; emits the FFN norm's operand
     a = base_args(dec->p_o, d.hidden, qd, batch, bn, dec->attn, dec->sk_part, dec->sk_flags);
     a.out_f32 = dec->resid;
     a.ldo = d.hidden;
     produce_norm(a, lw.ffn_norm);
     set_prefetch(a, lw.w_gate_up, dec->p_gu, bn, w4);
-    s = w4 ? run_gemm<EPI_RESID_ADD>(nullptr, lw.w_o, lw.s_o, a, dec->p_o, st, pdl)
+    if (!(skip & 8)) s = w4 ? run_gemm<EPI_RESID_ADD>(nullptr, lw.w_o, lw.s_o, a, dec->p_o, st, pdl)
            : run_gemm<EPI_RESID_ADD>(lw.w_o, nullptr, nullptr, a, dec->p_o, st, pdl);
     if (s != SUN_OK) return s;
     // gate/up (* r_b) + SwiGLU
@@ -731,7 +772,7 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     a.ldb = d.ffn;
     a.n_valid_out = d.ffn;
     set_prefetch(a, lw.w_down, dec->p_down, bn, w4);
-    s = w4 ? run_gemm<EPI_SWIGLU>(nullptr, lw.w_gate_up, lw.s_gate_up, a, dec->p_gu, st, pdl)
+    if (!(skip & 16)) s = w4 ? run_gemm<EPI_SWIGLU>(nullptr, lw.w_gate_up, lw.s_gate_up, a, dec->p_gu, st, pdl)
            : run_gemm<EPI_SWIGLU>(lw.w_gate_up, nullptr, nullptr, a, dec->p_gu, st, pdl);
     if (s != SUN_OK) return s;
     // down + residual; emits the next attention norm's (or the final norm's) operand
@@ -741,7 +782,7 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     produce_norm(a, l + 1 < d.n_layers ? dec->layers[l + 1].attn_norm : dec->w.final_norm);
     if (l + 1 < d.n_layers) set_prefetch(a, dec->layers[l + 1].w_qkv, dec->p_qkv, bn, w4);
     else set_prefetch(a, dec->w.lm_head, dec->p_lm, bn, false);
-    s = w4 ? run_gemm<EPI_RESID_ADD>(nullptr, lw.w_down, lw.s_down, a, dec->p_down, st, pdl)
+    if (!(skip & 32)) s = w4 ? run_gemm<EPI_RESID_ADD>(nullptr, lw.w_down, lw.s_down, a, dec->p_down, st, pdl)
            : run_gemm<EPI_RESID_ADD>(lw.w_down, nullptr, nullptr, a, dec->p_down, st, pdl);
     if (s != SUN_OK) return s;
   }
@@ -795,6 +836,21 @@ SunStatus sun_decode_step_profile(SunDecoder* dec, const int32_t* tokens, const 
   cudaEventDestroy(start);
   for (auto e : evs) cudaEventDestroy(e);
   return SUN_OK;
+}
+
+SunStatus sun_decode_step_timeline(SunDecoder* dec, const int32_t* tokens, const int32_t* positions,
+                                   const int32_t* block_tables, int32_t bt_stride, int32_t batch,
+                                   int32_t pages_per_split, int32_t* next_tokens, void* stream, uint64_t* timeline,
+                                   int32_t capacity, int32_t* n_launches) {
+  if (!dec || !timeline || !n_launches || capacity < 1) return fail(SUN_ERR_VALUE, "null argument");
+  g_tl.tl = reinterpret_cast<unsigned long long*>(timeline);
+  g_tl.next = 0;
+  g_tl.capacity = capacity;
+  SunStatus s = sun_decode_step(dec, tokens, positions, block_tables, bt_stride, batch, pages_per_split, nullptr,
+                                next_tokens, 0, stream);
+  *n_launches = g_tl.next;
+  g_tl = TimelineState{};
+  return s;
 }
 
 SunStatus sun_gemm_workspace_bytes(int64_t n_out, int64_t k, int32_t batch, size_t* bytes) {

@@ -134,6 +134,23 @@ SUN_DEVICE void bulk_load_hint(void* smem_dst, const void* gsrc, uint32_t bytes,
 }
 
 // ----------------------------------------------------------------------------
+// Step timeline (profiling only): per instrumented launch, the earliest CTA
+// start and the latest CTA end in %globaltimer ns (tl[2 i] = min start, tl[2 i + 1]
+// = max end; the caller pre-fills start with ~0 and end with 0).
+// ----------------------------------------------------------------------------
+SUN_DEVICE unsigned long long global_timer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+SUN_DEVICE void tl_begin(unsigned long long* tl, int idx) {
+  if (tl != nullptr && threadIdx.x == 0) atomicMin(&tl[2 * idx], global_timer_ns());
+}
+SUN_DEVICE void tl_end(unsigned long long* tl, int idx) {
+  if (tl != nullptr && threadIdx.x == 0) atomicMax(&tl[2 * idx + 1], global_timer_ns());
+}
+
+// ----------------------------------------------------------------------------
 // Programmatic dependent launch
 // ----------------------------------------------------------------------------
 SUN_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

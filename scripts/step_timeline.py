@@ -1,0 +1,66 @@
+"""Device-side timeline of one decode step (GEMM + attention launches, PDL on):
+earliest CTA start / latest CTA end per launch, gaps between launches."""
+import argparse, ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import bench
+from paper_2603_02599_b200 import _lib
+from paper_2603_02599_b200.kvpool import KvPool, pages_for
+from paper_2603_02599_b200.modules import SharedDecodeModule
+from paper_2603_02599_b200.spec import SPECS
+from paper_2603_02599_b200.weights import DeviceWeights, init_weights
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c3")
+ap.add_argument("--layers", type=int, default=3, help="layers to print")
+args = ap.parse_args()
+cfg = bench.CONFIGS[args.config]
+spec = SPECS[cfg["spec"]].with_bits(4) if cfg["bits"] == 4 else SPECS[cfg["spec"]]
+dev = torch.device("cuda")
+B = cfg["batch"]
+ctx = bench.contexts_for(cfg, B)
+max_ctx = max(ctx) + 64
+dw = DeviceWeights(spec, init_weights(spec, 0, dev), dev, max_ctx, free_source=True)
+kv = KvPool(spec, sum(pages_for(c + 40) for c in ctx) + 4, dev)
+kv.fill_random_(1)
+dec = SharedDecodeModule(spec, dw, kv, B, max_ctx)
+nxt = 0
+for i, c in enumerate(ctx):
+    n = pages_for(c + 40)
+    dec.block_tables[i, :n] = torch.arange(nxt, nxt + n, dtype=torch.int32, device=dev)
+    nxt += n
+dec.positions[:B] = torch.tensor(ctx, dtype=torch.int32, device=dev)
+for _ in range(5):
+    dec.step_static(B, 0, graph=False)
+cap = 8 * spec.n_layers + 8
+lib = _lib.load()
+names = ["qkv", "attn", "o", "gate_up", "down"]
+for rep in range(2):
+    tl = torch.zeros(cap, 2, dtype=torch.int64, device=dev)
+    tl[:, 0] = torch.iinfo(torch.int64).max
+    n = ctypes.c_int32()
+    torch.cuda.synchronize()
+    _lib.check(lib.sun_decode_step_timeline(dec._h, dec.tokens.data_ptr(), dec.positions.data_ptr(),
+                                            dec.block_tables.data_ptr(), dec.block_tables.stride(0), B, 0,
+                                            dec.next_tokens.data_ptr(), torch.cuda.current_stream().cuda_stream,
+                                            tl.data_ptr(), cap, ctypes.byref(n)), "timeline")
+    torch.cuda.synchronize()
+t = tl[: n.value].cpu().double()
+t0 = t[:, 0].min()
+t = (t - t0) / 1e3
+lab = [names[i % 5] if i < 5 * spec.n_layers else "lm_head" for i in range(n.value)]
+print(f"{args.config}: {n.value} launches, step span {t[:, 1].max():.1f} us")
+tot = {}
+prev_end = 0.0
+for i in range(n.value):
+    s, e = float(t[i, 0]), float(t[i, 1])
+    d = tot.setdefault(lab[i], [0.0, 0.0, 0])
+    d[0] += e - max(s, prev_end)   # exclusive time: from previous end (or own start) to own end
+    d[1] += e - s
+    d[2] += 1
+    if i < 5 * args.layers or i == n.value - 1:
+        print(f"  {i:3d} {lab[i]:8s} start {s:9.2f} end {e:9.2f} dur {e - s:7.2f} after-prev-end {e - prev_end:7.2f} (overlap {prev_end - s:6.2f})")
+    prev_end = max(prev_end, e)
+print("per class: exclusive us/launch (end - previous end), inclusive us/launch (end - start)")
+for k, (ex, inc, c) in tot.items():
+    print(f"  {k:8s} excl {ex / c:7.2f}  incl {inc / c:7.2f}  x{c}")

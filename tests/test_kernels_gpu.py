@@ -58,17 +58,25 @@ def test_gemm_deterministic_stream_k(cuda):
         assert torch.equal(a, kernels.gemm_bf16(w, x, 64))
 
 
-@pytest.mark.parametrize("sched", ["0", "2"])
+@pytest.mark.parametrize("sched", ["0", "2", "vcl2", "novcl"])
 def test_gemm_schedules_subprocess(sched):
     """The GEMM kernel tests and the end-to-end decode parity under the other
     schedules: 0 = cluster split-K / whole tiles only, 2 = stream-K on every
-    GEMM whose partials fit (covers every fused epilogue with partial tiles)."""
+    GEMM whose partials fit (covers every fused epilogue with partial tiles),
+    vcl2 = L2-reduced virtual clusters wherever a split pays, novcl = hardware
+    clusters only."""
     import os
     import subprocess
     import sys
 
     here = os.path.dirname(os.path.abspath(__file__))
-    env = dict(os.environ, SUN_GEMM_SCHED=sched)
+    env = dict(os.environ)
+    if sched == "vcl2":
+        env["SUN_GEMM_VCLUSTER"] = "2"
+    elif sched == "novcl":
+        env["SUN_GEMM_VCLUSTER"] = "0"
+    else:
+        env["SUN_GEMM_SCHED"] = sched
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", "(gemm or tiny) and not subprocess",
                         os.path.join(here, "test_kernels_gpu.py"), os.path.join(here, "test_decode_parity_gpu.py")],
                        env=env, capture_output=True, text=True, timeout=900)
