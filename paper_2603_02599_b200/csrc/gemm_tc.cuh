@@ -119,7 +119,7 @@ SUN_DEVICE unsigned long long gtimer() {
 #define SUN_STAMP(i) \
   do { if (a.stamps) a.stamps[blockIdx.x * 16 + (i)] = gtimer(); } while (0)
 
-constexpr int kGemmThreads = 192;
+constexpr int kGemmThreads = 224;  // producer(W), MMA, 4 epilogue, producer(X)
 #ifndef SUN_W4_CONV_WARPS
 #define SUN_W4_CONV_WARPS 8
 #endif
@@ -146,11 +146,13 @@ __host__ __device__ inline long long act_offset(int b, long long k, int rows) {
          (((((k & 63) >> 3) ^ (b & 7))) << 4) + (k & 7) * 2;
 }
 
-__host__ __device__ inline uint32_t gemm_stage_bytes(int bn, bool w4) {
-  return (w4 ? kW4PackedBytes + 1024u : 2u * kTileWBytes) + static_cast<uint32_t>(bn) * 256u;
-}
-__host__ __device__ inline size_t gemm_smem_bytes(int bn, int stages, bool w4) {
-  return 1024 + static_cast<size_t>(stages) * gemm_stage_bytes(bn, w4) + kEpiSmemBytes + 1024;
+// bf16: a weight stage is one 128-wide K step (two 16 KB SUN-BLK blocks), an
+// activation stage the matching bn x 128 SUN-ACT slice; separate rings.
+__host__ __device__ inline uint32_t gemm_stage_bytes(int bn, bool w4) { return 2u * kTileWBytes; }
+__host__ __device__ inline uint32_t gemm_xstage_bytes(int bn) { return static_cast<uint32_t>(bn) * 256u; }
+__host__ __device__ inline size_t gemm_smem_bytes(int bn, int stages, int xstages) {
+  return 1024 + static_cast<size_t>(stages) * 2u * kTileWBytes + static_cast<size_t>(xstages) * gemm_xstage_bytes(bn) +
+         kEpiSmemBytes + 1024;
 }
 __host__ __device__ inline uint32_t w4_xstage_bytes(int bn, int xk) { return static_cast<uint32_t>(xk * bn) * 256u; }
 __host__ __device__ inline size_t gemm_smem_bytes_w4(int bn, int wgroup, int wstages, int xk, int xstages) {
@@ -614,9 +616,8 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
   tl_begin(a.tl, a.tl_idx);
   const int stages = a.stages;
   const uint32_t sb = W4 ? w4_wstage_bytes(a.wgroup) : gemm_stage_bytes(a.bn, W4);
-  const uint32_t xoff = 2u * kTileWBytes;  // bf16: X offset inside a stage
-  const int xstages = W4 ? a.xstages : 0;
-  const uint32_t xsb = W4 ? w4_xstage_bytes(a.bn, a.xk) : 0u;
+  const int xstages = a.xstages;
+  const uint32_t xsb = W4 ? w4_xstage_bytes(a.bn, a.xk) : gemm_xstage_bytes(a.bn);
   const int wg = a.wgroup;
   uint8_t* stg = smem;
   uint8_t* xstg = stg + ((stages * sb + 1023u) & ~1023u);  // W4 activation ring (SW128 atoms: 1 KB aligned)
@@ -787,67 +788,82 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
       }
     }
     if (threadIdx.x == 32) SUN_STAMP(3);
-  } else if (warp == 0) {
+  } else if (!W4 && (warp == 0 || warp == 6)) {
+    // ---------------- bf16 producers (blocking, one per ring): warp 0 streams the
+    // weight stages (32 KB: one 128-wide K step of SUN-BLK), warp 6 the activation
+    // stages (bn x 128 SUN-ACT), so the weight ring runs ahead by its whole depth.
     if (elect_one()) {
-      // issue weight (or packed+scales) loads of stage j; X is added separately
-      auto issue_w = [&](int j) {
-        const int s = j % stages;
-        const int tile = (u0 + j) / KS;
-        const int ks = (u0 + j) % KS;
+      const bool wprod = warp == 0;
+      const int depth = wprod ? stages : xstages;
+      uint64_t* fb = wprod ? full : xfull;
+      uint64_t* eb = wprod ? empty : xempty;
+      if (!wprod) pdl_wait();  // activations are the previous kernel's output
+      int ks = u0 % KS, tile = u0 / KS, slot = 0, phase = 0;
+      for (int j = 0; j < n; ++j) {
         const int nb = nblk_of(ks);
-        mbar_arrive_expect_tx(&full[s], nb * (kTileWBytes + a.bn * 128u));
-        bulk_load_hint(stg + s * sb, a.wblk + (static_cast<long long>(tile) * a.kb64 + 2 * ks) * kTileWBytes,
-                       nb * kTileWBytes, &full[s], kEvictFirst);
-      };
-      auto issue_x = [&](int j) {
-        const int s = j % stages;
-        const int ks = (u0 + j) % KS;
-        const int nb = nblk_of(ks);
-        bulk_load_hint(stg + s * sb + xoff, a.xact + static_cast<long long>(2 * ks) * a.bn * 128,
-                       nb * a.bn * 128u, &full[s], kEvictLast);
-      };
-      const int pre = n < stages ? n : stages;
-      for (int j = 0; j < pre; ++j) issue_w(j);  // weights never depend on the previous kernel
-      pdl_wait();
-      for (int j = 0; j < pre; ++j) issue_x(j);
-      for (int j = pre; j < n; ++j) {
-        mbar_wait(&empty[j % stages], ((j / stages) & 1) ^ 1);
-        issue_w(j);
-        issue_x(j);
+        if (j >= depth) mbar_wait(&eb[slot], phase ^ 1);
+        if (wprod) {
+          mbar_arrive_expect_tx(&fb[slot], nb * kTileWBytes);
+          bulk_load_hint(stg + slot * sb, a.wblk + (static_cast<long long>(tile) * a.kb64 + 2 * ks) * kTileWBytes,
+                         nb * kTileWBytes, &fb[slot], kEvictFirst);
+        } else {
+          mbar_arrive_expect_tx(&fb[slot], nb * a.bn * 128u);
+          bulk_load_hint(xstg + slot * xsb, a.xact + static_cast<long long>(2 * ks) * a.bn * 128, nb * a.bn * 128u,
+                         &fb[slot], kEvictLast);
+        }
+        if (++ks == KS) {
+          ks = 0;
+          ++tile;
+        }
+        if (++slot == depth) {
+          slot = 0;
+          phase ^= 1;
+        }
       }
-      prefetch_next_weights(a);
+      if (wprod) prefetch_next_weights(a);
     }
   } else if (warp == 1 && !W4) {
     const uint32_t idesc = make_idesc_bf16(kTileM, a.bn);
-    int seg = 0;
+    int ks = u0 % KS, wslot = 0, wphase = 0, xslot = 0, xphase = 0, buf = 0, tphase = 0;
     for (int j = 0; j < n; ++j) {
-      const int s = j % stages;
-      const int ks = (u0 + j) % KS;
       const bool first = j == 0 || ks == 0, last = j == n - 1 || ks == KS - 1;
-      const int buf = seg % nbuf;
       const int nb = nblk_of(ks);
       if (first) {
-        mbar_wait(&tempty[buf], ((seg / nbuf) & 1) ^ 1);
+        mbar_wait(&tempty[buf], tphase ^ 1);
         tc_fence_after();
       }
-      mbar_wait(&full[s], (j / stages) & 1);
+      mbar_wait(&full[wslot], wphase);
+      mbar_wait(&xfull[xslot], xphase);
       tc_fence_after();
       if (j == 0 && threadIdx.x == 32) SUN_STAMP(2);
       if (elect_one()) {
-        const uint32_t xa = smem_u32(stg + s * sb + xoff);
+        const uint32_t xa = smem_u32(xstg + xslot * xsb);
         const uint32_t tacc = tmem_base + static_cast<uint32_t>(buf * a.bn);
-        const uint32_t wa = smem_u32(stg + s * sb);
+        const uint32_t wa = smem_u32(stg + wslot * sb);
         for (int kk = 0; kk < nb * 4; ++kk) {
           const uint32_t atom = kk >> 2;
           const uint32_t koff = (kk & 3) * 32;
           umma_bf16(tacc, make_sw128_desc(wa + atom * kTileWBytes + koff),
                     make_sw128_desc(xa + atom * (a.bn * 128u) + koff), idesc, (first && kk == 0) ? 0u : 1u);
         }
-        umma_commit(&empty[s]);
+        umma_commit(&empty[wslot]);
+        umma_commit(&xempty[xslot]);
         if (last) umma_commit(&tfull[buf]);
       }
       __syncwarp();
-      if (last) ++seg;
+      if (++wslot == stages) {
+        wslot = 0;
+        wphase ^= 1;
+      }
+      if (++xslot == xstages) {
+        xslot = 0;
+        xphase ^= 1;
+      }
+      if (++ks == KS) ks = 0;
+      if (last && ++buf == nbuf) {
+        buf = 0;
+        tphase ^= 1;
+      }
     }
     if (threadIdx.x == 32) SUN_STAMP(3);
   } else if (warp < 6) {

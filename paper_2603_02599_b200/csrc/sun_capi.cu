@@ -140,11 +140,14 @@ int gemm_max_grid() {
   return v;
 }
 
+// bf16 ring depths: 3 activation stages (2 at bn > 128), weight stages (32 KB)
+// fill the rest of the SM's shared memory (C3, bn = 64: 5 weight stages).
+int gemm_xstages(int bn) { return bn > 128 ? 2 : 3; }
 int gemm_stages(int bn, bool w4, int per_sm) {
-  const int budget = kSmemPerSm / per_sm - 2048;
-  const int avail = budget - 1024 - int(kEpiSmemBytes) - 512;
-  int st = avail / int(gemm_stage_bytes(bn, w4));
-  return std::max(2, std::min(w4 ? 16 : 6, st));  // barrier region (512 B) holds <= 16 stages
+  const int budget = kSmemPerSm / per_sm - 2048 - 2048 - int(kEpiSmemBytes) - 1024 -
+                     gemm_xstages(bn) * int(gemm_xstage_bytes(bn));
+  const int st = budget / int(gemm_stage_bytes(bn, w4));
+  return std::max(2, std::min(8, st));
 }
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -453,8 +456,9 @@ LaunchCfg launch_cfg(const GemmPlan& p, int bn, bool w4, bool have_sk) {
     ring = size_t(c.stages) * w4_wstage_bytes(c.wgroup) + size_t(c.xstages) * w4_xstage_bytes(bn, c.xk);
   } else {
     c.stages = gemm_stages(bn, w4, per_sm);
-    c.smem = gemm_smem_bytes(bn, c.stages, w4);
-    ring = size_t(c.stages) * gemm_stage_bytes(bn, w4);
+    c.xstages = gemm_xstages(bn);
+    c.smem = gemm_smem_bytes(bn, c.stages, c.xstages);
+    ring = size_t(c.stages) * gemm_stage_bytes(bn, w4) + size_t(c.xstages) * gemm_xstage_bytes(bn);
   }
   // Stream-K where whole tiles cannot balance over the SMs (more tiles than CTA
   // slots, e.g. gate_up 224 tiles / 148 SMs = 1.51) and every owner's
