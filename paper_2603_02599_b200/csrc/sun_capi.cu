@@ -564,7 +564,7 @@ int auto_pages_per_split(const SunDecoderDims& d, int batch) {
   // pages (128 tokens) so a unit amortises its TMA ramp.
   const int max_pages = (d.max_context + kPageTokens - 1) / kPageTokens;
   const long long pairs = (long long)batch * d.n_kv_heads;
-  if (pairs >= 3LL * kNumSms) return max_pages;
+  if (pairs >= 3LL * kNumSms && d.head_dim == 128) return max_pages;  // (d = 64: C2 0.99 vs 0.96 ms split)
   const long long want_units = 8LL * kNumSms;
   long long splits = (want_units + pairs - 1) / pairs;
   if (splits < 1) splits = 1;
