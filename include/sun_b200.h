@@ -155,11 +155,13 @@ SunStatus sun_decode_step_profile(SunDecoder* dec, const int32_t* tokens, const 
 /* One sun_decode_step (PDL as configured, not serialised) with a device-side
  * timeline of its GEMM and attention launches: timeline is a DEVICE uint64 array
  * [capacity][2] pre-filled with (~0, 0); launch i records the earliest CTA start
- * and the latest CTA end (%globaltimer ns). Profiling only. */
+ * and the latest CTA end (%globaltimer ns). If stamps is non-null and launch
+ * stamp_launch is a GEMM, its CTAs also write sun_gemm_bf16_stamped's per-CTA
+ * phase stamps there ([grid][16]). Profiling only. */
 SunStatus sun_decode_step_timeline(SunDecoder* dec, const int32_t* tokens, const int32_t* positions,
                                    const int32_t* block_tables, int32_t bt_stride, int32_t batch,
                                    int32_t pages_per_split, int32_t* next_tokens, void* stream, uint64_t* timeline,
-                                   int32_t capacity, int32_t* n_launches);
+                                   int32_t capacity, int32_t* n_launches, uint64_t* stamps, int32_t stamp_launch);
 
 /* Number of kernels this thread has launched through the library so far. */
 SunStatus sun_launch_count(int64_t* launches);

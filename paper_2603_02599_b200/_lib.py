@@ -71,7 +71,7 @@ SIGNATURES = {
     "sun_decode_step_profile": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp,
                                         ctypes.POINTER(c_f32), c_i32, ctypes.POINTER(c_i32)]),
     "sun_decode_step_timeline": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_i32,
-                                         ctypes.POINTER(c_i32)]),
+                                         ctypes.POINTER(c_i32), c_vp, c_i32]),
     "sun_launch_count": (c_i32, [ctypes.POINTER(c_i64)]),
     "sun_gemm_workspace_bytes": (c_i32, [c_i64, c_i64, c_i32, ctypes.POINTER(c_size)]),
     "sun_gemm_bf16": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i32, c_vp, c_i64, c_i32, c_vp,

@@ -256,6 +256,8 @@ thread_local LaunchTrace g_trace;
 struct TimelineState {
   unsigned long long* tl = nullptr;
   int next = 0, capacity = 0;
+  unsigned long long* stamps = nullptr;  // per-CTA phase stamps for launch `stamp_idx` (GEMMs)
+  int stamp_idx = -1;
 };
 thread_local TimelineState g_tl;
 template <typename A>
@@ -264,6 +266,9 @@ void tl_assign(A& a) {
     a.tl = g_tl.tl;
     a.tl_idx = g_tl.next++;
   }
+}
+void tl_stamps(GemmArgs& a) {
+  if (g_tl.stamps != nullptr && a.tl != nullptr && a.tl_idx == g_tl.stamp_idx) a.stamps = g_tl.stamps;
 }
 
 template <typename... KArgs, typename... Args>
@@ -532,6 +537,7 @@ SunStatus run_gemm(const void* wblk, const void* packed, const void* scales, Gem
   a.wgroup = c.wgroup;
   a.xk = c.xk;
   tl_assign(a);
+  tl_stamps(a);
   a.splits = c.splits;
   a.vcluster = c.vcluster;
   a.sk_units = c.sk_units;
@@ -845,11 +851,13 @@ SunStatus sun_decode_step_profile(SunDecoder* dec, const int32_t* tokens, const 
 SunStatus sun_decode_step_timeline(SunDecoder* dec, const int32_t* tokens, const int32_t* positions,
                                    const int32_t* block_tables, int32_t bt_stride, int32_t batch,
                                    int32_t pages_per_split, int32_t* next_tokens, void* stream, uint64_t* timeline,
-                                   int32_t capacity, int32_t* n_launches) {
+                                   int32_t capacity, int32_t* n_launches, uint64_t* stamps, int32_t stamp_launch) {
   if (!dec || !timeline || !n_launches || capacity < 1) return fail(SUN_ERR_VALUE, "null argument");
   g_tl.tl = reinterpret_cast<unsigned long long*>(timeline);
   g_tl.next = 0;
   g_tl.capacity = capacity;
+  g_tl.stamps = reinterpret_cast<unsigned long long*>(stamps);
+  g_tl.stamp_idx = stamp_launch;
   SunStatus s = sun_decode_step(dec, tokens, positions, block_tables, bt_stride, batch, pages_per_split, nullptr,
                                 next_tokens, 0, stream);
   *n_launches = g_tl.next;

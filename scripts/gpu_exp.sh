@@ -3,5 +3,4 @@ timeout 1500 python -m pytest -q -m gpu tests/ -x > gpurun_out/pytest_gpu.log 2>
 run() { tag=$1; shift; e=(); while [[ "$1" == *=* ]]; do e+=("$1"); shift; done; env "${e[@]}" timeout 300 python bench.py --steps 50 --no-cpu --no-e2e "$@" > gpurun_out/x_$tag.json 2>gpurun_out/x_$tag.err; }
 run c3
 run c4 --config c4 --steps 20
-python scripts/step_timeline.py --config c3 > gpurun_out/tl_c3.txt 2>&1
-python scripts/gemm_timeline.py > gpurun_out/timeline_base.txt 2>&1
+for k in 10 12 14; do python scripts/step_timeline.py --config c3 --layers 3 --stamp $k > gpurun_out/tl_stamp_$k.txt 2>&1; done

@@ -13,6 +13,7 @@ from paper_2603_02599_b200.weights import DeviceWeights, init_weights
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c3")
 ap.add_argument("--layers", type=int, default=3, help="layers to print")
+ap.add_argument("--stamp", type=int, default=-1, help="launch index whose per-CTA phases to print")
 args = ap.parse_args()
 cfg = bench.CONFIGS[args.config]
 spec = SPECS[cfg["spec"]].with_bits(4) if cfg["bits"] == 4 else SPECS[cfg["spec"]]
@@ -36,6 +37,7 @@ cap = 8 * spec.n_layers + 8
 lib = _lib.load()
 names = ["qkv", "attn", "o", "gate_up", "down"]
 for rep in range(2):
+    st = torch.zeros(4096 * 16, dtype=torch.int64, device=dev)
     tl = torch.zeros(cap, 2, dtype=torch.int64, device=dev)
     tl[:, 0] = torch.iinfo(torch.int64).max
     n = ctypes.c_int32()
@@ -43,7 +45,8 @@ for rep in range(2):
     _lib.check(lib.sun_decode_step_timeline(dec._h, dec.tokens.data_ptr(), dec.positions.data_ptr(),
                                             dec.block_tables.data_ptr(), dec.block_tables.stride(0), B, 0,
                                             dec.next_tokens.data_ptr(), torch.cuda.current_stream().cuda_stream,
-                                            tl.data_ptr(), cap, ctypes.byref(n)), "timeline")
+                                            tl.data_ptr(), cap, ctypes.byref(n), st.data_ptr() if args.stamp >= 0 else None,
+                                            args.stamp), "timeline")
     torch.cuda.synchronize()
 t = tl[: n.value].cpu().double()
 t0 = t[:, 0].min()
@@ -64,3 +67,16 @@ for i in range(n.value):
 print("per class: exclusive us/launch (end - previous end), inclusive us/launch (end - start)")
 for k, (ex, inc, c) in tot.items():
     print(f"  {k:8s} excl {ex / c:7.2f}  incl {inc / c:7.2f}  x{c}")
+
+if args.stamp >= 0:
+    sv = st.view(4096, 16).cpu().double()
+    sv = sv[sv[:, 0] > 0]
+    rel = (sv - t0) / 1e3
+    print(f"launch {args.stamp} ({lab[args.stamp]}): {len(sv)} CTAs; phase times relative to step start (us)")
+    nm = ["start", "setup", "first_stage", "last_mma", "first_acc", "epi_done", "exit", "-", "parked", "sync1",
+          "reduced", "epi_chunk"]
+    for i, name in enumerate(nm):
+        if name == "-" or (sv[:, i] == 0).all():
+            continue
+        c = rel[:, i][sv[:, i] > 0]
+        print(f"   {name:12s} min {c.min():9.2f} med {c.median():9.2f} max {c.max():9.2f}")
