@@ -4,9 +4,9 @@
 per step over a mixed-model batch (members prefilled by different task
 modules), optionally replayed from a CUDA graph per (batch, split) bucket.
 ``PrefillModule`` is a task-specific P_θp^τ: it writes the prompt's KV into the
-shared paged pool with the same kernels (one position per launch chain — the
-producer side is not the measured hot path) and returns the
-first generated token, as Eq. 2 specifies.
+shared paged pool with the same kernels — token-parallel, up to ``max_batch``
+prompt positions per step — and returns the first generated
+token, as Eq. 2 specifies.
 """
 from __future__ import annotations
 
@@ -173,29 +173,40 @@ class PrefillModule(_StepRunner):
         self._logits = torch.zeros(self.max_batch, spec.vocab, dtype=torch.float32, device=dev)
 
     def prefill(self, prompts: list[list[int]], block_tables: list[list[int]]) -> tuple[list[int], torch.Tensor]:
-        """Fill each prompt's pages and return (first tokens, first-token logits [B, V])."""
+        """Fill each prompt's pages and return (first tokens, first-token logits [B, V]).
+
+        Token-parallel chunked prefill: every (prompt, position) pair is one row of
+        a ``sun_decode_step`` batch (its own position, its prompt's block table), up
+        to ``max_batch`` rows per step. Inside a step each layer's QKV epilogue
+        appends the KV of all rows before that layer's attention runs, so a row at
+        position t attends over positions 0..t whether they came from an earlier
+        step or from the same one; a prompt's rows are issued in position order.
+        Same math per token as decoding the prompt one position at a time."""
         dev = self.weights.device
         B = len(prompts)
-        if B > self.max_batch:
-            raise ValueError("too many prompts for this prefill module")
         lens = [len(p) for p in prompts]
-        if min(lens) < 1:
+        if B < 1 or min(lens) < 1:
             raise ValueError("isl must be >= 1")
+        for i, row in enumerate(block_tables):
+            if len(row) * PAGE_TOKENS < lens[i]:
+                raise ValueError(f"prompt {i}: {len(row)} pages cannot hold {lens[i]} tokens")
         bt = torch.zeros(B, self.max_pages, dtype=torch.int32)
         for i, row in enumerate(block_tables):
             bt[i, :len(row)] = torch.tensor(row, dtype=torch.int32)
+        rows = [(i, t) for i in range(B) for t in range(lens[i])]  # prompt-major, positions ascending
         first = [0] * B
         last_logits = torch.zeros(B, self.spec.vocab, dtype=torch.float32, device=dev)
-        for t in range(max(lens)):
-            act = [i for i in range(B) if t < lens[i]]
-            toks = torch.tensor([prompts[i][t] for i in act], dtype=torch.int32).to(dev)
-            pos = torch.full((len(act),), t, dtype=torch.int32).to(dev)
-            bts = bt[act].to(dev)
-            self.launch(toks, pos, bts, len(act), self._next, self._logits)
-            done = [j for j, i in enumerate(act) if t == lens[i] - 1]
+        C = self.max_batch
+        for c0 in range(0, len(rows), C):
+            chunk = rows[c0:c0 + C]
+            toks = torch.tensor([prompts[i][t] for i, t in chunk], dtype=torch.int32).to(dev)
+            pos = torch.tensor([t for _, t in chunk], dtype=torch.int32).to(dev)
+            bts = bt[[i for i, _ in chunk]].to(dev)
+            self.launch(toks, pos, bts, len(chunk), self._next, self._logits)
+            done = [(j, i) for j, (i, t) in enumerate(chunk) if t == lens[i] - 1]
             if done:
-                nt = self._next[:len(act)].cpu()
-                for j in done:
-                    first[act[j]] = int(nt[j])
-                    last_logits[act[j]] = self._logits[j]
+                nt = self._next[:len(chunk)].cpu()
+                for j, i in done:
+                    first[i] = int(nt[j])
+                    last_logits[i] = self._logits[j]
         return first, last_logits

@@ -30,7 +30,7 @@ def test_scheduler_drives_b200_executor_mixed_batches(cuda):
     kv.tensor.zero_()
     alloc = PageAllocator(kv.num_pages)
     dec = SharedDecodeModule(spec, DeviceWeights(spec, w_d, cuda, max_ctx), kv, max_batch=16, max_context=max_ctx)
-    pre = {t: PrefillModule(spec, DeviceWeights(spec, w_ps[t], cuda, max_ctx), kv, 1, max_ctx, task_id=t)
+    pre = {t: PrefillModule(spec, DeviceWeights(spec, w_ps[t], cuda, max_ctx), kv, 64, max_ctx, task_id=t)
            for t in range(n_models)}
     ex = B200Executor(dec, pre, alloc, graph=True, keep_logits=True)
 
