@@ -65,30 +65,6 @@ SUN_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// Non-blocking probe: has the phase with this parity completed?
-SUN_DEVICE bool mbar_test(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, P1;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-
-// Busy-poll variant (no suspend): for latency-critical hand-offs between warps.
-SUN_DEVICE void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
 // ----------------------------------------------------------------------------
 // TMA
 // ----------------------------------------------------------------------------
@@ -138,7 +114,7 @@ SUN_DEVICE void bulk_load_hint(void* smem_dst, const void* gsrc, uint32_t bytes,
 // start and the latest CTA end in %globaltimer ns (tl[2 i] = min start, tl[2 i + 1]
 // = max end; the caller pre-fills start with ~0 and end with 0).
 // ----------------------------------------------------------------------------
-SUN_DEVICE unsigned long long global_timer_ns() {
+SUN_DEVICE unsigned long long global_timer_ns() {  // (gemm_tc.cuh's gtimer() is the same read)
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
