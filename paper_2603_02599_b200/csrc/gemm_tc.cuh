@@ -119,7 +119,7 @@ SUN_DEVICE unsigned long long gtimer() {
 #define SUN_STAMP(i) \
   do { if (a.stamps) a.stamps[blockIdx.x * 16 + (i)] = gtimer(); } while (0)
 
-constexpr int kGemmThreads = 224;  // producer(W), MMA, 4 epilogue, producer(X)
+constexpr int kGemmThreads = 352;  // producer(W), MMA, epilogue group A (4), producer(X), epilogue group B (4)
 #ifndef SUN_W4_CONV_WARPS
 #define SUN_W4_CONV_WARPS 8
 #endif
@@ -137,8 +137,9 @@ __host__ __device__ inline uint32_t w4_wstage_bytes(int wgroup) { return static_
 constexpr int kMaxWStages = 16, kMaxXStages = 8;
 constexpr int kW4MaxABufs = 6;  // W4: dequantised 128x128 A tiles (64 TMEM columns each) at the top of TMEM
 
-// partner staging [16][128] f32 | argmax scratch 512 B | column meta: pos[256], page[256], r_b[256] | 512 spare
-constexpr uint32_t kEpiSmemBytes = 16 * kTileM * 4 + 512 + 3072 + 512;
+// column meta: pos[256], page[256], r_b[256] | per epilogue group: partner staging [16][128] f32 + 512 B scratch
+constexpr uint32_t kEpiGroupBytes = 16 * kTileM * 4 + 512;
+constexpr uint32_t kEpiSmemBytes = 3072 + 2 * kEpiGroupBytes;
 
 // byte offset of activation element (row b, column k) in SUN-ACT with `rows` rows per atom
 __host__ __device__ inline long long act_offset(int b, long long k, int rows) {
@@ -173,15 +174,27 @@ __host__ __device__ inline int w4_abufs(int bn) {
   return n < kW4MaxABufs ? n : kW4MaxABufs;
 }
 
-SUN_DEVICE void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+// Epilogue warps form groups of four (one per TMEM lane quarter): group A =
+// warps 2..5, group B = warps 7..10 (bf16 kernel only); a group takes every other
+// 16-column chunk, with its own named barrier and staging smem.
+SUN_DEVICE int epi_grp() { return threadIdx.x >= 224 ? 1 : 0; }
+SUN_DEVICE bool epi_lead_warp() { return static_cast<int>(threadIdx.x >> 5) == (epi_grp() ? 7 : 2); }
+SUN_DEVICE bool epi_lead_thread() { return threadIdx.x == (epi_grp() ? 224u : 64u); }
+SUN_DEVICE void epi_bar() { asm volatile("bar.sync %0, 128;" ::"r"(1 + 2 * epi_grp()) : "memory"); }
+SUN_DEVICE int* epi_meta(float* epi) { return reinterpret_cast<int*>(epi); }
+SUN_DEVICE float* epi_stage(float* epi) {
+  return reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(epi) + 3072 + epi_grp() * kEpiGroupBytes);
+}
 
 template <int EPI>
-SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, float (&v)[16],
-                          float* stage_f32, float* red_val, int* red_idx) {
+SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, float (&v)[16], float* epi) {
   const int row = m_tile * kTileM + row_local;
   const int B = a.batch;
+  float* stage_f32 = epi_stage(epi);
+  float* red_val = stage_f32 + 16 * kTileM;
+  int* red_idx = reinterpret_cast<int*>(red_val + 64);
   if (a.ss_in != nullptr) {  // consumer of a factored RMSNorm: W.(x*g) * r_b
-    const float* rb = reinterpret_cast<const float*>(red_idx + 64 + 512);
+    const float* rb = reinterpret_cast<const float*>(epi_meta(epi) + 512);
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] *= rb[c0 + j];
   }
@@ -218,7 +231,7 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
           for (int j = 0; j < 16; ++j) red_val[q * 16 + j] = nw[j];
         }
         epi_bar();
-        if (threadIdx.x / 32 == 2 && lane < 16) {
+        if (epi_lead_warp() && lane < 16) {
           const float t = ((red_val[lane] + red_val[16 + lane]) + red_val[32 + lane]) + red_val[48 + lane];
           a.ss_out[static_cast<long long>(m_tile) * a.bn + c0 + lane] = t;
         }
@@ -271,7 +284,7 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
       }
     }
     epi_bar();
-    if (threadIdx.x / 32 == 2 && lane < 16) {
+    if (epi_lead_warp() && lane < 16) {
       float val = red_val[lane];
       int idx = red_idx[lane];
 #pragma unroll
@@ -325,7 +338,7 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
         const int fi = i < half ? i : i - half;
         const int partner = i < half ? row_local + half : row_local - half;
         const bool is_v = row >= qd + kd;
-        const int* meta = reinterpret_cast<const int*>(red_idx + 64);  // [0,256) pos, [256,512) page
+        const int* meta = epi_meta(epi);  // [0,256) pos, [256,512) page
         // hoisted, independent loads: one round trip for the 32 table values
         float cs[16], sn[16], pv[16];
 #pragma unroll
@@ -403,23 +416,21 @@ __global__ void block_activations_kernel(const __nv_bfloat16* __restrict__ x, in
 
 // Unsplit tile: TMEM accumulator -> fused epilogue directly.
 template <int EPI>
-SUN_DEVICE void direct_epilogue(const GemmArgs& a, int tile, uint32_t taddr, float* epi) {
+SUN_DEVICE void direct_epilogue(const GemmArgs& a, int tile, uint32_t taddr, float* epi, int ngroups) {
   const int q = (threadIdx.x / 32) & 3;
   const int row_local = q * 32 + (threadIdx.x & 31);
-  float* red_val = epi + 16 * kTileM;
-  int* red_idx = reinterpret_cast<int*>(red_val + 64);
   float v[16];
-  for (int c0 = 0; c0 < a.bn; c0 += 16) {
+  for (int c0 = 16 * epi_grp(); c0 < a.bn; c0 += 16 * ngroups) {
     tmem_ld16(taddr + c0, v);
-    epi_chunk<EPI>(a, tile, row_local, c0, v, epi, red_val, red_idx);
+    epi_chunk<EPI>(a, tile, row_local, c0, v, epi);
   }
 }
 
 // Per-column epilogue metadata, once per CTA: QKV positions / KV pages, and the
 // factored RMSNorm scale r_b = rsqrt(sum_t ss[t][b] / h + eps) (tile order fixed).
 template <int EPI>
-SUN_DEVICE void load_qkv_meta(const GemmArgs& a, float* epi) {
-  int* meta = reinterpret_cast<int*>(epi + 16 * kTileM + 128);
+SUN_DEVICE void load_qkv_meta(const GemmArgs& a, float* epi) {  // epilogue group A
+  int* meta = epi_meta(epi);
   if constexpr (EPI == EPI_QKV_ROPE) {
     for (int b = threadIdx.x - 64; b < a.bn; b += 128) {
       const int pos = b < a.batch ? a.positions[b] : 0;
@@ -546,8 +557,6 @@ SUN_DEVICE void sk_owner_epilogue(const GemmArgs& a, int tile, uint32_t taddr, i
   }
   mbar_wait(bar, 0);
   const float* parts = reinterpret_cast<const float*>(ring);
-  float* red_val = epi + 16 * kTileM;
-  int* red_idx = reinterpret_cast<int*>(red_val + 64);
   float v[16];
   for (int c0 = 0; c0 < a.bn; c0 += 16) {
     tmem_ld16(taddr + c0, v);
@@ -562,7 +571,7 @@ SUN_DEVICE void sk_owner_epilogue(const GemmArgs& a, int tile, uint32_t taddr, i
         v[4 * j + 3] += x.w;
       }
     }
-    epi_chunk<EPI>(a, tile, row_local, c0, v, epi, red_val, red_idx);
+    epi_chunk<EPI>(a, tile, row_local, c0, v, epi);
   }
   epi_bar();
   if (threadIdx.x == 64)
@@ -672,7 +681,7 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
     }
     for (int j = 0; j < 2; ++j) {
       mbar_init(&tfull[j], 1);
-      mbar_init(&tempty[j], 1);
+      mbar_init(&tempty[j], W4 ? 1 : 2);  // one arrival per epilogue group
     }
     for (int j = 0; j < kW4MaxABufs; ++j) {
       mbar_init(&dfull[j], kW4ConvThreads / 32);
@@ -866,10 +875,11 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
       }
     }
     if (threadIdx.x == 32) SUN_STAMP(3);
-  } else if (warp < 6) {
-    // ---------------- epilogue: warps 2..5 ----------------
+  } else if (warp < 6 || (!W4 && warp >= 7)) {
+    // ---------------- epilogue: group A = warps 2..5 (+ group B = warps 7..10, bf16) ----------------
     pdl_wait();
-    load_qkv_meta<EPI>(a, epi);
+    if (warp < 6) load_qkv_meta<EPI>(a, epi);
+    if constexpr (!W4) asm volatile("bar.sync 4, 256;" ::: "memory");  // group B waits for the meta
     const int q = warp & 3;
     const int row_local = q * 32 + (threadIdx.x & 31);
     for (int seg = 0; seg < nseg; ++seg) {
@@ -882,13 +892,13 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
       if (threadIdx.x == 64 && seg == 0) SUN_STAMP(4);
       const uint32_t taddr = tmem_base + static_cast<uint32_t>(buf * a.bn) + (static_cast<uint32_t>(q * 32) << 16);
       if (!clustered) {
-        if (kb == 0 && ke == KS) direct_epilogue<EPI>(a, tile, taddr, epi);
-        else if (kb > 0) sk_store_partial(a, taddr, row_local);
-        else sk_owner_epilogue<EPI>(a, tile, taddr, row_local, epi, stg, skbar);
+        if (kb == 0 && ke == KS) direct_epilogue<EPI>(a, tile, taddr, epi, W4 ? 1 : 2);
+        else if (epi_grp() == 0 && kb > 0) sk_store_partial(a, taddr, row_local);  // stream-K: group A only
+        else if (epi_grp() == 0) sk_owner_epilogue<EPI>(a, tile, taddr, row_local, epi, stg, skbar);
         tc_fence_before();
         epi_bar();
-        if (threadIdx.x == 64) mbar_arrive(&tempty[buf]);
-      } else {
+        if (epi_lead_thread()) mbar_arrive(&tempty[buf]);
+      } else if (epi_grp() == 0) {
         // park the partial (part_index layout) in the now idle shared memory
         // (hardware cluster: peers read it over DSMEM) or in L2 (virtual cluster)
         float* part = vcl ? a.sk_part + static_cast<long long>(blockIdx.x) * a.bn * kTileM
@@ -960,14 +970,13 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
       cluster_sync_all();  // every rank's partial is visible cluster-wide
     }
     if (threadIdx.x == 64) SUN_STAMP(9);
-    if (warp >= 2 && warp < 6) {
+    if ((warp >= 2 && warp < 6) || (!W4 && warp >= 7)) {
       const int q = warp & 3;
       const int row_local = q * 32 + (threadIdx.x & 31);
       float* part = reinterpret_cast<float*>(smem);
       const float* gpart = vcl ? a.sk_part + static_cast<long long>(blockIdx.x - rank) * a.bn * kTileM : nullptr;
-      float* red_val = epi + 16 * kTileM;
-      int* red_idx = reinterpret_cast<int*>(red_val + 64);
-      for (int c0 = static_cast<int>(rank) * 16; c0 < a.bn; c0 += static_cast<int>(S) * 16) {
+      const int ng = W4 ? 1 : 2;  // the rank's chunks alternate between the epilogue groups
+      for (int c0 = static_cast<int>(rank + S * epi_grp()) * 16; c0 < a.bn; c0 += static_cast<int>(S * ng) * 16) {
         float4 x[4][4];
         float v[16];
 #pragma unroll
@@ -992,7 +1001,7 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
             }
         }
         if (threadIdx.x == 64) SUN_STAMP(10);
-        epi_chunk<EPI>(a, t_first, row_local, c0, v, epi, red_val, red_idx);
+        epi_chunk<EPI>(a, t_first, row_local, c0, v, epi);
         if (threadIdx.x == 64) SUN_STAMP(11);
       }
     }

@@ -142,7 +142,10 @@ int gemm_max_grid() {
 
 // bf16 ring depths: 3 activation stages (2 at bn > 128), weight stages (32 KB)
 // fill the rest of the SM's shared memory (C3, bn = 64: 5 weight stages).
-int gemm_xstages(int bn) { return bn > 128 ? 2 : 3; }
+int gemm_xstages(int bn) {
+  static const int env = [] { const char* e = getenv("SUN_GEMM_XSTAGES"); return e ? atoi(e) : 0; }();
+  return env > 0 ? env : (bn > 128 ? 2 : 3);
+}
 int gemm_stages(int bn, bool w4, int per_sm) {
   const int budget = kSmemPerSm / per_sm - 2048 - 2048 - int(kEpiSmemBytes) - 1024 -
                      gemm_xstages(bn) * int(gemm_xstage_bytes(bn));
