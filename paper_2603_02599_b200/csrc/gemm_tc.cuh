@@ -186,8 +186,8 @@ SUN_DEVICE float* epi_stage(float* epi) {
   return reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(epi) + 3072 + epi_grp() * kEpiGroupBytes);
 }
 
-template <int EPI>
-SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, float (&v)[16], float* epi) {
+template <int EPI, int NC = 16>  // NC: columns in this chunk (16, or 8 for a half chunk)
+SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, float (&v)[NC], float* epi) {
   const int row = m_tile * kTileM + row_local;
   const int B = a.batch;
   float* stage_f32 = epi_stage(epi);
@@ -196,20 +196,20 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
   if (a.ss_in != nullptr) {  // consumer of a factored RMSNorm: W.(x*g) * r_b
     const float* rb = reinterpret_cast<const float*>(epi_meta(epi) + 512);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] *= rb[c0 + j];
+    for (int j = 0; j < NC; ++j) v[j] *= rb[c0 + j];
   }
   if constexpr (EPI == EPI_STORE_F32 || EPI == EPI_RESID_ADD) {
     if constexpr (EPI == EPI_RESID_ADD) {
       if (a.norm_w != nullptr) {  // producer of the next RMSNorm's operand + sums of squares
-        float nw[16];
+        float nw[NC];
         const bool in = row < a.n_out;
         float* base = a.out_f32 + static_cast<long long>(c0) * a.ldo + row;
-        float old[16];
+        float old[NC];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) old[j] = (in && c0 + j < B) ? base[j * a.ldo] : 0.f;
+        for (int j = 0; j < NC; ++j) old[j] = (in && c0 + j < B) ? base[j * a.ldo] : 0.f;
         const float g = in ? __bfloat162float(a.norm_w[row]) : 0.f;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < NC; ++j) {
           nw[j] = old[j] + v[j];
           if (in && c0 + j < B) {
             base[j * a.ldo] = nw[j];
@@ -222,17 +222,17 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
         const int lane = threadIdx.x & 31;
         const int q = (threadIdx.x / 32) & 3;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < NC; ++j) {
 #pragma unroll
           for (int off = 16; off > 0; off >>= 1) nw[j] += __shfl_xor_sync(0xffffffffu, nw[j], off);
         }
         if (lane == 0) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) red_val[q * 16 + j] = nw[j];
+          for (int j = 0; j < NC; ++j) red_val[q * NC + j] = nw[j];
         }
         epi_bar();
-        if (epi_lead_warp() && lane < 16) {
-          const float t = ((red_val[lane] + red_val[16 + lane]) + red_val[32 + lane]) + red_val[48 + lane];
+        if (epi_lead_warp() && lane < NC) {
+          const float t = ((red_val[lane] + red_val[NC + lane]) + red_val[2 * NC + lane]) + red_val[3 * NC + lane];
           a.ss_out[static_cast<long long>(m_tile) * a.bn + c0 + lane] = t;
         }
         epi_bar();
@@ -243,15 +243,15 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
       float* base = a.out_f32 + static_cast<long long>(c0) * a.ldo + row;
       if constexpr (EPI == EPI_RESID_ADD) {
         // issue all 16 residual loads before any store (one memory round trip)
-        float old[16];
+        float old[NC];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) old[j] = (c0 + j < B) ? base[j * a.ldo] : 0.f;
+        for (int j = 0; j < NC; ++j) old[j] = (c0 + j < B) ? base[j * a.ldo] : 0.f;
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
+        for (int j = 0; j < NC; ++j)
           if (c0 + j < B) base[j * a.ldo] = old[j] + v[j];
       } else {
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
+        for (int j = 0; j < NC; ++j)
           if (c0 + j < B) base[j * a.ldo] = v[j];
       }
     }
@@ -259,7 +259,7 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
     const int lane = threadIdx.x & 31;
     const int q = (threadIdx.x / 32) & 3;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < NC; ++j) {
       const int b = c0 + j;
       float val = v[j];
       int idx = row;
@@ -279,18 +279,18 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
         }
       }
       if (lane == 0) {
-        red_val[q * 16 + j] = val;
-        red_idx[q * 16 + j] = idx;
+        red_val[q * NC + j] = val;
+        red_idx[q * NC + j] = idx;
       }
     }
     epi_bar();
-    if (epi_lead_warp() && lane < 16) {
+    if (epi_lead_warp() && lane < NC) {
       float val = red_val[lane];
       int idx = red_idx[lane];
 #pragma unroll
       for (int w = 1; w < 4; ++w) {
-        const float ov = red_val[w * 16 + lane];
-        const int oi = red_idx[w * 16 + lane];
+        const float ov = red_val[w * NC + lane];
+        const int oi = red_idx[w * NC + lane];
         if (ov > val || (ov == val && oi < idx)) {
           val = ov;
           idx = oi;
@@ -306,17 +306,17 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
     if constexpr (EPI == EPI_QKV_ROPE) {
       const float bias = (a.bias != nullptr && row < a.n_out) ? __bfloat162float(a.bias[row]) : 0.f;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] += bias;
+      for (int j = 0; j < NC; ++j) v[j] += bias;
     }
 #pragma unroll
-    for (int j = 0; j < 16; ++j) stage_f32[j * kTileM + row_local] = v[j];
+    for (int j = 0; j < NC; ++j) stage_f32[j * kTileM + row_local] = v[j];
     epi_bar();
     if constexpr (EPI == EPI_SWIGLU) {
       if (row_local < 64) {
         const int jo = m_tile * 64 + row_local;
         if (jo < a.n_valid_out) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
+          for (int j = 0; j < NC; ++j) {
             const int b = c0 + j;
             if (b < B) {
               const float g = v[j];
@@ -340,9 +340,9 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
         const bool is_v = row >= qd + kd;
         const int* meta = epi_meta(epi);  // [0,256) pos, [256,512) page
         // hoisted, independent loads: one round trip for the 32 table values
-        float cs[16], sn[16], pv[16];
+        float cs[NC], sn[NC], pv[NC];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < NC; ++j) {
           const int pos = meta[(c0 + j) & 255];
           const bool ok = !is_v && (c0 + j < B);
           cs[j] = ok ? a.rope_cos[static_cast<long long>(pos) * half + fi] : 1.f;
@@ -352,7 +352,7 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
         const bool lo_half = i < half;
         if (row < qd) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
+          for (int j = 0; j < NC; ++j) {
             if (c0 + j < B) {
               const float o = lo_half ? (v[j] * cs[j] - pv[j] * sn[j]) : (v[j] * cs[j] + pv[j] * sn[j]);
               a.out_bf16[static_cast<long long>(c0 + j) * a.ldb + row] = __float2bfloat16_rn(o);
@@ -363,7 +363,7 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
           const int g = (row - qd - kvsel * kd) / d;
           const long long inner = ((static_cast<long long>(a.layer * 2 + kvsel) * a.n_kv_heads + g) * a.page_size) * d + i;
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
+          for (int j = 0; j < NC; ++j) {
             if (c0 + j < B) {
               const float o = is_v ? v[j] : (lo_half ? (v[j] * cs[j] - pv[j] * sn[j]) : (v[j] * cs[j] + pv[j] * sn[j]));
               const int pos = meta[(c0 + j) & 255];
@@ -975,34 +975,51 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
       const int row_local = q * 32 + (threadIdx.x & 31);
       float* part = reinterpret_cast<float*>(smem);
       const float* gpart = vcl ? a.sk_part + static_cast<long long>(blockIdx.x - rank) * a.bn * kTileM : nullptr;
-      const int ng = W4 ? 1 : 2;  // the rank's chunks alternate between the epilogue groups
-      for (int c0 = static_cast<int>(rank + S * epi_grp()) * 16; c0 < a.bn; c0 += static_cast<int>(S * ng) * 16) {
-        float4 x[4][4];
-        float v[16];
+      // reduce columns [c0, c0 + NC) over the S ranks (float4 slots q0.. of the chunk), in rank order
+      auto reduce_cols = [&](int c0, int q0, auto& v) {
+        constexpr int NQ = sizeof(v) / sizeof(float) / 4;
+        float4 x[4][NQ];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = 0.f;
-        for (uint32_t r0 = 0; r0 < S; r0 += 4) {  // 4 ranks' loads in flight, summed in rank order
+        for (int j = 0; j < 4 * NQ; ++j) v[j] = 0.f;
+        const int cbase = c0 & ~15;
+        for (uint32_t r0 = 0; r0 < S; r0 += 4) {  // 4 ranks' loads in flight
 #pragma unroll
           for (int u = 0; u < 4; ++u)
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
+            for (int j = 0; j < NQ; ++j)
               x[u][j] = (r0 + u >= S) ? make_float4(0.f, 0.f, 0.f, 0.f)
                         : vcl ? __ldcg(reinterpret_cast<const float4*>(gpart + static_cast<long long>(r0 + u) * a.bn * kTileM +
-                                                                      part_index(c0, j, row_local)))
-                              : ld_dsmem_f4(dsmem_addr(part + part_index(c0, j, row_local), r0 + u));
+                                                                      part_index(cbase, q0 + j, row_local)))
+                              : ld_dsmem_f4(dsmem_addr(part + part_index(cbase, q0 + j, row_local), r0 + u));
 #pragma unroll
           for (int u = 0; u < 4; ++u)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < NQ; ++j) {
               v[4 * j] += x[u][j].x;
               v[4 * j + 1] += x[u][j].y;
               v[4 * j + 2] += x[u][j].z;
               v[4 * j + 3] += x[u][j].w;
             }
         }
+      };
+      const int nmine = (a.bn / 16 - static_cast<int>(rank) + static_cast<int>(S) - 1) / static_cast<int>(S);
+      if (!W4 && nmine == 1) {
+        // one 16-column chunk for this rank: each epilogue group takes 8 columns
+        const int c0 = static_cast<int>(rank) * 16 + 8 * epi_grp();
+        float v[8];
+        reduce_cols(c0, 2 * epi_grp(), v);
         if (threadIdx.x == 64) SUN_STAMP(10);
-        epi_chunk<EPI>(a, t_first, row_local, c0, v, epi);
+        epi_chunk<EPI, 8>(a, t_first, row_local, c0, v, epi);
         if (threadIdx.x == 64) SUN_STAMP(11);
+      } else {
+        const int ng = W4 ? 1 : 2;  // the rank's chunks alternate between the epilogue groups
+        for (int c0 = static_cast<int>(rank + S * epi_grp()) * 16; c0 < a.bn; c0 += static_cast<int>(S * ng) * 16) {
+          float v[16];
+          reduce_cols(c0, 0, v);
+          if (threadIdx.x == 64) SUN_STAMP(10);
+          epi_chunk<EPI>(a, t_first, row_local, c0, v, epi);
+          if (threadIdx.x == 64) SUN_STAMP(11);
+        }
       }
     }
     if (vcl) {  // the last of the tile's 2S arrivals rearms the counter for the next launch
