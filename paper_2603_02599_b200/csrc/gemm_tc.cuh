@@ -28,6 +28,8 @@
 // Replaces the weight term `decoder_weight_bytes / (mbu * hbm_bandwidth)` of
 // the reference's step price (poolsim costmodel.py:101-113) with real work.
 #pragma once
+#include <type_traits>
+
 #include "sun_common.cuh"
 
 namespace sun {
@@ -180,14 +182,18 @@ __host__ __device__ inline int w4_abufs(int bn) {
 SUN_DEVICE int epi_grp() { return threadIdx.x >= 224 ? 1 : 0; }
 SUN_DEVICE bool epi_lead_warp() { return static_cast<int>(threadIdx.x >> 5) == (epi_grp() ? 7 : 2); }
 SUN_DEVICE bool epi_lead_thread() { return threadIdx.x == (epi_grp() ? 224u : 64u); }
-SUN_DEVICE void epi_bar() { asm volatile("bar.sync %0, 128;" ::"r"(1 + 2 * epi_grp()) : "memory"); }
+SUN_DEVICE void epi_bar() {  // immediate ids keep the kernel's named-barrier count small
+  if (epi_grp()) asm volatile("bar.sync 3, 128;" ::: "memory");
+  else asm volatile("bar.sync 1, 128;" ::: "memory");
+}
 SUN_DEVICE int* epi_meta(float* epi) { return reinterpret_cast<int*>(epi); }
 SUN_DEVICE float* epi_stage(float* epi) {
   return reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(epi) + 3072 + epi_grp() * kEpiGroupBytes);
 }
 
 template <int EPI, int NC = 16>  // NC: columns in this chunk (16, or 8 for a half chunk)
-SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, float (&v)[NC], float* epi) {
+SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, float (&v)[NC], float* epi,
+                          const float* pre0 = nullptr, const float* pre1 = nullptr) {
   const int row = m_tile * kTileM + row_local;
   const int B = a.batch;
   float* stage_f32 = epi_stage(epi);
@@ -206,8 +212,8 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
         float* base = a.out_f32 + static_cast<long long>(c0) * a.ldo + row;
         float old[NC];
 #pragma unroll
-        for (int j = 0; j < NC; ++j) old[j] = (in && c0 + j < B) ? base[j * a.ldo] : 0.f;
-        const float g = in ? __bfloat162float(a.norm_w[row]) : 0.f;
+        for (int j = 0; j < NC; ++j) old[j] = pre0 ? pre0[j] : ((in && c0 + j < B) ? base[j * a.ldo] : 0.f);
+        const float g = pre1 ? pre1[0] : (in ? __bfloat162float(a.norm_w[row]) : 0.f);
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
           nw[j] = old[j] + v[j];
@@ -245,7 +251,7 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
         // issue all 16 residual loads before any store (one memory round trip)
         float old[NC];
 #pragma unroll
-        for (int j = 0; j < NC; ++j) old[j] = (c0 + j < B) ? base[j * a.ldo] : 0.f;
+        for (int j = 0; j < NC; ++j) old[j] = pre0 ? pre0[j] : ((c0 + j < B) ? base[j * a.ldo] : 0.f);
 #pragma unroll
         for (int j = 0; j < NC; ++j)
           if (c0 + j < B) base[j * a.ldo] = old[j] + v[j];
@@ -345,8 +351,8 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
         for (int j = 0; j < NC; ++j) {
           const int pos = meta[(c0 + j) & 255];
           const bool ok = !is_v && (c0 + j < B);
-          cs[j] = ok ? a.rope_cos[static_cast<long long>(pos) * half + fi] : 1.f;
-          sn[j] = ok ? a.rope_sin[static_cast<long long>(pos) * half + fi] : 0.f;
+          cs[j] = pre0 ? pre0[j] : (ok ? a.rope_cos[static_cast<long long>(pos) * half + fi] : 1.f);
+          sn[j] = pre1 ? pre1[j] : (ok ? a.rope_sin[static_cast<long long>(pos) * half + fi] : 0.f);
           pv[j] = stage_f32[j * kTileM + partner];
         }
         const bool lo_half = i < half;
@@ -423,6 +429,42 @@ SUN_DEVICE void direct_epilogue(const GemmArgs& a, int tile, uint32_t taddr, flo
   for (int c0 = 16 * epi_grp(); c0 < a.bn; c0 += 16 * ngroups) {
     tmem_ld16(taddr + c0, v);
     epi_chunk<EPI>(a, tile, row_local, c0, v, epi);
+  }
+}
+
+// Split-K epilogue inputs that do not depend on this GEMM's result (previous
+// residual + next-norm gain; RoPE cos/sin of the columns), loaded by the epilogue
+// warps while the main loop still runs: under a saturated HBM a global round
+// trip costs ~2 us, which otherwise sat between the reduction and the stores.
+struct EpiPreNone {};
+struct EpiPre {
+  float p0[16], p1[16];
+  int c0 = -1;
+};
+template <int EPI>
+SUN_DEVICE void epi_preload(const GemmArgs& a, int m_tile, int row_local, int c0, int nc, float* epi, EpiPre& pr) {
+  const int row = m_tile * kTileM + row_local;
+  const int B = a.batch;
+  pr.c0 = c0;
+  if constexpr (EPI == EPI_RESID_ADD) {
+    const bool in = row < a.n_out;
+    const float* base = a.out_f32 + static_cast<long long>(c0) * a.ldo + row;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) pr.p0[j] = (j < nc && in && c0 + j < B) ? base[j * a.ldo] : 0.f;
+    pr.p1[0] = (a.norm_w != nullptr && in) ? __bfloat162float(a.norm_w[row]) : 0.f;
+  } else if constexpr (EPI == EPI_QKV_ROPE) {
+    const int d = a.head_dim, half = d >> 1, qd = a.n_q_heads * d, kd = a.n_kv_heads * d;
+    const int i = row % d;
+    const int fi = i < half ? i : i - half;
+    const bool is_v = row >= qd + kd;
+    const int* meta = epi_meta(epi);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int pos = meta[(c0 + j) & 255];
+      const bool ok = j < nc && row < a.n_out && !is_v && (c0 + j < B);
+      pr.p0[j] = ok ? a.rope_cos[static_cast<long long>(pos) * half + fi] : 1.f;
+      pr.p1[j] = ok ? a.rope_sin[static_cast<long long>(pos) * half + fi] : 0.f;
+    }
   }
 }
 
@@ -643,6 +685,8 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(skbar + 1);
 
   const int warp = warp_id_sync();
+  constexpr bool kPre = !W4 && (EPI == EPI_RESID_ADD || EPI == EPI_QKV_ROPE);
+  std::conditional_t<kPre, EpiPre, EpiPreNone> pre;  // this epilogue group's first split-K chunk
   const uint32_t S = a.splits > 1 ? static_cast<uint32_t>(a.splits) : 1u;
   const bool clustered = S > 1;  // split-K over S CTAs (hardware cluster or virtual)
   const bool vcl = clustered && a.vcluster;
@@ -880,6 +924,15 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
     pdl_wait();
     if (warp < 6) load_qkv_meta<EPI>(a, epi);
     if constexpr (!W4) asm volatile("bar.sync 4, 256;" ::: "memory");  // group B waits for the meta
+    if constexpr (kPre) {
+      if (clustered) {  // the first chunk this group will handle after the reduction
+        const int rl = (warp & 3) * 32 + (threadIdx.x & 31);
+        const int nmine = (a.bn / 16 - static_cast<int>(rank) + static_cast<int>(S) - 1) / static_cast<int>(S);
+        if (nmine == 1) epi_preload<EPI>(a, t_first, rl, static_cast<int>(rank) * 16 + 8 * epi_grp(), 8, epi, pre);
+        else if (static_cast<int>(rank + S * epi_grp()) * 16 < a.bn)
+          epi_preload<EPI>(a, t_first, rl, static_cast<int>(rank + S * epi_grp()) * 16, 16, epi, pre);
+      }
+    }
     const int q = warp & 3;
     const int row_local = q * 32 + (threadIdx.x & 31);
     for (int seg = 0; seg < nseg; ++seg) {
@@ -1009,7 +1062,8 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
         float v[8];
         reduce_cols(c0, 2 * epi_grp(), v);
         if (threadIdx.x == 64) SUN_STAMP(10);
-        epi_chunk<EPI, 8>(a, t_first, row_local, c0, v, epi);
+        if constexpr (kPre) epi_chunk<EPI, 8>(a, t_first, row_local, c0, v, epi, pre.p0, pre.p1);
+        else epi_chunk<EPI, 8>(a, t_first, row_local, c0, v, epi);
         if (threadIdx.x == 64) SUN_STAMP(11);
       } else {
         const int ng = W4 ? 1 : 2;  // the rank's chunks alternate between the epilogue groups
@@ -1017,7 +1071,12 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
           float v[16];
           reduce_cols(c0, 0, v);
           if (threadIdx.x == 64) SUN_STAMP(10);
-          epi_chunk<EPI>(a, t_first, row_local, c0, v, epi);
+          if constexpr (kPre) {
+            if (c0 == pre.c0) epi_chunk<EPI>(a, t_first, row_local, c0, v, epi, pre.p0, pre.p1);
+            else epi_chunk<EPI>(a, t_first, row_local, c0, v, epi);
+          } else {
+            epi_chunk<EPI>(a, t_first, row_local, c0, v, epi);
+          }
           if (threadIdx.x == 64) SUN_STAMP(11);
         }
       }

@@ -74,7 +74,7 @@ if args.stamp >= 0:
     rel = (sv - t0) / 1e3
     print(f"launch {args.stamp} ({lab[args.stamp]}): {len(sv)} CTAs; phase times relative to step start (us)")
     nm = ["start", "setup", "first_stage", "last_mma", "first_acc", "epi_done", "exit", "-", "parked", "sync1",
-          "reduced", "epi_chunk"]
+          "reduced", "epi_chunk", "qkv_bar1", "qkv_bar2", "qkv_loads"]
     for i, name in enumerate(nm):
         if name == "-" or (sv[:, i] == 0).all():
             continue
