@@ -50,10 +50,16 @@ SUN_DEVICE void store_attn_out(const AttnArgs& a, int b, int head, int dim, floa
     a.out[static_cast<long long>(b) * a.ld_out + head * D + dim] = o;
 }
 
+#ifndef SUN_ATTN_D64_STAGES
+#define SUN_ATTN_D64_STAGES 2
+#endif
+#ifndef SUN_ATTN_D128_STAGES
+#define SUN_ATTN_D128_STAGES 3
+#endif
 template <int D>
 struct AttnCfg {
   static constexpr int kWarps = 4;
-  static constexpr int kStages = (D == 128) ? 3 : 4;
+  static constexpr int kStages = (D == 128) ? SUN_ATTN_D128_STAGES : SUN_ATTN_D64_STAGES;
   static constexpr int kBoxes = D / 64;                          // 128 B boxes per row
   static constexpr uint32_t kTileBytes = kPageTokens * D * 2;    // K (or V) of one page
   static constexpr uint32_t kStageBytes = 2 * kTileBytes;
