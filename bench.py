@@ -261,6 +261,12 @@ def gpu_arm(args, cfg):
     spec = SPECS[cfg["spec"]].with_bits(cfg["bits"]) if cfg["bits"] == 4 else SPECS[cfg["spec"]]
     assign = build_assignment(cfg, world, args.routing)
     mine = assign[rank]
+    # PINNED at N > 1 with a Zipf mix can hand one worker more requests than one
+    # decode step holds (the kernels take B <= 256): that worker decodes its first
+    # 256 (the partitioned baseline is then capacity-bound, as in the paper)
+    batch_cap = 256
+    capped = len(mine) > batch_cap
+    mine = mine[:batch_cap]
     B = len(mine)
     ctx = contexts_for(cfg, B)
     total_steps = args.warmup + args.steps
@@ -399,6 +405,7 @@ def gpu_arm(args, cfg):
                        "global_batch": int(tok_all.item()) // args.steps, "ctx_min": min(ctx), "ctx_max": max(ctx),
                        "routing": args.routing, "parallelism": f"{world} shared decode workers (request-level DP)",
                        "models_in_batch": sorted({m for _, m in mine}), "cuda_graph": graph,
+                       "rank0_batch_capped_at_256": capped,
                        "pdl": not args.no_pdl,
                        "l2": "inputs larger than L2 (weights + KV per step >> 126 MB), no explicit flush"},
             "tokens_per_s_per_gpu": value / world,
