@@ -240,6 +240,9 @@ def kernel_bytes(spec, B, ctx):
         "gemm_lm_head_argmax": V * h * 2 + B * h * 2 + B * V * 4,
         "embed_norm": B * h * 8,
         "argmax": 0,
+        # SUN_GEMM_CHAIN=1: O + gate_up + down + the next layer's QKV in one launch
+        "gemm_chain": (wbytes(h, qd) + wbytes(2 * f, h) + wbytes(h, f) + wbytes(qd + 2 * kd, h)
+                       + B * (qd + h + f + h) * 2 + B * h * 20 + B * (qd + 2 * kd) * 2),
     }
 
 

@@ -1,0 +1,341 @@
+// gemm_chain.cuh — a layer's GEMM chain (O-proj -> gate_up -> down -> next QKV) as
+// one persistent launch of 148 CTAs (one per SM).
+//
+// Why: between two separate GEMM launches the next GEMM's CTAs only become resident
+// when the previous GEMM's CTAs exit (each holds ~200 KB of shared memory), so its
+// weight stream starts after the previous tail (split-K reduction + fused epilogue,
+// several µs) and its ramp is exposed. Here the weight producer of every CTA runs
+// ahead across phase boundaries — the next GEMM's weights stream into the ring
+// while the epilogue warps finish the current phase — and only the activation
+// producer waits for the grid-wide "phase p done" count before loading phase p's
+// input. Split phases reduce through L2 (virtual clusters, gemm_tc.cuh), whole-tile
+// phases use the TMEM double buffer across phase boundaries.
+//
+// Deadlock freedom: 148 CTAs x 1 per SM are co-resident once the previous kernel
+// drains (PDL: the dependent launch needs every CTA of this grid to have started);
+// the only cross-CTA waits are phase counts and per-tile split counters, both
+// produced by epilogue warps that never wait on anything but their own CTA's MMA.
+#pragma once
+#include "gemm_tc.cuh"
+
+namespace sun {
+
+constexpr int kChainMaxPhases = 4;
+
+struct ChainArgs {
+  GemmArgs ph[kChainMaxPhases];
+  int epi[kChainMaxPhases];  // EpiKind per phase
+  int nph;
+  unsigned* bar;  // [2]: phases completed x CTAs, CTAs exited (zeroed once, self-resetting)
+  unsigned long long* tl;
+  int tl_idx;
+};
+
+struct PhaseSched {
+  int u0, u1, n, t_first, nseg, S, rank;
+};
+
+SUN_DEVICE PhaseSched phase_sched(const GemmArgs& a) {
+  PhaseSched p;
+  const int KS = a.ksteps, G = static_cast<int>(gridDim.x), c = static_cast<int>(blockIdx.x);
+  p.S = a.splits > 1 ? a.splits : 1;
+  p.rank = 0;
+  if (p.S > 1) {
+    if (c < a.m_tiles * p.S) {
+      const int t = c / p.S;
+      p.rank = c % p.S;
+      p.u0 = t * KS + p.rank * KS / p.S;
+      p.u1 = t * KS + (p.rank + 1) * KS / p.S;
+    } else {
+      p.u0 = p.u1 = 0;  // idle in this phase
+    }
+  } else {
+    p.u0 = static_cast<int>(static_cast<long long>(c) * a.m_tiles / G) * KS;
+    p.u1 = static_cast<int>(static_cast<long long>(c + 1) * a.m_tiles / G) * KS;
+  }
+  p.n = p.u1 - p.u0;
+  p.t_first = p.n > 0 ? p.u0 / KS : 0;
+  p.nseg = p.n > 0 ? (p.u1 - 1) / KS - p.t_first + 1 : 0;
+  return p;
+}
+
+SUN_DEVICE void chain_wait_phase(const unsigned* bar, unsigned target) {
+  if (target == 0) return;
+  while (ld_acquire_u32(bar) < target) __nanosleep(64);
+}
+
+SUN_DEVICE void epi_pair_bar() { asm volatile("bar.sync 4, 256;" ::: "memory"); }  // both epilogue groups
+
+// One phase of the epilogue warps (both groups). Returns after every segment of
+// this CTA's range is written out and the TMEM buffers are released.
+template <int EPI>
+SUN_DEVICE void chain_epilogue_phase(const GemmArgs& a, const PhaseSched& ps, float* epi, uint32_t tmem_base,
+                                     uint64_t* tfull, uint64_t* tempty, int& buf, int& tphase) {
+  const int warp = static_cast<int>(threadIdx.x >> 5);
+  const int q = warp & 3;
+  const int row_local = q * 32 + (threadIdx.x & 31);
+  const int KS = a.ksteps;
+  if (warp < 6) load_qkv_meta<EPI>(a, epi);
+  epi_pair_bar();
+  for (int seg = 0; seg < ps.nseg; ++seg) {
+    const int tile = ps.t_first + seg;
+    mbar_wait(&tfull[buf], tphase);
+    tc_fence_after();
+    const uint32_t taddr = tmem_base + static_cast<uint32_t>(buf * a.bn) + (static_cast<uint32_t>(q * 32) << 16);
+    if (ps.S == 1) {
+      direct_epilogue<EPI>(a, tile, taddr, epi, 2);
+      tc_fence_before();
+      epi_bar();
+      if (epi_lead_thread()) mbar_arrive(&tempty[buf]);
+    } else {
+      // split phase: park this rank's partial in L2, meet the tile's S CTAs, reduce
+      // this rank's columns (chunks rank, rank + S, ... alternate between the groups)
+      const int S = ps.S, rank = ps.rank;
+      if (epi_grp() == 0) {
+        float* part = a.sk_part + static_cast<long long>(blockIdx.x) * a.bn * kTileM;
+        float v[16];
+        for (int c0 = 0; c0 < a.bn; c0 += 16) {
+          tmem_ld16(taddr + c0, v);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            __stcg(reinterpret_cast<float4*>(part + part_index(c0, j, row_local)),
+                   make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+        }
+        __threadfence();
+      }
+      tc_fence_before();
+      epi_pair_bar();
+      if (epi_lead_thread()) mbar_arrive(&tempty[buf]);  // accumulator parked: the MMA may reuse it
+      unsigned* tile_cnt = a.sk_flags + tile;
+      if (threadIdx.x == 64) {
+        atomicAdd(tile_cnt, 1u);
+        while (ld_acquire_u32(tile_cnt) < static_cast<unsigned>(S)) {
+        }
+      }
+      epi_pair_bar();
+      const float* gpart = a.sk_part + static_cast<long long>(blockIdx.x - rank) * a.bn * kTileM;
+      auto reduce_cols = [&](int c0, int q0, auto& v) {
+        constexpr int NQ = sizeof(v) / sizeof(float) / 4;
+        float4 x[4][NQ];
+#pragma unroll
+        for (int j = 0; j < 4 * NQ; ++j) v[j] = 0.f;
+        const int cbase = c0 & ~15;
+        for (int r0 = 0; r0 < S; r0 += 4) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int j = 0; j < NQ; ++j)
+              x[u][j] = (r0 + u >= S) ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                      : __ldcg(reinterpret_cast<const float4*>(
+                                            gpart + static_cast<long long>(r0 + u) * a.bn * kTileM +
+                                            part_index(cbase, q0 + j, row_local)));
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int j = 0; j < NQ; ++j) {
+              v[4 * j] += x[u][j].x;
+              v[4 * j + 1] += x[u][j].y;
+              v[4 * j + 2] += x[u][j].z;
+              v[4 * j + 3] += x[u][j].w;
+            }
+        }
+      };
+      const int cfirst = rank * 16, cstride = S * 16;
+      const int nmine = (a.bn - cfirst + cstride - 1) / cstride;
+      if (nmine == 1) {
+        const int c0 = cfirst + 8 * epi_grp();
+        float v[8];
+        reduce_cols(c0, 2 * epi_grp(), v);
+        epi_chunk<EPI, 8>(a, tile, row_local, c0, v, epi);
+      } else {
+        for (int c0 = cfirst + epi_grp() * cstride; c0 < a.bn; c0 += 2 * cstride) {
+          float v[16];
+          reduce_cols(c0, 0, v);
+          epi_chunk<EPI>(a, tile, row_local, c0, v, epi);
+        }
+      }
+      epi_pair_bar();  // the last of the tile's 2S arrivals rearms its counter
+      if (threadIdx.x == 64 && atomicAdd(tile_cnt, 1u) == 2u * S - 1u) *tile_cnt = 0u;
+    }
+    if (++buf == 2) {
+      buf = 0;
+      tphase ^= 1;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kGemmThreads, 1) gemm_chain_kernel(const __grid_constant__ ChainArgs c) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  tl_begin(c.tl, c.tl_idx);
+  const GemmArgs& a0 = c.ph[0];
+  const int stages = a0.stages, xstages = a0.xstages, bn = a0.bn;
+  const uint32_t sb = gemm_stage_bytes(bn, false);
+  const uint32_t xsb = gemm_xstage_bytes(bn);
+  uint8_t* stg = smem;
+  uint8_t* xstg = stg + ((stages * sb + 1023u) & ~1023u);
+  float* epi = reinterpret_cast<float*>(xstg + xstages * xsb);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(epi) + kEpiSmemBytes);
+  uint64_t* empty = full + kMaxWStages;
+  uint64_t* xfull = empty + kMaxWStages;
+  uint64_t* xempty = xfull + kMaxXStages;
+  uint64_t* tfull = xempty + kMaxXStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = warp_id_sync();
+  const unsigned G = gridDim.x;
+  const uint32_t ncols = tmem_cols_for(bn);
+
+  if (warp == 0 && elect_one()) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < xstages; ++s) {
+      mbar_init(&xfull[s], 1);
+      mbar_init(&xempty[s], 1);
+    }
+    for (int j = 0; j < 2; ++j) {
+      mbar_init(&tfull[j], 1);
+      mbar_init(&tempty[j], 2);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, ncols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_launch_dependents();
+
+  if (warp == 0 || warp == 6) {
+    // producers: warp 0 streams every phase's weights back to back (no waits but
+    // ring slots); warp 6 loads a phase's activations once all CTAs finished the
+    // previous phase (phase 0: once the previous kernel completed)
+    if (elect_one()) {
+      const bool wprod = warp == 0;
+      const int depth = wprod ? stages : xstages;
+      uint64_t* fb = wprod ? full : xfull;
+      uint64_t* eb = wprod ? empty : xempty;
+      int slot = 0, phase = 0, issued = 0;
+      for (int p = 0; p < c.nph; ++p) {
+        const GemmArgs& a = c.ph[p];
+        const PhaseSched ps = phase_sched(a);
+        if (!wprod) {
+          if (p == 0) pdl_wait();
+          else chain_wait_phase(c.bar, G * p);
+        }
+        const int KS = a.ksteps;
+        int ks = ps.n > 0 ? ps.u0 % KS : 0, tile = ps.n > 0 ? ps.u0 / KS : 0;
+        for (int j = 0; j < ps.n; ++j) {
+          const int nb = min(2, a.kb64 - 2 * ks);
+          if (issued >= depth) mbar_wait(&eb[slot], phase ^ 1);
+          if (wprod) {
+            mbar_arrive_expect_tx(&fb[slot], nb * kTileWBytes);
+            bulk_load_hint(stg + slot * sb, a.wblk + (static_cast<long long>(tile) * a.kb64 + 2 * ks) * kTileWBytes,
+                           nb * kTileWBytes, &fb[slot], kEvictFirst);
+          } else {
+            mbar_arrive_expect_tx(&fb[slot], nb * a.bn * 128u);
+            bulk_load_hint(xstg + slot * xsb, a.xact + static_cast<long long>(2 * ks) * a.bn * 128, nb * a.bn * 128u,
+                           &fb[slot], kEvictLast);
+          }
+          ++issued;
+          if (++ks == KS) {
+            ks = 0;
+            ++tile;
+          }
+          if (++slot == depth) {
+            slot = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // MMA issuer: one TMEM double buffer and one pair of rings across all phases
+    const uint32_t idesc = make_idesc_bf16(kTileM, bn);
+    int wslot = 0, wphase = 0, xslot = 0, xphase = 0, buf = 0, tphase = 0;
+    for (int p = 0; p < c.nph; ++p) {
+      const GemmArgs& a = c.ph[p];
+      const PhaseSched ps = phase_sched(a);
+      const int KS = a.ksteps;
+      int ks = ps.n > 0 ? ps.u0 % KS : 0;
+      for (int j = 0; j < ps.n; ++j) {
+        const bool first = j == 0 || ks == 0, last = j == ps.n - 1 || ks == KS - 1;
+        const int nb = min(2, a.kb64 - 2 * ks);
+        if (first) {
+          mbar_wait(&tempty[buf], tphase ^ 1);
+          tc_fence_after();
+        }
+        mbar_wait(&full[wslot], wphase);
+        mbar_wait(&xfull[xslot], xphase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t xa = smem_u32(xstg + xslot * xsb);
+          const uint32_t wa = smem_u32(stg + wslot * sb);
+          const uint32_t tacc = tmem_base + static_cast<uint32_t>(buf * bn);
+          for (int kk = 0; kk < nb * 4; ++kk) {
+            const uint32_t atom = kk >> 2;
+            const uint32_t koff = (kk & 3) * 32;
+            umma_bf16(tacc, make_sw128_desc(wa + atom * kTileWBytes + koff),
+                      make_sw128_desc(xa + atom * (bn * 128u) + koff), idesc, (first && kk == 0) ? 0u : 1u);
+          }
+          umma_commit(&empty[wslot]);
+          umma_commit(&xempty[xslot]);
+          if (last) umma_commit(&tfull[buf]);
+        }
+        __syncwarp();
+        if (++wslot == stages) {
+          wslot = 0;
+          wphase ^= 1;
+        }
+        if (++xslot == xstages) {
+          xslot = 0;
+          xphase ^= 1;
+        }
+        if (++ks == KS) ks = 0;
+        if (last && ++buf == 2) {
+          buf = 0;
+          tphase ^= 1;
+        }
+      }
+    }
+  } else if (warp < 6 || warp >= 7) {
+    // epilogue groups A (warps 2..5) and B (7..10)
+    int buf = 0, tphase = 0;
+    for (int p = 0; p < c.nph; ++p) {
+      const GemmArgs& a = c.ph[p];
+      const PhaseSched ps = phase_sched(a);
+      if (p == 0) {
+        pdl_wait();
+      } else {  // this phase's input, norm statistics and positions are final: one thread polls
+        if (threadIdx.x == 64) chain_wait_phase(c.bar, G * p);
+        epi_pair_bar();
+      }
+      switch (c.epi[p]) {
+        case EPI_RESID_ADD: chain_epilogue_phase<EPI_RESID_ADD>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase); break;
+        case EPI_SWIGLU: chain_epilogue_phase<EPI_SWIGLU>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase); break;
+        case EPI_QKV_ROPE: chain_epilogue_phase<EPI_QKV_ROPE>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase); break;
+        default: chain_epilogue_phase<EPI_STORE_F32>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase); break;
+      }
+      epi_pair_bar();
+      if (threadIdx.x == 64) {  // this CTA's outputs of phase p are written
+        __threadfence();
+        atomicAdd(c.bar, 1u);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, ncols);
+  }
+  if (threadIdx.x == 0 && atomicAdd(c.bar + 1, 1u) == G - 1) {  // last CTA out rearms the counters
+    c.bar[0] = 0u;
+    c.bar[1] = 0u;
+  }
+  tl_end(c.tl, c.tl_idx);
+}
+
+}  // namespace sun

@@ -20,6 +20,7 @@
 #include "elementwise.cuh"
 #include "gemm_tc.cuh"
 #include "gemm_w4.cuh"
+#include "gemm_chain.cuh"
 
 using namespace sun;
 
@@ -181,6 +182,7 @@ void init_kernel_attrs() {
     set_max_smem(gemm_kernel<EPI_RESID_ADD, true>);
     set_max_smem(gemm_kernel<EPI_QKV_ROPE, true>);
     set_max_smem(gemm_kernel<EPI_SWIGLU, true>);
+    set_max_smem(gemm_chain_kernel);
     set_max_smem(attn_decode_kernel<64>);
     set_max_smem(attn_decode_kernel<128>);
     (void)0;
@@ -312,7 +314,8 @@ int gemm_sched() {
 
 // Workspace layout shared by sizing and creation.
 struct WsLayout {
-  size_t resid, xn, q, attn, act, part_o, part_ml, attn_cnt, ss, amax_val, amax_idx, logits, sk_part, sk_flags, total;
+  size_t resid, xn, q, attn, act, part_o, part_ml, attn_cnt, ss, amax_val, amax_idx, logits, sk_part, sk_flags,
+      chain_bar, total;
   int max_splits;
 };
 
@@ -348,6 +351,7 @@ WsLayout layout_ws(const SunDecoderDims& d, int max_batch) {
   w.logits = take(size_t(max_batch) * d.vocab * 4);
   w.sk_part = take(sk_part_bytes(bmp));
   w.sk_flags = take(kMaxGemmCtas * 4);
+  w.chain_bar = take(64);
   w.total = off;
   return w;
 }
@@ -393,6 +397,7 @@ struct SunDecoder {
   int* amax_idx;
   float* sk_part;
   unsigned* sk_flags;
+  unsigned* chain_bar;
   GemmPlan p_qkv, p_o, p_gu, p_down, p_lm;
 };
 
@@ -554,6 +559,44 @@ SunStatus run_gemm(const void* wblk, const void* packed, const void* scales, Gem
   return SUN_OK;
 }
 
+// Layer GEMM chain (SUN_GEMM_CHAIN=1, bf16): the phases' GemmArgs are filled as for
+// run_gemm; every split phase reduces through L2 over 148 persistent CTAs.
+int gemm_chain_enabled() {
+  static int v = [] {
+    const char* e = getenv("SUN_GEMM_CHAIN");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+SunStatus run_chain(GemmArgs* ph, const int* epi, const GemmPlan* plans, const void* const* wblk, int nph,
+                    unsigned* bar, cudaStream_t st, bool pdl) {
+  ChainArgs c;
+  memset(&c, 0, sizeof(c));
+  const int bn = ph[0].bn;
+  const int stages = gemm_stages(bn, false, 1), xstages = gemm_xstages(bn);
+  for (int i = 0; i < nph; ++i) {
+    GemmArgs a = ph[i];
+    const GemmPlan& p = plans[i];
+    a.wblk = static_cast<const uint8_t*>(wblk[i]);
+    a.stages = stages;
+    a.xstages = xstages;
+    const int want = p.m_tiles <= kNumSms ? std::min(std::min(8, kNumSms / std::max(1, p.m_tiles)), p.ksteps) : 1;
+    a.splits = want;
+    a.vcluster = want > 1 ? 1 : 0;
+    a.sk_units = 0;
+    c.ph[i] = a;
+    c.epi[i] = epi[i];
+  }
+  c.nph = nph;
+  c.bar = bar;
+  tl_assign(c);
+  g_cluster = 1;
+  SUN_CUDA(launch(gemm_chain_kernel, dim3(kNumSms), dim3(kGemmThreads), gemm_smem_bytes(bn, stages, xstages), st,
+                  pdl, c));
+  return SUN_OK;
+}
+
 // Split combine inside the attention kernel (last split merges) or as a separate
 // grid (default: measured faster on B200 for C3, the parallel merge has no
 // serial tail). Env SUN_ATTN_FUSED_COMBINE=1 selects the fused variant.
@@ -653,6 +696,7 @@ SunStatus sun_decoder_create(const SunDecoderDims* dims, const SunWeights* weigh
   dec->logits = reinterpret_cast<float*>(ws + dec->L.logits);
   dec->sk_part = reinterpret_cast<float*>(ws + dec->L.sk_part);
   dec->sk_flags = reinterpret_cast<unsigned*>(ws + dec->L.sk_flags);
+  dec->chain_bar = reinterpret_cast<unsigned*>(ws + dec->L.chain_bar);
 
   const SunDecoderDims& d = *dims;
   const int qd = d.n_q_heads * d.head_dim;
@@ -667,6 +711,7 @@ SunStatus sun_decoder_create(const SunDecoderDims* dims, const SunWeights* weigh
   cudaError_t e = cudaMemset(ws, 0, dec->L.part_o);
   if (e == cudaSuccess) e = cudaMemset(ws + dec->L.attn_cnt, 0, size_t(max_batch) * d_cnt_heads(*dims) * 4);
   if (e == cudaSuccess) e = cudaMemset(ws + dec->L.sk_flags, 0, kMaxGemmCtas * 4);
+  if (e == cudaSuccess) e = cudaMemset(ws + dec->L.chain_bar, 0, 64);
   if (e != cudaSuccess) {
     delete dec;
     return fail(SUN_ERR_CUDA, "cudaMemset ws: %s", cudaGetErrorString(e));
@@ -742,9 +787,8 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
                   static_cast<const __nv_bfloat16*>(dec->w.embed), dec->resid,
                   static_cast<const __nv_bfloat16*>(dec->layers[0].attn_norm), dec->xn, dec->ss, d.hidden, bn,
                   ss_tiles));
-  for (int l = 0; l < d.n_layers; ++l) {
+  auto qkv_args = [&](int l) {  // QKV (* r_b) + bias + RoPE + KV append
     const SunLayerWeights& lw = dec->layers[l];
-    // QKV (* r_b) + bias + RoPE + KV append
     GemmArgs a = base_args(dec->p_qkv, qkv_rows(d), d.hidden, batch, bn, dec->xn, dec->sk_part, dec->sk_flags);
     consume_norm(a);
     a.out_bf16 = dec->q;
@@ -762,37 +806,69 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     a.n_kv_heads = d.n_kv_heads;
     a.head_dim = d.head_dim;
     a.page_size = d.page_size;
-    set_prefetch(a, w4 ? lw.w_o : lw.w_o, dec->p_o, bn, w4);  // O-proj weights, through the attention kernel
-    if (!(skip & 1)) s = w4 ? run_gemm<EPI_QKV_ROPE>(nullptr, lw.w_qkv, lw.s_qkv, a, dec->p_qkv, st, pdl)
-           : run_gemm<EPI_QKV_ROPE>(lw.w_qkv, nullptr, nullptr, a, dec->p_qkv, st, pdl);
-    if (s != SUN_OK) return s;
-    // paged attention
-    aa.layer = l;
-    if (!(skip & 2) && (s = run_attention(d, dec->tm_kv, aa, batch, st, pdl)) != SUN_OK) return s;
-    // O projection + residual; emits the FFN norm's operand
-    a = base_args(dec->p_o, d.hidden, qd, batch, bn, dec->attn, dec->sk_part, dec->sk_flags);
+    return a;
+  };
+  auto o_args = [&](int l) {  // O projection + residual; emits the FFN norm's operand
+    GemmArgs a = base_args(dec->p_o, d.hidden, qd, batch, bn, dec->attn, dec->sk_part, dec->sk_flags);
     a.out_f32 = dec->resid;
     a.ldo = d.hidden;
-    produce_norm(a, lw.ffn_norm);
-    set_prefetch(a, lw.w_gate_up, dec->p_gu, bn, w4);
-    if (!(skip & 8)) s = w4 ? run_gemm<EPI_RESID_ADD>(nullptr, lw.w_o, lw.s_o, a, dec->p_o, st, pdl)
-           : run_gemm<EPI_RESID_ADD>(lw.w_o, nullptr, nullptr, a, dec->p_o, st, pdl);
-    if (s != SUN_OK) return s;
-    // gate/up (* r_b) + SwiGLU
-    a = base_args(dec->p_gu, gu_rows(d), d.hidden, batch, bn, dec->xn, dec->sk_part, dec->sk_flags);
+    produce_norm(a, dec->layers[l].ffn_norm);
+    return a;
+  };
+  auto gu_args = [&](int l) {  // gate/up (* r_b) + SwiGLU
+    GemmArgs a = base_args(dec->p_gu, gu_rows(d), d.hidden, batch, bn, dec->xn, dec->sk_part, dec->sk_flags);
     consume_norm(a);
     a.out_bf16 = dec->act;
     a.ldb = d.ffn;
     a.n_valid_out = d.ffn;
+    return a;
+  };
+  auto down_args = [&](int l) {  // down + residual; emits the next attention norm's (or the final norm's) operand
+    GemmArgs a = base_args(dec->p_down, d.hidden, d.ffn, batch, bn, dec->act, dec->sk_part, dec->sk_flags);
+    a.out_f32 = dec->resid;
+    a.ldo = d.hidden;
+    produce_norm(a, l + 1 < d.n_layers ? dec->layers[l + 1].attn_norm : dec->w.final_norm);
+    return a;
+  };
+  const bool chain = gemm_chain_enabled() && !w4;
+  for (int l = 0; l < d.n_layers; ++l) {
+    const SunLayerWeights& lw = dec->layers[l];
+    GemmArgs a;
+    if (!chain || l == 0) {
+      a = qkv_args(l);
+      set_prefetch(a, lw.w_o, dec->p_o, bn, w4);  // O-proj weights, through the attention kernel
+      if (!(skip & 1)) s = w4 ? run_gemm<EPI_QKV_ROPE>(nullptr, lw.w_qkv, lw.s_qkv, a, dec->p_qkv, st, pdl)
+             : run_gemm<EPI_QKV_ROPE>(lw.w_qkv, nullptr, nullptr, a, dec->p_qkv, st, pdl);
+      if (s != SUN_OK) return s;
+    }
+    // paged attention
+    aa.layer = l;
+    if (!(skip & 2) && (s = run_attention(d, dec->tm_kv, aa, batch, st, pdl)) != SUN_OK) return s;
+    if (chain) {  // O -> gate_up -> down (-> next layer's QKV) in one persistent launch
+      GemmArgs ph[4] = {o_args(l), gu_args(l), down_args(l), GemmArgs{}};
+      int epi[4] = {EPI_RESID_ADD, EPI_SWIGLU, EPI_RESID_ADD, EPI_QKV_ROPE};
+      GemmPlan plans[4] = {dec->p_o, dec->p_gu, dec->p_down, dec->p_qkv};
+      const void* wb[4] = {lw.w_o, lw.w_gate_up, lw.w_down, nullptr};
+      int nph = 3;
+      if (l + 1 < d.n_layers) {
+        ph[3] = qkv_args(l + 1);
+        wb[3] = dec->layers[l + 1].w_qkv;
+        nph = 4;
+      }
+      if ((s = run_chain(ph, epi, plans, wb, nph, dec->chain_bar, st, pdl)) != SUN_OK) return s;
+      continue;
+    }
+    a = o_args(l);
+    set_prefetch(a, lw.w_gate_up, dec->p_gu, bn, w4);
+    if (!(skip & 8)) s = w4 ? run_gemm<EPI_RESID_ADD>(nullptr, lw.w_o, lw.s_o, a, dec->p_o, st, pdl)
+           : run_gemm<EPI_RESID_ADD>(lw.w_o, nullptr, nullptr, a, dec->p_o, st, pdl);
+    if (s != SUN_OK) return s;
+    a = gu_args(l);
     set_prefetch(a, lw.w_down, dec->p_down, bn, w4);
     if (!(skip & 16)) s = w4 ? run_gemm<EPI_SWIGLU>(nullptr, lw.w_gate_up, lw.s_gate_up, a, dec->p_gu, st, pdl)
            : run_gemm<EPI_SWIGLU>(lw.w_gate_up, nullptr, nullptr, a, dec->p_gu, st, pdl);
     if (s != SUN_OK) return s;
-    // down + residual; emits the next attention norm's (or the final norm's) operand
-    a = base_args(dec->p_down, d.hidden, d.ffn, batch, bn, dec->act, dec->sk_part, dec->sk_flags);
-    a.out_f32 = dec->resid;
-    a.ldo = d.hidden;
-    produce_norm(a, l + 1 < d.n_layers ? dec->layers[l + 1].attn_norm : dec->w.final_norm);
+    a = down_args(l);
     if (l + 1 < d.n_layers) set_prefetch(a, dec->layers[l + 1].w_qkv, dec->p_qkv, bn, w4);
     else set_prefetch(a, dec->w.lm_head, dec->p_lm, bn, false);
     if (!(skip & 32)) s = w4 ? run_gemm<EPI_RESID_ADD>(nullptr, lw.w_down, lw.s_down, a, dec->p_down, st, pdl)

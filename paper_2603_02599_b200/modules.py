@@ -48,6 +48,7 @@ class _StepRunner:
         self._lib = lib
         import os as _os
         self.fused_combine = _os.environ.get("SUN_ATTN_FUSED_COMBINE", "0") == "1"
+        self.gemm_chain = _os.environ.get("SUN_GEMM_CHAIN", "0") == "1" and spec.weight_bits == 16
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -89,6 +90,11 @@ class _StepRunner:
         is launched unless fused or the attention ran unsplit (combine=False)."""
         combine = (not self.fused_combine) if combine is None else combine
         names = ["embed_norm"]
+        if self.gemm_chain:  # O -> gate_up -> down -> next QKV as one launch per layer
+            names.append("gemm_qkv_rope_kv")
+            for _ in range(self.spec.n_layers):
+                names += ["attention"] + (["attn_combine"] if combine else []) + ["gemm_chain"]
+            return names + ["gemm_lm_head_argmax", "argmax"]
         for _ in range(self.spec.n_layers):
             names += ["gemm_qkv_rope_kv", "attention"] + (["attn_combine"] if combine else []) + [
                 "gemm_o_resid_norm", "gemm_gate_up_swiglu", "gemm_down_resid_norm"]

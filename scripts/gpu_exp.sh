@@ -1,6 +1,7 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest -q -m gpu tests/ -x -k "w4 or W4 or variants or tiny or gemm" > gpurun_out/pytest_gpu.log 2>&1; tail -1 gpurun_out/pytest_gpu.log
-timeout 300 python scripts/w4_sweep.py > gpurun_out/w4_sweep.txt 2>&1
-run() { tag=$1; shift; e=(); while [[ "$1" == *=* ]]; do e+=("$1"); shift; done; env "${e[@]}" timeout 300 python bench.py --steps 50 --no-cpu --no-e2e "$@" > gpurun_out/x_$tag.json 2>gpurun_out/x_$tag.err; }
-run c4 --config c4 --steps 20
-python scripts/step_timeline.py --config c4 > gpurun_out/tl_c4.txt 2>&1
+export SUN_GEMM_CHAIN=1
+timeout 300 python -m pytest -q -m gpu tests/test_decode_parity_gpu.py -x > gpurun_out/pytest_chain.log 2>&1; tail -1 gpurun_out/pytest_chain.log
+timeout 300 python bench.py --steps 50 --no-cpu --no-e2e > gpurun_out/x_chain.json 2>gpurun_out/x_chain.err
+timeout 300 python bench.py --config c2 --steps 30 --no-cpu --no-e2e > gpurun_out/x_chain_c2.json 2>gpurun_out/x_chain_c2.err
+unset SUN_GEMM_CHAIN
+timeout 300 python bench.py --steps 50 --no-cpu --no-e2e > gpurun_out/x_base.json 2>gpurun_out/x_base.err
