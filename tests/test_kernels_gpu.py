@@ -58,13 +58,13 @@ def test_gemm_deterministic_stream_k(cuda):
         assert torch.equal(a, kernels.gemm_bf16(w, x, 64))
 
 
-@pytest.mark.parametrize("sched", ["0", "2", "vcl2", "novcl"])
+@pytest.mark.parametrize("sched", ["0", "2", "vcl2", "novcl", "chain"])
 def test_gemm_schedules_subprocess(sched):
     """The GEMM kernel tests and the end-to-end decode parity under the other
     schedules: 0 = cluster split-K / whole tiles only, 2 = stream-K on every
     GEMM whose partials fit (covers every fused epilogue with partial tiles),
     vcl2 = L2-reduced virtual clusters wherever a split pays, novcl = hardware
-    clusters only."""
+    clusters only, chain = the persistent per-layer GEMM chain kernel."""
     import os
     import subprocess
     import sys
@@ -75,6 +75,8 @@ def test_gemm_schedules_subprocess(sched):
         env["SUN_GEMM_VCLUSTER"] = "2"
     elif sched == "novcl":
         env["SUN_GEMM_VCLUSTER"] = "0"
+    elif sched == "chain":
+        env["SUN_GEMM_CHAIN"] = "1"
     else:
         env["SUN_GEMM_SCHED"] = sched
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", "(gemm or tiny) and not subprocess",
