@@ -14,6 +14,6 @@ timeout 900 python scripts/measure_step_grid.py --spec llama3.1-8b --bits 16 --o
 timeout 900 python scripts/measure_step_grid.py --spec llama3.1-8b --bits 4 --out gpurun_out/b200_steps_8b_w4.json > gpurun_out/grid4.log 2>&1
 for cfg in c3 c4; do
   python scripts/step_timeline.py --config $cfg > gpurun_out/tl_$cfg.txt 2>&1
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"gemm_kernel|attn_|embed_norm|argmax" -s 195 -c 195 --csv --log-file gpurun_out/launches_$cfg.csv python scripts/profile_step.py --config $cfg --steps 2 > gpurun_out/ncu1_$cfg.log 2>&1
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"gemm_kernel|attn_|embed_norm|argmax" -s 163 -c 163 --csv --log-file gpurun_out/launches_$cfg.csv python scripts/profile_step.py --config $cfg --steps 2 > gpurun_out/ncu1_$cfg.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gemm_kernel|attn_decode" -s 10 -c 5 -o gpurun_out/full_$cfg python scripts/profile_step.py --config $cfg --steps 1 > gpurun_out/ncu2_$cfg.log 2>&1
 done
