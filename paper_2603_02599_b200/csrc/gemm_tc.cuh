@@ -710,7 +710,11 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
   const int nseg = n > 0 ? (u1 - 1) / KS - t_first + 1 : 0;
   const uint32_t ncols = W4 ? 512u : tmem_cols_for(a.bn);
   const int nbuf = acc_buffers(a.bn, W4);
-  const int na = W4 ? w4_abufs(a.bn) : 1;  // A tile i at TMEM column 512 - 64 (i + 1)
+  // W4: each converter / MMA iteration covers kp K blocks (2 when bn <= 128: halves the
+  // per-block hand-off overhead that bounded the pipeline); A slot i = 64 kp TMEM
+  // columns ending at column 512 - 64 kp i
+  const int kp = (W4 && a.bn <= 128 && a.xk % 2 == 0 && a.wgroup % 2 == 0) ? 2 : 1;
+  const int na = W4 ? min(kW4MaxABufs, (512 - acc_buffers(a.bn, true) * a.bn) / (64 * kp)) : 1;
   const long long rows_pad = static_cast<long long>(a.m_tiles) * kTileM;
   if (threadIdx.x == 0) SUN_STAMP(0);
 
@@ -793,9 +797,10 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
     const uint32_t idesc = make_idesc_bf16(kTileM, a.bn);
     int ks = u0 % KS, seg_left = min(KS - ks, n);
     int xslot = 0, xphase = 0, xpos = 0, aslot = 0, aphase = 0, buf = 0, tphase = 0;
-    for (int j = 0; j < n; ++j) {
-      const bool first = j == 0 || ks == 0, last = seg_left == 1;
-      const bool xlast = xpos + 1 == a.xk || last;
+    for (int j = 0; j < n;) {
+      const int nbk = min(kp, seg_left);  // K blocks this iteration (never straddles a segment / stage)
+      const bool first = j == 0 || ks == 0, last = seg_left == nbk;
+      const bool xlast = xpos + nbk == a.xk || last;
       if (first) {
         mbar_wait(&tempty[buf], tphase ^ 1);
         tc_fence_after();
@@ -807,11 +812,13 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
       if (elect_one()) {
         const uint32_t xa = smem_u32(xstg + xslot * xsb) + static_cast<uint32_t>(xpos) * 2u * a.bn * 128u;
         const uint32_t tacc = tmem_base + static_cast<uint32_t>(buf * a.bn);
-        const uint32_t ta = tmem_base + static_cast<uint32_t>(512 - 64 * (aslot + 1));
+        const uint32_t ta = tmem_base + static_cast<uint32_t>(512 - 64 * kp * (aslot + 1));
+        for (int b = 0; b < nbk; ++b)
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          umma_bf16_ta(tacc, ta + kk * 8, make_sw128_desc(xa + (kk >> 2) * (a.bn * 128u) + (kk & 3) * 32), idesc,
-                       (first && kk == 0) ? 0u : 1u);
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16_ta(tacc, ta + b * 64 + kk * 8,
+                         make_sw128_desc(xa + (2 * b + (kk >> 2)) * (a.bn * 128u) + (kk & 3) * 32), idesc,
+                         (first && b == 0 && kk == 0) ? 0u : 1u);
         umma_commit(&dempty[aslot]);
         if (xlast) umma_commit(&xempty[xslot]);
         if (last) umma_commit(&tfull[buf]);
@@ -828,12 +835,14 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
           xphase ^= 1;
         }
       } else {
-        ++xpos;
+        xpos += nbk;
       }
-      ++ks;
-      if (--seg_left == 0) {
+      ks += nbk;
+      j += nbk;
+      seg_left -= nbk;
+      if (seg_left == 0) {
         ks = 0;
-        seg_left = min(KS, n - j - 1);
+        seg_left = min(KS, n - j);
         if (++buf == nbuf) {
           buf = 0;
           tphase ^= 1;
@@ -976,13 +985,16 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
     const int part = (warp - 6) >> 2;  // columns [16 * kW4Chunks * part, +16 * kW4Chunks) of each A tile
     const uint32_t lane_off = static_cast<uint32_t>(lg * 32) << 16;
     int ks = u0 % KS, seg_left = min(KS - ks, n);
-    int wslot = 0, wphase = 0, wpos = 0, aslot = 0, aphase = 0;
-    for (int j = 0; j < n; ++j) {
+    int wslot = 0, wphase = 0, wpos = 0, aslot = 0, aphase = 0, it = 0;
+    for (int j = 0; j < n;) {
+      const int nbk = min(kp, seg_left);
       if (wpos == 0) mbar_wait(&full[wslot], wphase);
-      const bool wlast = wpos + 1 == wg || seg_left == 1;
+      const bool wlast = wpos + nbk == wg || seg_left == nbk;
       const uint32_t st = smem_u32(stg + wslot * sb);
-      uint32_t o[16 * kW4Chunks];
-      w4_dequant_row(st + wpos * kW4PackedBytes, st + wg * kW4PackedBytes + wpos * 256u, row, part, o);
+      uint32_t o0[16 * kW4Chunks], o1[16 * kW4Chunks];
+      w4_dequant_row(st + wpos * kW4PackedBytes, st + wg * kW4PackedBytes + wpos * 256u, row, part, o0);
+      if (nbk == 2)
+        w4_dequant_row(st + (wpos + 1) * kW4PackedBytes, st + wg * kW4PackedBytes + (wpos + 1) * 256u, row, part, o1);
       if (wlast) {  // this warp is done reading the weight stage
         __syncwarp();
         if (elect_one()) mbar_arrive(&empty[wslot]);
@@ -992,11 +1004,13 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
           wphase ^= 1;
         }
       } else {
-        ++wpos;
+        wpos += nbk;
       }
-      if (j >= na) mbar_wait(&dempty[aslot], aphase ^ 1);  // MMA j-na done with this A tile
+      if (it >= na) mbar_wait(&dempty[aslot], aphase ^ 1);  // MMA it-na done with this A slot
       tc_fence_after();
-      tmem_st(tmem_base + lane_off + static_cast<uint32_t>(512 - 64 * (aslot + 1) + 16 * kW4Chunks * part), o);
+      const uint32_t ta = tmem_base + lane_off + static_cast<uint32_t>(512 - 64 * kp * (aslot + 1) + 16 * kW4Chunks * part);
+      tmem_st(ta, o0);
+      if (nbk == 2) tmem_st(ta + 64, o1);
       tc_fence_before();
       __syncwarp();
       if (elect_one()) mbar_arrive(&dfull[aslot]);
@@ -1004,7 +1018,10 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
         aslot = 0;
         aphase ^= 1;
       }
-      if (--seg_left == 0) seg_left = min(KS, n - j - 1);
+      ++it;
+      j += nbk;
+      seg_left -= nbk;
+      if (seg_left == 0) seg_left = min(KS, n - j);
     }
   }
 

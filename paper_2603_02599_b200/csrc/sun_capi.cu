@@ -461,8 +461,10 @@ LaunchCfg launch_cfg(const GemmPlan& p, int bn, bool w4, bool have_sk) {
     static const int env_xk = [] { const char* e = getenv("SUN_W4_XK"); return e ? atoi(e) : 0; }();
     static const int env_xs = [] { const char* e = getenv("SUN_W4_XSTAGES"); return e ? atoi(e) : 0; }();
     c.wgroup = env_wg > 0 ? env_wg : 4;
-    c.xk = env_xk > 0 ? env_xk : (bn <= 32 ? 4 : (bn <= 64 ? 2 : 1));
-    c.xstages = env_xs > 0 ? env_xs : (bn > 128 ? 2 : 3);
+    // K-block pairs per converter / MMA iteration need activation stages of an even
+    // number of blocks when bn <= 128 (gemm_tc.cuh `kp`)
+    c.xk = env_xk > 0 ? env_xk : (bn <= 32 ? 4 : (bn <= 128 ? 2 : 1));
+    c.xstages = env_xs > 0 ? env_xs : (bn > 64 ? 2 : 3);
     const int budget = kSmemPerSm - 2048 - 2048 - int(kEpiSmemBytes) - 1024 - c.xstages * int(w4_xstage_bytes(bn, c.xk));
     c.stages = std::max(2, std::min(16, budget / int(w4_wstage_bytes(c.wgroup))));
     c.smem = gemm_smem_bytes_w4(bn, c.wgroup, c.stages, c.xk, c.xstages);
