@@ -6,24 +6,31 @@
 // batch is the MMA N dimension (bn = round_up(B, 16) <= 256). K advances 128 per
 // pipeline stage (two 64-wide SWIZZLE_128B atoms). Both operands are stored in
 // the exact shared-memory image the UMMA descriptors expect, so every stage is
-// two linear cp.async.bulk copies (one 32 KB weight run, one activation run):
+// one linear cp.async.bulk copy:
 //   * SUN-BLK weights: [m_tiles][k/64][128 rows][64 cols] with 16-byte chunk c of
 //     row r at position c ^ (r & 7) — a tile's whole K is one sequential stream;
 //   * SUN-ACT activations: [k/64][bn rows][64 cols], same swizzle, written in
-//     that form by the kernels that produce them (RMSNorm, attention combine,
-//     SwiGLU epilogue).
-// Per-request cost dominates small TMA boxes on B200 (a 4 KB bulk stream reaches
+//     that form by the kernels that produce them (GEMM epilogues, attention).
+// Per-request cost dominates small bulk copies on B200 (a 4 KB stream reaches
 // ~2.3 TB/s, 16 KB 6.3, 64 KB 7.2; scripts/probe/stream_probe.cu), hence the
-// large linear requests. QSUN W4 stages bring packed int4 + scales instead and
-// converter warps dequantise into a bf16 SW128 tile (gemm_w4.cuh).
+// large linear requests. Weights and activations have separate rings, each fed by
+// its own producer warp, so the weight ring runs ahead by its whole depth.
+// QSUN W4 (gemm_w4.cuh): packed int4 + scales stages, converter warps dequantise
+// in registers and store the A tile into tensor memory.
 //
 // Schedules: with <= 148 tiles the S CTAs of a thread-block cluster split K for
 // one tile and reduce through DSMEM in fixed rank order (deterministic, one
-// wave, no global partials); with more tiles one persistent CTA per SM walks a
-// contiguous range of whole tiles with a double-buffered TMEM accumulator so a
-// tile's epilogue overlaps the next tile's stream. Warp roles: 0 = producer,
-// 1 = TMEM owner + single-thread MMA issuer, 2..5 = epilogue, 6..9 = W4
-// converters. Every kernel prefetches its weights before griddepcontrol.wait.
+// wave, no global partials) — or through L2 ("virtual clusters") where S-CTA
+// hardware clusters do not pack the GPCs; with more tiles one persistent CTA per
+// SM walks a contiguous range of whole tiles with a double-buffered TMEM
+// accumulator so a tile's epilogue overlaps the next tile's stream (stream-K is
+// available behind SUN_GEMM_SCHED).
+// Warp roles, bf16 (352 threads): 0 = weight producer, 1 = TMEM owner + single-
+// thread MMA issuer, 2..5 = epilogue group A, 6 = activation producer, 7..10 =
+// epilogue group B (groups take alternate 16-column chunks). W4 (480 threads):
+// 0 = weight producer, 1 = MMA, 2..5 = epilogue, 6..13 = converters (TMEM lane
+// group = warp % 4), 14 = activation producer. Weights are issued before
+// griddepcontrol.wait (they never depend on the previous kernel).
 //
 // Replaces the weight term `decoder_weight_bytes / (mbu * hbm_bandwidth)` of
 // the reference's step price (poolsim costmodel.py:101-113) with real work.
