@@ -8,7 +8,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2603_02599_b200.handoff import page_runs, recv_kv, send_kv
+from paper_2603_02599_b200.handoff import page_runs, recv_kv, recv_kv_async, send_kv, send_kv_async
 from paper_2603_02599_b200.kvpool import KvPool, PageAllocator
 from paper_2603_02599_b200.spec import TINY
 from paper_2603_02599_b200.sun_types import KvHandle
@@ -74,3 +74,56 @@ def test_kv_handoff_two_ranks_gloo():
 def test_page_runs():
     assert page_runs([3, 4, 5, 9, 10, 2]) == [(3, 3), (9, 2), (2, 1)]
     assert page_runs([]) == []
+
+
+def _async_worker(rank, port, q):
+    """Async hand-off overlapped with decode work: the receiver posts the payload
+    receives for two requests, keeps 'stepping' (CPU work standing in for decode
+    steps on other pages), and only then waits and admits."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        pool = KvPool(TINY, 24, "cpu")
+        g = torch.Generator().manual_seed(200 + rank)
+        pool.tensor.copy_(torch.randn(pool.tensor.shape, generator=g).to(torch.bfloat16))
+        alloc = PageAllocator(pool.num_pages)
+        if rank == 0:
+            sends, out = [], []
+            for rid, pages in ((3, [1, 7]), (4, [8, 9, 10])):
+                h = KvHandle(request_id=rid, resident_tokens=len(pages) * 16, bytes_per_token=TINY.kv_bytes_per_token,
+                             pages=pages, model_id=rid)
+                sends.append(send_kv_async(h, pool, 1))
+                out.append(pool.tensor[pages].clone())
+            for s in sends:
+                s.wait()
+            q.put(("sent", out))
+        else:
+            alloc.alloc(5)
+            pending = [recv_kv_async(pool, alloc, 0) for _ in range(2)]
+            busy = pool.tensor[:5].float().sum().item()  # decode work on resident pages meanwhile
+            got = []
+            for p_ in pending:
+                h = p_.wait()
+                got.append((h.request_id, list(h.pages), pool.tensor[h.pages].clone()))
+            q.put(("recv", got, busy))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_kv_handoff_async_overlap_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_async_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((m[0], m[1:]) for m in (q.get(timeout=120), q.get(timeout=120)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    sent = res["sent"][0]
+    got = res["recv"][0]
+    assert [g[0] for g in got] == [3, 4]
+    for payload, g in zip(sent, got):
+        assert torch.equal(payload, g[2])
+        assert len(page_runs(g[1])) == 1 and min(g[1]) >= 5  # fresh pages, one contiguous run each
