@@ -147,6 +147,18 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
  * device time of the i-th launch (order: embed+norm, then per layer [norm], qkv,
  * attention (split combine fused), o, norm, gate_up, down; final norm, lm_head, argmax).
  * Synchronises the stream. For measurement only. */
+/* sun_decode_step whose rows are grouped for the attention (token-parallel
+ * prefill, PrefillModule): group g is rows [group_start[g], group_start[g] +
+ * group_len[g]) — positions of ONE sequence, ascending, same block-table row,
+ * at most 16 / (n_q_heads / n_kv_heads) rows — and its KV pages are staged once
+ * for all of them. group_start / group_len are DEVICE int32 arrays [n_groups]
+ * covering every row. Same results as sun_decode_step. */
+SunStatus sun_decode_step_grouped(SunDecoder* dec, const int32_t* tokens, const int32_t* positions,
+                                  const int32_t* block_tables, int32_t bt_stride, int32_t batch,
+                                  int32_t pages_per_split, float* logits, int32_t* next_tokens, int32_t flags,
+                                  void* stream, const int32_t* group_start, const int32_t* group_len,
+                                  int32_t n_groups);
+
 SunStatus sun_decode_step_profile(SunDecoder* dec, const int32_t* tokens, const int32_t* positions,
                                   const int32_t* block_tables, int32_t bt_stride, int32_t batch,
                                   int32_t pages_per_split, float* logits, int32_t* next_tokens, void* stream,

@@ -68,6 +68,8 @@ SIGNATURES = {
                                    ctypes.POINTER(SunKvPool), c_vp, c_size, c_i32, c_i32, ctypes.POINTER(c_vp)]),
     "sun_decoder_destroy": (c_i32, [c_vp]),
     "sun_decode_step": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_i32, c_vp]),
+    "sun_decode_step_grouped": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_i32, c_vp,
+                                        c_vp, c_vp, c_i32]),
     "sun_decode_step_profile": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp,
                                         ctypes.POINTER(c_f32), c_i32, ctypes.POINTER(c_i32)]),
     "sun_decode_step_timeline": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_i32,

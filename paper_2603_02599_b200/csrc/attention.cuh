@@ -39,6 +39,11 @@ struct AttnArgs {
   int fused_combine;       // 1: last split merges in-kernel; 0: attn_combine_kernel does it
   unsigned long long* tl;  // step timeline (profiling only)
   int tl_idx;
+  // grouped rows (token-parallel prefill): grid z = groups; group z is rows
+  // [group_start[z], group_start[z] + group_len[z]) of one sequence at ascending
+  // positions, all read against the same KV pages (<= 16 / GQA-group rows each)
+  const int* group_start;
+  const int* group_len;
 };
 
 template <int D>
@@ -304,6 +309,217 @@ __global__ void __launch_bounds__(128)
     }
   }
   tl_end(a.tl, a.tl_idx);
+}
+
+// Grouped-rows variant for token-parallel prefill: the rows of one prompt at
+// consecutive positions share the KV pages, so one CTA stages each page once for
+// up to 16 query rows (rows x GQA heads fill the m16n8k16 A tile whose upper
+// half the decode kernel leaves at zero); each row keeps its own causal limit
+// and online-softmax state. Same arithmetic per row as attn_decode_kernel.
+template <int D>
+__global__ void __launch_bounds__(128)
+    attn_group_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnArgs a) {
+  using C = AttnCfg<D>;
+  const int split = blockIdx.x;
+  const int kvh = blockIdx.y;
+  const int b0 = a.group_start[blockIdx.z];
+  const int nr = a.group_len[blockIdx.z];
+  pdl_wait();
+  pdl_launch_dependents();
+  const int ctx = a.positions[b0 + nr - 1] + 1;  // the group's longest context
+  const int n_pages = (ctx + kPageTokens - 1) / kPageTokens;
+  const int p0 = split * a.pages_per_split;
+  if (p0 >= n_pages) return;
+  const int p1 = min(n_pages, p0 + a.pages_per_split);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kWarps * C::kStages * C::kStageBytes);
+  float* merge_ml = reinterpret_cast<float*>(bars + C::kWarps * C::kStages);  // [warps][16][2]
+
+  const int warp = warp_id_sync();
+  const int lane = threadIdx.x & 31;
+  const int G = a.n_q_heads / a.n_kv_heads;
+  const int g = lane >> 2;
+  const int t = lane & 3;
+  uint8_t* my_stages = smem + warp * C::kStages * C::kStageBytes;
+  uint64_t* my_bars = bars + warp * C::kStages;
+  // query rows g (lower half) and g + 8 (upper half) -> (row of the group, head)
+  const int r_lo = g / G, r_hi = (g + 8) / G;
+  const bool v_lo = r_lo < nr, v_hi = r_hi < nr;
+  const bool has_hi = nr * G > 8;  // warp-uniform
+  const int ctx_lo = v_lo ? a.positions[b0 + r_lo] + 1 : ctx;
+  const int ctx_hi = v_hi ? a.positions[b0 + r_hi] + 1 : ctx;
+
+  const int n_my = (p1 - p0 - warp + C::kWarps - 1) / C::kWarps > 0 ? (p1 - p0 - warp + C::kWarps - 1) / C::kWarps : 0;
+  const int* bt = a.block_tables + static_cast<long long>(b0) * a.bt_stride;
+  const int row_k = ((a.layer * 2 + 0) * a.n_kv_heads + kvh) * kPageTokens;
+  const int row_v = ((a.layer * 2 + 1) * a.n_kv_heads + kvh) * kPageTokens;
+  auto issue = [&](int i) {
+    const int s = i % C::kStages;
+    const int page = bt[p0 + warp + i * C::kWarps];
+    uint8_t* dst = my_stages + s * C::kStageBytes;
+    mbar_arrive_expect_tx(&my_bars[s], C::kStageBytes);
+#pragma unroll
+    for (int bx = 0; bx < C::kBoxes; ++bx) {
+      tma_load_3d(dst + bx * 2048, &tm_kv, &my_bars[s], bx * 64, row_k, page, kEvictFirst);
+      tma_load_3d(dst + C::kTileBytes + bx * 2048, &tm_kv, &my_bars[s], bx * 64, row_v, page, kEvictFirst);
+    }
+  };
+  if (lane == 0) {
+    for (int s = 0; s < C::kStages; ++s) mbar_init(&my_bars[s], 1);
+    fence_barrier_init();
+    const int pre = min(n_my, C::kStages);
+    for (int i = 0; i < pre; ++i) issue(i);
+  }
+  __syncwarp();
+
+  uint32_t qa[D / 16][2], qb[D / 16][2];
+  {
+    const __nv_bfloat16* ql = a.q + (static_cast<long long>(b0 + r_lo) * a.n_q_heads + kvh * G + g % G) * D;
+    const __nv_bfloat16* qh = a.q + (static_cast<long long>(b0 + r_hi) * a.n_q_heads + kvh * G + (g + 8) % G) * D;
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+      qa[kk][0] = v_lo ? *reinterpret_cast<const uint32_t*>(ql + kk * 16 + 2 * t) : 0u;
+      qa[kk][1] = v_lo ? *reinterpret_cast<const uint32_t*>(ql + kk * 16 + 8 + 2 * t) : 0u;
+      qb[kk][0] = v_hi ? *reinterpret_cast<const uint32_t*>(qh + kk * 16 + 2 * t) : 0u;
+      qb[kk][1] = v_hi ? *reinterpret_cast<const uint32_t*>(qh + kk * 16 + 8 + 2 * t) : 0u;
+    }
+  }
+  float o[D / 8][4];
+#pragma unroll
+  for (int n = 0; n < D / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float m_lo = -INFINITY, l_lo = 0.f, m_hi = -INFINITY, l_hi = 0.f;
+  const int mi = lane >> 3;
+  const int mr = lane & 7;
+
+  // online softmax of one half (e0: accumulator element offset 0 = row g, 2 = row g + 8)
+  auto soft = [&](const float (&sacc)[2][4], int e0, int row_ctx, int tok0, float& m_run, float& l_run, float (&p)[4]) {
+    float sv[4];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int n = 0; n < 2; ++n)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int tok = tok0 + n * 8 + 2 * t + e;
+        const float x = tok < row_ctx ? sacc[n][e0 + e] * a.scale_log2 : -INFINITY;
+        sv[n * 2 + e] = x;
+        mx = fmaxf(mx, x);
+      }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const float m_new = fmaxf(m_run, mx);
+    // a page wholly past this row's causal limit leaves the state untouched
+    const float corr = (m_new == -INFINITY) ? 1.f : exp2f(m_run - m_new);
+    m_run = m_new;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) p[e] = (m_new == -INFINITY) ? 0.f : exp2f(sv[e] - m_new);
+    l_run = l_run * corr + (p[0] + p[1] + p[2] + p[3]);
+    return corr;
+  };
+
+  for (int i = 0; i < n_my; ++i) {
+    const int s = i % C::kStages;
+    mbar_wait(&my_bars[s], (i / C::kStages) & 1);
+    const uint32_t kbase = smem_u32(my_stages + s * C::kStageBytes);
+    const uint32_t vbase = kbase + C::kTileBytes;
+    const int tok0 = (p0 + warp + i * C::kWarps) * kPageTokens;
+    float sacc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+      uint32_t r0, r1, r2, r3;
+      const int tok = ((mi >> 1) << 3) + mr;
+      const int dim = kk * 16 + ((mi & 1) << 3);
+      ldmatrix_x4(kbase + kv_swz(tok, dim), r0, r1, r2, r3);
+      mma_16816(sacc[0], qa[kk][0], qb[kk][0], qa[kk][1], qb[kk][1], r0, r1);
+      mma_16816(sacc[1], qa[kk][0], qb[kk][0], qa[kk][1], qb[kk][1], r2, r3);
+    }
+    float pl[4], ph[4] = {0.f, 0.f, 0.f, 0.f};
+    const float c_lo = soft(sacc, 0, ctx_lo, tok0, m_lo, l_lo, pl);
+    float c_hi = 1.f;
+    if (has_hi) c_hi = soft(sacc, 2, ctx_hi, tok0, m_hi, l_hi, ph);
+#pragma unroll
+    for (int n = 0; n < D / 8; ++n) {
+      o[n][0] *= c_lo;
+      o[n][1] *= c_lo;
+      o[n][2] *= c_hi;
+      o[n][3] *= c_hi;
+    }
+    const uint32_t a0 = pack_bf16x2(pl[0], pl[1]), a2 = pack_bf16x2(pl[2], pl[3]);
+    const uint32_t a1 = pack_bf16x2(ph[0], ph[1]), a3 = pack_bf16x2(ph[2], ph[3]);
+    const uint32_t b0l = pack_bf16x2(pl[0] - bf16_round(pl[0]), pl[1] - bf16_round(pl[1]));
+    const uint32_t b2l = pack_bf16x2(pl[2] - bf16_round(pl[2]), pl[3] - bf16_round(pl[3]));
+    const uint32_t b1l = pack_bf16x2(ph[0] - bf16_round(ph[0]), ph[1] - bf16_round(ph[1]));
+    const uint32_t b3l = pack_bf16x2(ph[2] - bf16_round(ph[2]), ph[3] - bf16_round(ph[3]));
+#pragma unroll
+    for (int nn = 0; nn < D / 16; ++nn) {
+      uint32_t r0, r1, r2, r3;
+      const int tok = ((mi & 1) << 3) + mr;
+      const int dim = nn * 16 + ((mi >> 1) << 3);
+      ldmatrix_x4_trans(vbase + kv_swz(tok, dim), r0, r1, r2, r3);
+      mma_16816(o[2 * nn], a0, a1, a2, a3, r0, r1);
+      mma_16816(o[2 * nn + 1], a0, a1, a2, a3, r2, r3);
+      mma_16816(o[2 * nn], b0l, b1l, b2l, b3l, r0, r1);
+      mma_16816(o[2 * nn + 1], b0l, b1l, b2l, b3l, r2, r3);
+    }
+    __syncwarp();
+    if (lane == 0 && i + C::kStages < n_my) {
+      fence_proxy_async_smem();
+      issue(i + C::kStages);
+    }
+  }
+  l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 1);
+  l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 2);
+  l_hi += __shfl_xor_sync(0xffffffffu, l_hi, 1);
+  l_hi += __shfl_xor_sync(0xffffffffu, l_hi, 2);
+
+  __syncthreads();
+  float* merge_o = reinterpret_cast<float*>(smem);  // [warps][16][D]
+#pragma unroll
+  for (int n = 0; n < D / 8; ++n) {
+    merge_o[(warp * 16 + g) * D + n * 8 + 2 * t] = o[n][0];
+    merge_o[(warp * 16 + g) * D + n * 8 + 2 * t + 1] = o[n][1];
+    merge_o[(warp * 16 + g + 8) * D + n * 8 + 2 * t] = o[n][2];
+    merge_o[(warp * 16 + g + 8) * D + n * 8 + 2 * t + 1] = o[n][3];
+  }
+  if (t == 0) {
+    merge_ml[(warp * 16 + g) * 2 + 0] = m_lo;
+    merge_ml[(warp * 16 + g) * 2 + 1] = l_lo;
+    merge_ml[(warp * 16 + g + 8) * 2 + 0] = m_hi;
+    merge_ml[(warp * 16 + g + 8) * 2 + 1] = l_hi;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < nr * G * D; idx += blockDim.x) {
+    const int qr = idx / D;
+    const int dim = idx % D;
+    const int b = b0 + qr / G;
+    const int head = kvh * G + qr % G;
+    // this row's own split count (the combine kernel uses the same rule)
+    const int npr = (a.positions[b] + 1 + kPageTokens - 1) / kPageTokens;
+    const int nsr = (npr + a.pages_per_split - 1) / a.pages_per_split;
+    if (split >= nsr) continue;  // wholly past this row's causal limit
+    float mm = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < C::kWarps; ++w) mm = fmaxf(mm, merge_ml[(w * 16 + qr) * 2]);
+    float acc = 0.f, ll = 0.f;
+#pragma unroll
+    for (int w = 0; w < C::kWarps; ++w) {
+      const float mw = merge_ml[(w * 16 + qr) * 2];
+      const float sc = (mw == -INFINITY) ? 0.f : exp2f(mw - mm);
+      acc += merge_o[(w * 16 + qr) * D + dim] * sc;
+      ll += merge_ml[(w * 16 + qr) * 2 + 1] * sc;
+    }
+    if (nsr == 1) {
+      store_attn_out<D>(a, b, head, dim, acc / ll);
+      continue;
+    }
+    const long long u = (static_cast<long long>(b) * a.n_q_heads + head) * a.max_splits + split;
+    a.part_o[u * D + dim] = acc;
+    if (dim == 0) {
+      a.part_ml[u * 2 + 0] = mm;
+      a.part_ml[u * 2 + 1] = ll;
+    }
+  }
 }
 
 // Merge the split partials of one (sequence, query head) and emit the bf16

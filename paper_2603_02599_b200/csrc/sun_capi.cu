@@ -183,6 +183,8 @@ void init_kernel_attrs() {
     set_max_smem(gemm_kernel<EPI_QKV_ROPE, true>);
     set_max_smem(gemm_kernel<EPI_SWIGLU, true>);
     set_max_smem(gemm_chain_kernel);
+    set_max_smem(attn_group_kernel<64>);
+    set_max_smem(attn_group_kernel<128>);
     set_max_smem(attn_decode_kernel<64>);
     set_max_smem(attn_decode_kernel<128>);
     (void)0;
@@ -628,9 +630,32 @@ int auto_pages_per_split(const SunDecoderDims& d, int batch) {
   return int(pps);
 }
 
+// Row groups for the attention of the next sun_decode_step (sun_decode_step_grouped).
+struct RowGroups {
+  const int* start = nullptr;
+  const int* len = nullptr;
+  int n = 0;
+};
+thread_local RowGroups g_groups;
+
 SunStatus run_attention(const SunDecoderDims& d, const CUtensorMap& tm_kv, AttnArgs aa, int batch,
                         cudaStream_t st, bool pdl) {
   tl_assign(aa);
+  if (g_groups.start != nullptr) {  // token-parallel prefill: rows of a prompt share KV page loads
+    aa.group_start = g_groups.start;
+    aa.group_len = g_groups.len;
+    aa.fused_combine = 0;
+    dim3 ggrid(aa.max_splits, d.n_kv_heads, g_groups.n);
+    if (d.head_dim == 128) SUN_CUDA(launch(attn_group_kernel<128>, ggrid, dim3(128), AttnCfg<128>::kSmem, st, pdl, tm_kv, aa));
+    else SUN_CUDA(launch(attn_group_kernel<64>, ggrid, dim3(128), AttnCfg<64>::kSmem, st, pdl, tm_kv, aa));
+    if (aa.max_splits > 1) {
+      if (d.head_dim == 128)
+        SUN_CUDA(launch(attn_combine_kernel<128>, dim3(d.n_q_heads, batch), dim3(128), 0, st, pdl, aa));
+      else
+        SUN_CUDA(launch(attn_combine_kernel<64>, dim3(d.n_q_heads, batch), dim3(128), 0, st, pdl, aa));
+    }
+    return SUN_OK;
+  }
   dim3 grid(aa.max_splits, d.n_kv_heads, batch);
   if (d.head_dim == 128) {
     SUN_CUDA(launch(attn_decode_kernel<128>, grid, dim3(128), AttnCfg<128>::kSmem, st, pdl, tm_kv, aa));
@@ -927,6 +952,21 @@ SunStatus sun_decode_step_profile(SunDecoder* dec, const int32_t* tokens, const 
   cudaEventDestroy(start);
   for (auto e : evs) cudaEventDestroy(e);
   return SUN_OK;
+}
+
+SunStatus sun_decode_step_grouped(SunDecoder* dec, const int32_t* tokens, const int32_t* positions,
+                                  const int32_t* block_tables, int32_t bt_stride, int32_t batch,
+                                  int32_t pages_per_split, float* logits, int32_t* next_tokens, int32_t flags,
+                                  void* stream, const int32_t* group_start, const int32_t* group_len,
+                                  int32_t n_groups) {
+  if (!group_start || !group_len || n_groups < 1 || n_groups > batch) return fail(SUN_ERR_VALUE, "bad row groups");
+  g_groups.start = group_start;
+  g_groups.len = group_len;
+  g_groups.n = n_groups;
+  SunStatus s = sun_decode_step(dec, tokens, positions, block_tables, bt_stride, batch, pages_per_split, logits,
+                                next_tokens, flags, stream);
+  g_groups = RowGroups{};
+  return s;
 }
 
 SunStatus sun_decode_step_timeline(SunDecoder* dec, const int32_t* tokens, const int32_t* positions,

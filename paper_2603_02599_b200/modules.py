@@ -58,7 +58,7 @@ class _StepRunner:
 
     def launch(self, tokens: torch.Tensor, positions: torch.Tensor, block_tables: torch.Tensor, batch: int,
                next_tokens: torch.Tensor, logits: torch.Tensor | None = None, pages_per_split: int = 0,
-               feedback: bool = False) -> None:
+               feedback: bool = False, groups: tuple[torch.Tensor, torch.Tensor] | None = None) -> None:
         """Enqueue one decode step on the current stream (all tensors on device).
 
         feedback=True also writes the sampled tokens back into ``tokens`` and
@@ -68,6 +68,14 @@ class _StepRunner:
         if block_tables.shape[1] < 1 or block_tables.dtype != torch.int32:
             raise ValueError("block_tables must be int32 [B, max_pages]")
         st = torch.cuda.current_stream().cuda_stream
+        if groups is not None:  # rows grouped by prompt for the attention (token-parallel prefill)
+            gs, gl = groups
+            _lib.check(self._lib.sun_decode_step_grouped(
+                self._h, tokens.data_ptr(), positions.data_ptr(), block_tables.data_ptr(), block_tables.stride(0),
+                batch, pages_per_split, None if logits is None else logits.data_ptr(), next_tokens.data_ptr(),
+                _lib.SUN_STEP_FEEDBACK if feedback else 0, st, gs.data_ptr(), gl.data_ptr(), gs.numel()),
+                "sun_decode_step_grouped")
+            return
         _lib.check(self._lib.sun_decode_step(
             self._h, tokens.data_ptr(), positions.data_ptr(), block_tables.data_ptr(), block_tables.stride(0), batch,
             pages_per_split, None if logits is None else logits.data_ptr(), next_tokens.data_ptr(),
@@ -171,9 +179,11 @@ class SharedDecodeModule(_StepRunner):
 class PrefillModule(_StepRunner):
     """P_θp^τ — a task-specific prefill module writing into the shared pool."""
 
-    def __init__(self, spec, weights, kv, max_batch, max_context, task_id: int, use_pdl: bool = True):
+    def __init__(self, spec, weights, kv, max_batch, max_context, task_id: int, use_pdl: bool = True,
+                 grouped: bool = True):
         super().__init__(spec, weights, kv, max_batch, max_context, use_pdl)
         self.task_id = task_id
+        self.grouped = grouped  # one attention CTA per (prompt, consecutive positions) group
         dev = weights.device
         self._next = torch.zeros(self.max_batch, dtype=torch.int32, device=dev)
         self._logits = torch.zeros(self.max_batch, spec.vocab, dtype=torch.float32, device=dev)
@@ -203,12 +213,21 @@ class PrefillModule(_StepRunner):
         first = [0] * B
         last_logits = torch.zeros(B, self.spec.vocab, dtype=torch.float32, device=dev)
         C = self.max_batch
+        R = max(1, 16 // (self.spec.n_q_heads // self.spec.n_kv_heads))  # rows per attention group
         for c0 in range(0, len(rows), C):
             chunk = rows[c0:c0 + C]
             toks = torch.tensor([prompts[i][t] for i, t in chunk], dtype=torch.int32).to(dev)
             pos = torch.tensor([t for _, t in chunk], dtype=torch.int32).to(dev)
             bts = bt[[i for i, _ in chunk]].to(dev)
-            self.launch(toks, pos, bts, len(chunk), self._next, self._logits)
+            gstart, glen = [], []
+            for j, (i, t) in enumerate(chunk):  # runs of one prompt's consecutive positions, <= R rows
+                if glen and glen[-1] < R and chunk[j - 1][0] == i and chunk[j - 1][1] == t - 1:
+                    glen[-1] += 1
+                else:
+                    gstart.append(j)
+                    glen.append(1)
+            groups = (torch.tensor(gstart, dtype=torch.int32).to(dev), torch.tensor(glen, dtype=torch.int32).to(dev))
+            self.launch(toks, pos, bts, len(chunk), self._next, self._logits, groups=groups if self.grouped else None)
             done = [(j, i) for j, (i, t) in enumerate(chunk) if t == lens[i] - 1]
             if done:
                 nt = self._next[:len(chunk)].cpu()

@@ -15,13 +15,14 @@ alloc = PageAllocator(kv.num_pages)
 pages = [alloc.alloc(pages_for(isl)) for _ in range(n)]
 g = torch.Generator().manual_seed(0)
 prompts = [torch.randint(0, spec.vocab, (isl,), generator=g).tolist() for _ in range(n)]
-for mb in (64, 256):
-    pre = PrefillModule(spec, DeviceWeights(spec, init_weights(spec, 1, dev), dev, isl + 8), kv, mb, isl + 8, task_id=0)
+for mb, grouped in ((256, False), (64, True), (256, True)):
+    pre = PrefillModule(spec, DeviceWeights(spec, init_weights(spec, 1, dev), dev, isl + 8), kv, mb, isl + 8, task_id=0,
+                        grouped=grouped)
     pre.prefill(prompts[:1], pages[:1])
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     first, _ = pre.prefill(prompts, pages)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    print(f"{spec.name} max_batch={mb}: {n} x {isl} tokens in {dt * 1e3:.1f} ms = {n * isl / dt:.0f} prompt tok/s", flush=True)
+    print(f"{spec.name} max_batch={mb} grouped={grouped}: {n} x {isl} tokens in {dt * 1e3:.1f} ms = {n * isl / dt:.0f} prompt tok/s", flush=True)
     del pre
