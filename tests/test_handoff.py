@@ -36,7 +36,7 @@ def _worker(rank, port, q):
                 h = KvHandle(request_id=rid, resident_tokens=len(pages) * 16 - 3, bytes_per_token=TINY.kv_bytes_per_token,
                              pages=pages, model_id=rid % 2)
                 send_kv(h, pool, 1)
-                out.append(pool.tensor[pages].clone())
+                out.append(pool.tensor[pages].float().numpy().copy())  # numpy: no fd sharing across exit
             q.put(("sent", out))
         else:  # decode side
             alloc.alloc(3)  # pool partly in use already
@@ -44,7 +44,7 @@ def _worker(rank, port, q):
             for _ in range(2):
                 h = recv_kv(pool, alloc, 0)
                 got.append((h.request_id, h.resident_tokens, h.bytes_per_token, h.model_id, list(h.pages),
-                            pool.tensor[h.pages].clone()))
+                            pool.tensor[h.pages].float().numpy().copy()))
             q.put(("recv", got, alloc.free_pages))
     finally:
         dist.destroy_process_group()
@@ -66,7 +66,7 @@ def test_kv_handoff_two_ranks_gloo():
     assert [g[0] for g in got] == [7, 8]
     assert got[0][1] == 3 * 16 - 3 and got[0][2] == TINY.kv_bytes_per_token and got[0][3] == 1
     for (payload, g) in zip(sent, got):
-        assert torch.equal(payload, g[5])
+        assert (payload == g[5]).all()
         assert len(page_runs(g[4])) == 1  # landed in a contiguous run of the receiver's pool
     assert free_after == 24 - 3 - 3 - 4
 
@@ -93,7 +93,7 @@ def _async_worker(rank, port, q):
                 h = KvHandle(request_id=rid, resident_tokens=len(pages) * 16, bytes_per_token=TINY.kv_bytes_per_token,
                              pages=pages, model_id=rid)
                 sends.append(send_kv_async(h, pool, 1))
-                out.append(pool.tensor[pages].clone())
+                out.append(pool.tensor[pages].float().numpy().copy())  # numpy: no fd sharing across exit
             for s in sends:
                 s.wait()
             q.put(("sent", out))
@@ -104,7 +104,7 @@ def _async_worker(rank, port, q):
             got = []
             for p_ in pending:
                 h = p_.wait()
-                got.append((h.request_id, list(h.pages), pool.tensor[h.pages].clone()))
+                got.append((h.request_id, list(h.pages), pool.tensor[h.pages].float().numpy().copy()))
             q.put(("recv", got, busy))
     finally:
         dist.destroy_process_group()
@@ -125,5 +125,5 @@ def test_kv_handoff_async_overlap_gloo():
     got = res["recv"][0]
     assert [g[0] for g in got] == [3, 4]
     for payload, g in zip(sent, got):
-        assert torch.equal(payload, g[2])
+        assert (payload == g[2]).all()
         assert len(page_runs(g[1])) == 1 and min(g[1]) >= 5  # fresh pages, one contiguous run each
