@@ -1,4 +1,5 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest -q -m gpu tests/test_decode_parity_gpu.py tests/test_serving_gpu.py -x > gpurun_out/pytest_grp.log 2>&1; tail -3 gpurun_out/pytest_grp.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
-timeout 600 python scripts/prefill_speed.py > gpurun_out/prefill.txt 2>&1
+run() { tag=$1; shift; e=(); while [[ "$1" == *=* ]]; do e+=("$1"); shift; done; env "${e[@]}" timeout 300 python bench.py --steps 20 --no-cpu --no-e2e "$@" > gpurun_out/x_$tag.json 2>gpurun_out/x_$tag.err; }
+run c5 --config c5
+run c5fc SUN_ATTN_FUSED_COMBINE=1 --config c5
+for p in 64 128 256; do run c5p$p --config c5 --pps $p; done
