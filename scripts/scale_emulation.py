@@ -26,11 +26,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c3")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--out", required=True)
+ap.add_argument("--cap", type=int, default=256, help="per-GPU batch cap (KV capacity of one B200)")
 args = ap.parse_args()
 cfg = bench.CONFIGS[args.config]
 spec = SPECS[cfg["spec"]]
 dev = torch.device("cuda")
-B_max = 256
+B_max = args.cap
 ctx_max = cfg["isl"] + cfg["osl"] + 8
 dw = DeviceWeights(spec, init_weights(spec, 0, dev), dev, ctx_max + args.reps + 8, free_source=True)
 kv = KvPool(spec, B_max * pages_for(ctx_max + args.reps + 8) + 4, dev)
@@ -64,16 +65,18 @@ def step_ms(B):
 rows = []
 for routing in ("lot", "pinned"):
     for world in (1, 2, 4, 8):
-        per = [min(len(p), B_max) for p in bench.build_assignment(cfg, world, routing)]
+        full = [len(p) for p in bench.build_assignment(cfg, world, routing)]
+        per = [min(b, B_max) for b in full]
         t = [step_ms(B) for B in per]
         tpot = max(t)
-        rows.append({"routing": routing, "n_gpus": world, "batch_per_rank": per, "step_ms_per_rank": t,
+        rows.append({"routing": routing, "n_gpus": world, "requests_per_rank": full, "batch_per_rank": per,
+                     "step_ms_per_rank": t,
                      "tpot_ms": tpot, "tokens_per_s": sum(per) / (tpot / 1e3)})
         print(f"{routing:6s} N={world}: batches {per} -> TPOT {tpot:.3f} ms, {sum(per) / tpot * 1e3:.0f} tok/s", flush=True)
 base = rows[0]["tokens_per_s"]
 for r in rows:
     r["speedup_vs_1gpu_lot"] = r["tokens_per_s"] / base
-out = {"config": cfg["workload"], "how": "each rank's batch timed on one B200 (CUDA graph, median of %d); N-GPU step = "
+out = {"config": cfg["workload"], "batch_cap": B_max, "how": "each rank's batch timed on one B200 (CUDA graph, median of %d); N-GPU step = "
        "slowest rank (independent decode workers, no collective)" % args.reps, "rows": rows}
 with open(args.out, "w") as f:
     json.dump(out, f, indent=1)
