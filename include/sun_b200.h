@@ -138,6 +138,10 @@ SunStatus sun_decoder_destroy(SunDecoder* dec);
  * This is the operator that replaces costmodel.decode_step_time_from_totals
  * at engine.py:427-429. Errors: batch < 1 -> SUN_ERR_VALUE. */
 #define SUN_STEP_FEEDBACK 1 /* flags: also write tokens[b] = next_tokens[b], positions[b] += 1 on device */
+/* flags: every row is a different sequence (a decode batch; not token-parallel prefill
+ * rows of one prompt): the step's KV append then touches only each row's last page,
+ * so the attention stages the other pages while the QKV kernel is still finishing */
+#define SUN_STEP_DISTINCT_ROWS 2
 SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t* positions,
                           const int32_t* block_tables, int32_t bt_stride, int32_t batch,
                           int32_t pages_per_split, float* logits, int32_t* next_tokens, int32_t flags,
@@ -164,7 +168,7 @@ SunStatus sun_decode_step_profile(SunDecoder* dec, const int32_t* tokens, const 
                                   int32_t pages_per_split, float* logits, int32_t* next_tokens, void* stream,
                                   float* kernel_ms, int32_t capacity, int32_t* n_kernels);
 
-/* One sun_decode_step (PDL as configured, not serialised) with a device-side
+/* One sun_decode_step (PDL as configured, not serialised, rows distinct) with a device-side
  * timeline of its GEMM and attention launches: timeline is a DEVICE uint64 array
  * [capacity][2] pre-filled with (~0, 0); launch i records the earliest CTA start
  * and the latest CTA end (%globaltimer ns). If stamps is non-null and launch

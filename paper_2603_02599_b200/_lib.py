@@ -29,6 +29,7 @@ SUN_ERR_UNSUPPORTED = 3
 SUN_ERR_CUDA = 4
 SUN_ERR_CAPACITY = 5
 SUN_STEP_FEEDBACK = 1
+SUN_STEP_DISTINCT_ROWS = 2
 
 
 class SunDecoderDims(ctypes.Structure):

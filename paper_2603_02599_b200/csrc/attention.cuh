@@ -44,6 +44,10 @@ struct AttnArgs {
   // positions, all read against the same KV pages (<= 16 / GQA-group rows each)
   const int* group_start;
   const int* group_len;
+  // 1: every row is a different sequence (the decode batch), so the step's QKV
+  // kernel writes only each row's last page: the other pages are staged before
+  // griddepcontrol.wait, i.e. while the QKV grid is still finishing (PDL)
+  int prestage;
 };
 
 template <int D>
@@ -86,8 +90,12 @@ __global__ void __launch_bounds__(128)
   const int kvh = blockIdx.y;
   const int b = blockIdx.z;
   tl_begin(a.tl, a.tl_idx);
-  pdl_wait();
-  pdl_launch_dependents();  // early: the next kernel may start its prologue / weight prefetch
+  // positions / block tables are inputs of the whole step (never written inside it)
+  const bool pre = a.prestage != 0;
+  if (!pre) {
+    pdl_wait();
+    pdl_launch_dependents();  // early: the next kernel may start its prologue / weight prefetch
+  }
   const int ctx = a.positions[b] + 1;
   const int n_pages = (ctx + kPageTokens - 1) / kPageTokens;
   const int p0 = split * a.pages_per_split;
@@ -127,12 +135,20 @@ __global__ void __launch_bounds__(128)
     }
   };
 
+  const int npre = min(n_my, C::kStages);
+  int ipre = 0;
   if (lane == 0) {
     for (int s = 0; s < C::kStages; ++s) mbar_init(&my_bars[s], 1);
     fence_barrier_init();
-    const int pre = min(n_my, C::kStages);
-    for (int i = 0; i < pre; ++i) issue(i);
+    if (pre)  // pages before the row's last one: untouched by this step's KV append
+      for (; ipre < npre && p0 + warp + ipre * C::kWarps < n_pages - 1; ++ipre) issue(ipre);
   }
+  if (pre) {
+    pdl_wait();  // q and the appended K/V are the QKV kernel's outputs
+    pdl_launch_dependents();
+  }
+  if (lane == 0)
+    for (; ipre < npre; ++ipre) issue(ipre);
   __syncwarp();
 
   // Q fragments (A operand, rows = query heads of the group, zero-padded to 16).

@@ -68,6 +68,10 @@ struct GemmArgs {
   int xstages;       // W4: activation stages of xk K blocks
   int wgroup;        // W4: K blocks per weight stage (packed [wgroup][8 KB] | scales [wgroup][256 B])
   int xk;            // W4: K blocks per activation stage
+  int push_bytes;    // hardware cluster split-K, push mode (> 0): every rank bulk-copies the
+                     // chunks other ranks own into their receive areas (this many bytes of
+                     // smem after the barriers, [S-1 senders][ceil(bn/16/S) chunks][8 KB]);
+                     // 0: owners pull the peers' parked partials over DSMEM
   // STORE / RESID / LOGITS
   float* out_f32;
   long long ldo;
@@ -689,7 +693,9 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
   uint64_t* dfull = tempty + 2;                // [kW4MaxABufs] W4: A tile dequantised
   uint64_t* dempty = dfull + kW4MaxABufs;      // [kW4MaxABufs] W4: A tile consumed by the MMA
   uint64_t* skbar = dempty + kW4MaxABufs;      // stream-K owner: contributor partials landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(skbar + 1);
+  uint64_t* rbar = skbar + 1;                   // push mode: the peers' chunks landed in recv
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 1);
+  float* recv = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 1024);
 
   const int warp = warp_id_sync();
   constexpr bool kPre = !W4 && (EPI == EPI_RESID_ADD || EPI == EPI_QKV_ROPE);
@@ -698,6 +704,9 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
   const bool clustered = S > 1;  // split-K over S CTAs (hardware cluster or virtual)
   const bool vcl = clustered && a.vcluster;
   const uint32_t rank = clustered ? (vcl ? blockIdx.x % S : cluster_ctarank()) : 0u;
+  const bool push = clustered && !vcl && a.push_bytes > 0;
+  const int nch = a.bn / 16;                                       // 16-column chunks; chunk c is
+  const int nmax = (nch + static_cast<int>(S) - 1) / static_cast<int>(S);  // reduced by rank c % S
   // this CTA's work: the contiguous range [u0, u1) of work units u = tile * ksteps + ks
   const int KS = a.ksteps;
   int u0, u1;
@@ -743,13 +752,21 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
       mbar_init(&dempty[j], 1);
     }
     mbar_init(skbar, 1);
+    mbar_init(rbar, 1);
     fence_barrier_init();
+    if (push) {  // (S - 1) peers x this rank's chunks x 8 KB will complete_tx on rbar
+      const int mine = static_cast<int>(rank) < nch ? (nch - static_cast<int>(rank) + static_cast<int>(S) - 1) / static_cast<int>(S) : 0;
+      mbar_arrive_expect_tx(rbar, static_cast<uint32_t>(mine) * (S - 1) * 8192u);
+    }
   }
   if (warp == 1) tmem_alloc(tmem_slot, ncols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // push mode: this arrival publishes rbar's init cluster-wide; the matching wait sits
+  // just before the first remote copy, long after every peer has arrived
+  if (push) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   if (threadIdx.x == 0) SUN_STAMP(1);
   // Early trigger: the next kernel may launch now and run its prologue (and, for
   // a GEMM, its weight prefetch) as SMs free up; its griddepcontrol.wait still
@@ -983,6 +1000,7 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
           }
         }
         if (vcl) __threadfence();
+        if (push) fence_proxy_async_smem();  // the parked chunks are the bulk copies' source
       }
     }
   } else if (W4 && warp < 6 + kW4ConvThreads / 32) {
@@ -1043,6 +1061,25 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
         }
       }
       __syncthreads();
+    } else if (push) {
+      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // peers' rbar initialised
+      __syncthreads();                                                     // our partial is parked
+      if (threadIdx.x == 64) {
+        // send every chunk another rank reduces to that rank's receive area (slot = our
+        // rank among its S - 1 senders); completion is counted on the owner's rbar
+        const float* part = reinterpret_cast<const float*>(smem);
+        for (int c = 0; c < nch; ++c) {
+          const uint32_t o = static_cast<uint32_t>(c) % S;
+          if (o == rank) continue;
+          const uint32_t slot = rank < o ? rank : rank - 1;
+          const uint32_t dst = dsmem_addr(recv + (slot * nmax + static_cast<uint32_t>(c) / S) * 2048u, o);
+          asm volatile(
+              "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], 8192, [%2];" ::"r"(dst),
+              "r"(smem_u32(part + c * 2048)), "r"(dsmem_addr(rbar, o))
+              : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
     } else {
       cluster_sync_all();  // every rank's partial is visible cluster-wide
     }
@@ -1052,6 +1089,7 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
       const int row_local = q * 32 + (threadIdx.x & 31);
       float* part = reinterpret_cast<float*>(smem);
       const float* gpart = vcl ? a.sk_part + static_cast<long long>(blockIdx.x - rank) * a.bn * kTileM : nullptr;
+      if (push) mbar_wait(rbar, 0);  // every peer's copy of our chunks has landed
       // reduce columns [c0, c0 + NC) over the S ranks (float4 slots q0.. of the chunk), in rank order
       auto reduce_cols = [&](int c0, int q0, auto& v) {
         constexpr int NQ = sizeof(v) / sizeof(float) / 4;
@@ -1067,6 +1105,11 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
               x[u][j] = (r0 + u >= S) ? make_float4(0.f, 0.f, 0.f, 0.f)
                         : vcl ? __ldcg(reinterpret_cast<const float4*>(gpart + static_cast<long long>(r0 + u) * a.bn * kTileM +
                                                                       part_index(cbase, q0 + j, row_local)))
+                        : push ? *reinterpret_cast<const float4*>(
+                                     (r0 + u == rank ? part + part_index(cbase, 0, 0)
+                                                     : recv + ((r0 + u < rank ? r0 + u : r0 + u - 1) * nmax +
+                                                               static_cast<uint32_t>(cbase >> 4) / S) * 2048u) +
+                                     part_index(0, q0 + j, row_local))
                               : ld_dsmem_f4(dsmem_addr(part + part_index(cbase, q0 + j, row_local), r0 + u));
 #pragma unroll
           for (int u = 0; u < 4; ++u)
@@ -1108,6 +1151,8 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
     if (vcl) {  // the last of the tile's 2S arrivals rearms the counter for the next launch
       __syncthreads();
       if (threadIdx.x == 64 && atomicAdd(tile_cnt, 1u) == 2 * S - 1) *tile_cnt = 0u;
+    } else if (push) {
+      if (threadIdx.x == 64) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // sources read
     } else {
       cluster_sync_all();  // nobody exits while a peer may still read its partial
     }

@@ -435,9 +435,24 @@ int cluster_splits(const GemmPlan& p, size_t smem, bool w4, int slots) {
 // Launch configuration of one GEMM (also used to aim the previous GEMM's L2
 // prefetch at the CTAs that will start streaming first).
 struct LaunchCfg {
-  int grid, splits, vcluster, sk_units, stages, xstages, wgroup, xk;
+  int grid, splits, vcluster, sk_units, stages, xstages, wgroup, xk, push;
   size_t smem;
 };
+
+// Push-mode split-K reduction (SUN_GEMM_PUSH=1, default off): hardware-cluster ranks
+// bulk-copy the chunks their peers reduce into the peers' receive areas (DSMEM,
+// completion on the owner's mbarrier) instead of the owners pulling them after a
+// cluster barrier; no cluster barrier at the end either. Used when the receive
+// area fits next to the ring. Measured neutral on C3 (5.055 vs 5.061 ms/step) and
+// C4 (14.76 vs 14.73): the tail is the slowest rank and the epilogue's stores,
+// not the barrier.
+int gemm_push() {
+  static int v = [] {
+    const char* e = getenv("SUN_GEMM_PUSH");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
 
 // Virtual clusters (SUN_GEMM_VCLUSTER, default on): when the hardware cannot
 // co-schedule enough S-CTA clusters (QKV: 48 tiles want S = 3 -> 144 CTAs, but
@@ -504,6 +519,14 @@ LaunchCfg launch_cfg(const GemmPlan& p, int bn, bool w4, bool have_sk) {
       c.vcluster = 1;
     }
     c.grid = c.splits > 1 ? p.m_tiles * c.splits : std::min(p.m_tiles, slots);
+    if (c.splits > 1 && !c.vcluster && gemm_push()) {
+      const int nch = bn / 16, nmax = (nch + c.splits - 1) / c.splits;
+      const size_t recv = size_t(c.splits - 1) * nmax * 8192;
+      if (c.smem + recv <= size_t(kSmemPerSm) / per_sm) {
+        c.push = int(recv);
+        c.smem += recv;
+      }
+    }
   }
   return c;
 }
@@ -553,6 +576,7 @@ SunStatus run_gemm(const void* wblk, const void* packed, const void* scales, Gem
   a.splits = c.splits;
   a.vcluster = c.vcluster;
   a.sk_units = c.sk_units;
+  a.push_bytes = c.push;
   g_cluster = c.vcluster ? 1u : unsigned(c.splits);
   if (w4) {
     if constexpr (EPI == EPI_LOGITS) return fail(SUN_ERR_UNSUPPORTED, "lm_head is bf16");
@@ -793,6 +817,8 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
   aa.act_rows = bn;
   aa.counters = dec->attn_cnt;
   aa.fused_combine = attn_fused_combine();
+  static const int prestage_env = [] { const char* e = getenv("SUN_ATTN_PRESTAGE"); return e ? atoi(e) : 1; }();
+  aa.prestage = (flags & SUN_STEP_DISTINCT_ROWS) && g_groups.start == nullptr && prestage_env ? 1 : 0;
 
   // RMSNorm is factored into the GEMMs: a producer writes xg = bf16(x * g) and
   // per-tile sums of squares, the consumer GEMM scales row b of its result by
@@ -980,7 +1006,7 @@ SunStatus sun_decode_step_timeline(SunDecoder* dec, const int32_t* tokens, const
   g_tl.stamps = reinterpret_cast<unsigned long long*>(stamps);
   g_tl.stamp_idx = stamp_launch;
   SunStatus s = sun_decode_step(dec, tokens, positions, block_tables, bt_stride, batch, pages_per_split, nullptr,
-                                next_tokens, 0, stream);
+                                next_tokens, SUN_STEP_DISTINCT_ROWS, stream);
   *n_launches = g_tl.next;
   g_tl = TimelineState{};
   return s;

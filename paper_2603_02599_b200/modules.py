@@ -23,6 +23,10 @@ from .weights import DeviceWeights
 class _StepRunner:
     """Owns one C decoder (TMA descriptors + workspace) over a weight set."""
 
+    # rows of a step are different sequences (SUN_STEP_DISTINCT_ROWS): true for the
+    # decode batch, not for token-parallel prefill rows of one prompt
+    distinct_rows = False
+
     def __init__(self, spec: DecoderSpec, weights: DeviceWeights, kv: KvPool, max_batch: int, max_context: int,
                  use_pdl: bool = True):
         self.spec, self.weights, self.kv = spec, weights, kv
@@ -76,10 +80,11 @@ class _StepRunner:
                 _lib.SUN_STEP_FEEDBACK if feedback else 0, st, gs.data_ptr(), gl.data_ptr(), gs.numel()),
                 "sun_decode_step_grouped")
             return
+        flags = (_lib.SUN_STEP_FEEDBACK if feedback else 0) | (_lib.SUN_STEP_DISTINCT_ROWS if self.distinct_rows else 0)
         _lib.check(self._lib.sun_decode_step(
             self._h, tokens.data_ptr(), positions.data_ptr(), block_tables.data_ptr(), block_tables.stride(0), batch,
-            pages_per_split, None if logits is None else logits.data_ptr(), next_tokens.data_ptr(),
-            _lib.SUN_STEP_FEEDBACK if feedback else 0, st), "sun_decode_step")
+            pages_per_split, None if logits is None else logits.data_ptr(), next_tokens.data_ptr(), flags, st),
+            "sun_decode_step")
 
     def profile(self, tokens, positions, block_tables, batch, next_tokens, logits=None, pages_per_split=0):
         """Serialised step with a CUDA event after every kernel -> per-launch device ms."""
@@ -121,8 +126,12 @@ class SharedDecodeModule(_StepRunner):
 
     Static device buffers (tokens / positions / block tables / next tokens /
     logits) back an optional CUDA graph per (batch, pages_per_split) bucket, so
-    a step is one graph launch (32 layers x 8 kernels otherwise).
+    a step is one graph launch (32 layers x 8 kernels otherwise). Every row is a
+    different request (the scheduler's batch), which lets the attention stage KV
+    pages ahead of the step's KV append (``distinct_rows``).
     """
+
+    distinct_rows = True
 
     def __init__(self, spec, weights, kv, max_batch, max_context, use_pdl: bool = True, keep_logits: bool = True):
         super().__init__(spec, weights, kv, max_batch, max_context, use_pdl)

@@ -14,6 +14,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c3")
 ap.add_argument("--layers", type=int, default=3, help="layers to print")
 ap.add_argument("--stamp", type=int, default=-1, help="launch index whose per-CTA phases to print")
+ap.add_argument("--slow", type=int, default=0, help="with --stamp: also list the N CTAs that finish last")
 args = ap.parse_args()
 cfg = bench.CONFIGS[args.config]
 spec = SPECS[cfg["spec"]].with_bits(4) if cfg["bits"] == 4 else SPECS[cfg["spec"]]
@@ -80,3 +81,10 @@ if args.stamp >= 0:
             continue
         c = rel[:, i][sv[:, i] > 0]
         print(f"   {name:12s} min {c.min():9.2f} med {c.median():9.2f} max {c.max():9.2f}")
+    if args.slow > 0:
+        order = torch.argsort(rel[:, 6], descending=True)[: args.slow]
+        print(f"   slowest {args.slow} CTAs (blockIdx: start first_stage last_mma parked sync1 reduced epi_chunk exit)")
+        allrows = (st.view(4096, 16)[:, 0] > 0).nonzero().flatten().cpu()
+        for k in order.tolist():
+            r = rel[k]
+            print(f"   {int(allrows[k]):4d}: " + " ".join(f"{float(r[i]):8.2f}" for i in (0, 2, 3, 8, 9, 10, 11, 6)))
