@@ -141,15 +141,17 @@ SunStatus sun_decoder_destroy(SunDecoder* dec);
 /* flags: every row is a different sequence (a decode batch; not token-parallel prefill
  * rows of one prompt): the step's KV append then touches only each row's last page,
  * so the attention stages the other pages while the QKV kernel is still finishing */
-#define SUN_STEP_DISTINCT_ROWS 2
+#define SUN_STEP_DISTINCT_ROWS 2 /* (bf16: also selects the persistent layer GEMM chain, which
+                                     needs the whole GPU: one such step in flight per GPU) */
 SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t* positions,
                           const int32_t* block_tables, int32_t bt_stride, int32_t batch,
                           int32_t pages_per_split, float* logits, int32_t* next_tokens, int32_t flags,
                           void* stream);
 
-/* Same step, serialised, with a CUDA event after every kernel: kernel_ms[i] is the
- * device time of the i-th launch (order: embed+norm, then per layer [norm], qkv,
- * attention (split combine fused), o, norm, gate_up, down; final norm, lm_head, argmax).
+/* Same step (rows distinct), serialised, with a CUDA event after every kernel: kernel_ms[i] is the
+ * device time of the i-th launch (order: embed+norm, then per layer qkv, attention
+ * [combine], o, gate_up, down — or, with the bf16 layer chain, qkv once and then per
+ * layer attention [combine], chain; lm_head, argmax).
  * Synchronises the stream. For measurement only. */
 /* sun_decode_step whose rows are grouped for the attention (token-parallel
  * prefill, PrefillModule): group g is rows [group_start[g], group_start[g] +

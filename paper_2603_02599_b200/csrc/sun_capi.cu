@@ -577,6 +577,8 @@ SunStatus run_gemm(const void* wblk, const void* packed, const void* scales, Gem
   a.vcluster = c.vcluster;
   a.sk_units = c.sk_units;
   a.push_bytes = c.push;
+  static const int self_pf = [] { const char* e = getenv("SUN_GEMM_SELF_PF_KB"); return e ? atoi(e) * 1024 : 0; }();
+  a.self_pf_bytes = self_pf;
   g_cluster = c.vcluster ? 1u : unsigned(c.splits);
   if (w4) {
     if constexpr (EPI == EPI_LOGITS) return fail(SUN_ERR_UNSUPPORTED, "lm_head is bf16");
@@ -587,14 +589,19 @@ SunStatus run_gemm(const void* wblk, const void* packed, const void* scales, Gem
   return SUN_OK;
 }
 
-// Layer GEMM chain (SUN_GEMM_CHAIN=1, bf16): the phases' GemmArgs are filled as for
-// run_gemm; every split phase reduces through L2 over 148 persistent CTAs.
-int gemm_chain_enabled() {
+// Layer GEMM chain (bf16): the phases' GemmArgs are filled as for run_gemm; every
+// split phase reduces through L2 over 148 persistent CTAs. Used by default for
+// decode batches (SUN_STEP_DISTINCT_ROWS; measured C2 1.65 -> 1.59 ms, C3 5.03 ->
+// 4.95, C5 22.6 -> 22.3 once the attention prestages its pages);
+// SUN_GEMM_CHAIN=0 / 1 forces it off / on. Its grid-count phase barriers need all
+// 148 CTAs resident together: one step in flight per GPU (the workspace is not
+// re-entrant anyway), no second persistent decoder on another stream.
+bool use_chain(int flags, bool w4) {
   static int v = [] {
     const char* e = getenv("SUN_GEMM_CHAIN");
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : -1;
   }();
-  return v;
+  return !w4 && (v == 1 || (v < 0 && (flags & SUN_STEP_DISTINCT_ROWS)));
 }
 
 SunStatus run_chain(GemmArgs* ph, const int* epi, const GemmPlan* plans, const void* const* wblk, int nph,
@@ -883,7 +890,7 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     produce_norm(a, l + 1 < d.n_layers ? dec->layers[l + 1].attn_norm : dec->w.final_norm);
     return a;
   };
-  const bool chain = gemm_chain_enabled() && !w4;
+  const bool chain = use_chain(flags, w4);
   for (int l = 0; l < d.n_layers; ++l) {
     const SunLayerWeights& lw = dec->layers[l];
     GemmArgs a;
@@ -963,7 +970,7 @@ SunStatus sun_decode_step_profile(SunDecoder* dec, const int32_t* tokens, const 
   dec->pdl = false;  // serialise kernels so event deltas attribute time to one kernel
   g_trace.events = &evs;
   SunStatus s = sun_decode_step(dec, tokens, positions, block_tables, bt_stride, batch, pages_per_split, logits,
-                                next_tokens, 0, stream);
+                                next_tokens, SUN_STEP_DISTINCT_ROWS, stream);
   g_trace.events = nullptr;
   dec->pdl = pdl;
   if (s != SUN_OK) return s;

@@ -52,7 +52,9 @@ class _StepRunner:
         self._lib = lib
         import os as _os
         self.fused_combine = _os.environ.get("SUN_ATTN_FUSED_COMBINE", "0") == "1"
-        self.gemm_chain = _os.environ.get("SUN_GEMM_CHAIN", "0") == "1" and spec.weight_bits == 16
+        # (mirrors sun_capi.cu use_chain: bf16 decode batches by default; SUN_GEMM_CHAIN=0/1 forces)
+        chain_env = _os.environ.get("SUN_GEMM_CHAIN")
+        self.gemm_chain = spec.weight_bits == 16 and (chain_env == "1" or (chain_env is None and self.distinct_rows))
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -29,6 +29,8 @@ def classify(names):
             after_attn = True
         elif "attn_combine" in n:
             out.append("attn_combine")
+        elif "gemm_chain" in n:
+            out.append("gemm_chain")
         elif "argmax" in n:
             out.append("argmax")
         elif "gemm_kernel<2" in n:

@@ -52,7 +52,10 @@ for rep in range(2):
 t = tl[: n.value].cpu().double()
 t0 = t[:, 0].min()
 t = (t - t0) / 1e3
-lab = [names[i % 5] if i < 5 * spec.n_layers else "lm_head" for i in range(n.value)]
+short = {"gemm_qkv_rope_kv": "qkv", "attention": "attn", "gemm_o_resid_norm": "o", "gemm_gate_up_swiglu": "gate_up",
+         "gemm_down_resid_norm": "down", "gemm_chain": "chain", "gemm_lm_head_argmax": "lm_head"}
+lab = [short[k] for k in dec.kernel_names(combine=False) if k in short]  # the launches that record a timeline slot
+assert len(lab) == n.value, (len(lab), n.value)
 print(f"{args.config}: {n.value} launches, step span {t[:, 1].max():.1f} us")
 tot = {}
 prev_end = 0.0
@@ -62,7 +65,7 @@ for i in range(n.value):
     d[0] += e - max(s, prev_end)   # exclusive time: from previous end (or own start) to own end
     d[1] += e - s
     d[2] += 1
-    if i < 5 * args.layers or i == n.value - 1:
+    if i < (len(lab) - 1) * args.layers // spec.n_layers or i == n.value - 1:
         print(f"  {i:3d} {lab[i]:8s} start {s:9.2f} end {e:9.2f} dur {e - s:7.2f} after-prev-end {e - prev_end:7.2f} (overlap {prev_end - s:6.2f})")
     prev_end = max(prev_end, e)
 print("per class: exclusive us/launch (end - previous end), inclusive us/launch (end - start)")

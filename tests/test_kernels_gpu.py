@@ -58,14 +58,15 @@ def test_gemm_deterministic_stream_k(cuda):
         assert torch.equal(a, kernels.gemm_bf16(w, x, 64))
 
 
-@pytest.mark.parametrize("sched", ["0", "2", "vcl2", "novcl", "push", "chain"])
+@pytest.mark.parametrize("sched", ["0", "2", "vcl2", "novcl", "push", "nochain"])
 def test_gemm_schedules_subprocess(sched):
     """The GEMM kernel tests and the end-to-end decode parity under the other
     schedules: 0 = cluster split-K / whole tiles only, 2 = stream-K on every
     GEMM whose partials fit (covers every fused epilogue with partial tiles),
     vcl2 = L2-reduced virtual clusters wherever a split pays, novcl = hardware
     clusters only, push = hardware-cluster partials pushed to their owners by DSMEM bulk
-    copies (instead of pulled after a cluster barrier), chain = the persistent per-layer GEMM chain kernel."""
+    copies (instead of pulled after a cluster barrier), nochain = separate GEMM launches
+    instead of the persistent per-layer GEMM chain kernel (the bf16 decode default)."""
     import os
     import subprocess
     import sys
@@ -78,8 +79,8 @@ def test_gemm_schedules_subprocess(sched):
         env["SUN_GEMM_VCLUSTER"] = "0"
     elif sched == "push":
         env["SUN_GEMM_PUSH"] = "1"
-    elif sched == "chain":
-        env["SUN_GEMM_CHAIN"] = "1"
+    elif sched == "nochain":
+        env["SUN_GEMM_CHAIN"] = "0"
     else:
         env["SUN_GEMM_SCHED"] = sched
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", "(gemm or tiny) and not subprocess",
