@@ -26,6 +26,8 @@ struct ChainArgs {
   GemmArgs ph[kChainMaxPhases];
   int epi[kChainMaxPhases];  // EpiKind per phase
   int nph;
+  unsigned long long* stamps;  // profiling: per CTA [16] = per phase p: [4p] activations ready,
+                               // [4p+1] first MMA, [4p+2] last MMA issued, [4p+3] epilogue done
   unsigned* bar;  // [2]: phases completed x CTAs, CTAs exited (zeroed once, self-resetting)
   unsigned long long* tl;
   int tl_idx;
@@ -58,6 +60,9 @@ SUN_DEVICE PhaseSched phase_sched(const GemmArgs& a) {
   p.nseg = p.n > 0 ? (p.u1 - 1) / KS - p.t_first + 1 : 0;
   return p;
 }
+
+#define SUN_CSTAMP(i) \
+  do { if (c.stamps) c.stamps[blockIdx.x * 16 + (i)] = gtimer(); } while (0)
 
 SUN_DEVICE void chain_wait_phase(const unsigned* bar, unsigned target) {
   if (target == 0) return;
@@ -224,6 +229,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_chain_kernel(const __gri
         if (!wprod) {
           if (p == 0) pdl_wait();
           else chain_wait_phase(c.bar, G * p);
+          SUN_CSTAMP(4 * p);
         }
         const int KS = a.ksteps;
         int ks = ps.n > 0 ? ps.u0 % KS : 0, tile = ps.n > 0 ? ps.u0 / KS : 0;
@@ -270,6 +276,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_chain_kernel(const __gri
         mbar_wait(&full[wslot], wphase);
         mbar_wait(&xfull[xslot], xphase);
         tc_fence_after();
+        if (j == 0 && threadIdx.x == 32) SUN_CSTAMP(4 * p + 1);
+        if (j == ps.n - 1 && threadIdx.x == 32) SUN_CSTAMP(4 * p + 2);
         if (elect_one()) {
           const uint32_t xa = smem_u32(xstg + xslot * xsb);
           const uint32_t wa = smem_u32(stg + wslot * sb);
@@ -320,6 +328,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_chain_kernel(const __gri
       }
       epi_pair_bar();
       if (threadIdx.x == 64) {  // this CTA's outputs of phase p are written
+        SUN_CSTAMP(4 * p + 3);
         __threadfence();
         atomicAdd(c.bar, 1u);
       }

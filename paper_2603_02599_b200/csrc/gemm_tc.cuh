@@ -118,9 +118,6 @@ struct GemmArgs {
   // producer once its own loads are out (fills HBM during the epilogue/launch gap)
   const uint8_t* pf_w;  // next weights (SUN-BLK or SUN-W4 packed); null = off
   int pf_w4, pf_m_tiles, pf_ksteps, pf_kb64, pf_splits, pf_grid, pf_sk_units, pf_bytes;
-  // bf16: once its ring is full, the weight producer prefetches this many further bytes of
-  // its own range into L2 (0 = off)
-  int self_pf_bytes;
   // optional per-CTA %globaltimer stamps [gridDim.x][8] (profiling only)
   unsigned long long* stamps;
   unsigned long long* tl;  // step timeline slot array (profiling only) and this launch's index
@@ -890,17 +887,6 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
       int ks = u0 % KS, tile = u0 / KS, slot = 0, phase = 0;
       for (int j = 0; j < n; ++j) {
         const int nb = nblk_of(ks);
-        if (wprod && j == depth && a.self_pf_bytes > 0) {
-          // ring full: pull the next self_pf_bytes of this CTA's own weight range into L2
-          // (before the activations exist this is HBM time the ring cannot use)
-          const long long b0 = static_cast<long long>(tile) * a.kb64 + 2 * ks;
-          const long long b1 = static_cast<long long>((u1 - 1) / KS) * a.kb64 + min(2 * ((u1 - 1) % KS) + 2, a.kb64);
-          const long long len = min((b1 - b0) * static_cast<long long>(kTileWBytes), static_cast<long long>(a.self_pf_bytes));
-          if (len > 0)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.wblk + b0 * kTileWBytes),
-                         "r"(static_cast<uint32_t>(len))
-                         : "memory");
-        }
         if (j >= depth) mbar_wait(&eb[slot], phase ^ 1);
         if (wprod) {
           mbar_arrive_expect_tx(&fb[slot], nb * kTileWBytes);

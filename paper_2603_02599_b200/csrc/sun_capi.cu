@@ -577,8 +577,6 @@ SunStatus run_gemm(const void* wblk, const void* packed, const void* scales, Gem
   a.vcluster = c.vcluster;
   a.sk_units = c.sk_units;
   a.push_bytes = c.push;
-  static const int self_pf = [] { const char* e = getenv("SUN_GEMM_SELF_PF_KB"); return e ? atoi(e) * 1024 : 0; }();
-  a.self_pf_bytes = self_pf;
   g_cluster = c.vcluster ? 1u : unsigned(c.splits);
   if (w4) {
     if constexpr (EPI == EPI_LOGITS) return fail(SUN_ERR_UNSUPPORTED, "lm_head is bf16");
@@ -626,6 +624,7 @@ SunStatus run_chain(GemmArgs* ph, const int* epi, const GemmPlan* plans, const v
   c.nph = nph;
   c.bar = bar;
   tl_assign(c);
+  if (g_tl.stamps != nullptr && c.tl != nullptr && c.tl_idx == g_tl.stamp_idx) c.stamps = g_tl.stamps;
   g_cluster = 1;
   SUN_CUDA(launch(gemm_chain_kernel, dim3(kNumSms), dim3(kGemmThreads), gemm_smem_bytes(bn, stages, xstages), st,
                   pdl, c));

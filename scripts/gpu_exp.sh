@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest -q -m gpu tests/ > gpurun_out/pt_chain.log 2>&1; echo "pytest rc $?" >> gpurun_out/pt_chain.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -2 gpurun_out/smoke.log
-timeout 300 python scripts/step_timeline.py --config c3 > gpurun_out/tl_chain.txt 2>&1
-timeout 300 python bench.py --steps 50 > gpurun_out/x_c3full.json 2>gpurun_out/x_c3full.err
+run() { tag=$1; shift; e=(); while [[ "$1" == *=* ]]; do e+=("$1"); shift; done; env "${e[@]}" timeout 300 python bench.py --steps 50 --no-cpu --no-e2e "$@" > gpurun_out/x_$tag.json 2>gpurun_out/x_$tag.err; }
+for r in a b; do for o in 0 2 4 6; do run c3p$o$r SUN_CHAIN_OPTS=$o --config c3; done; done
+for o in 0 6; do run c2p$o SUN_CHAIN_OPTS=$o --config c2; done

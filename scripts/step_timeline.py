@@ -79,6 +79,8 @@ if args.stamp >= 0:
     print(f"launch {args.stamp} ({lab[args.stamp]}): {len(sv)} CTAs; phase times relative to step start (us)")
     nm = ["start", "setup", "first_stage", "last_mma", "first_acc", "epi_done", "exit", "-", "parked", "sync1",
           "reduced", "epi_chunk", "qkv_bar1", "qkv_bar2", "qkv_loads"]
+    if lab[args.stamp] == "chain":  # per phase (O, gate_up, down, next QKV)
+        nm = [f"{ph}:{ev}" for ph in ("o", "gate_up", "down", "qkv") for ev in ("x_ready", "first_mma", "last_mma", "epi_done")]
     for i, name in enumerate(nm):
         if name == "-" or (sv[:, i] == 0).all():
             continue
