@@ -20,6 +20,19 @@ from .spec import DecoderSpec
 from .weights import DeviceWeights
 
 
+def uses_gemm_chain(weight_bits: int, distinct_rows: bool, env: str | None) -> bool:
+    """Whether sun_decode_step runs the persistent layer GEMM chain (mirrors
+    sun_capi.cu use_chain): bf16 decode batches by default, SUN_GEMM_CHAIN=0/1 forces."""
+    if weight_bits != 16:
+        return False
+    if env is not None:
+        try:
+            return int(env) == 1
+        except ValueError:  # atoi semantics: not a number -> 0
+            return False
+    return distinct_rows
+
+
 class _StepRunner:
     """Owns one C decoder (TMA descriptors + workspace) over a weight set."""
 
@@ -52,9 +65,7 @@ class _StepRunner:
         self._lib = lib
         import os as _os
         self.fused_combine = _os.environ.get("SUN_ATTN_FUSED_COMBINE", "0") == "1"
-        # (mirrors sun_capi.cu use_chain: bf16 decode batches by default; SUN_GEMM_CHAIN=0/1 forces)
-        chain_env = _os.environ.get("SUN_GEMM_CHAIN")
-        self.gemm_chain = spec.weight_bits == 16 and (chain_env == "1" or (chain_env is None and self.distinct_rows))
+        self.gemm_chain = uses_gemm_chain(spec.weight_bits, self.distinct_rows, _os.environ.get("SUN_GEMM_CHAIN"))
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -114,3 +114,19 @@ def test_step_bytes_model():
     sb = pricing.step_bytes(LLAMA31_8B, [1024 + (j * 256) // 64 for j in range(64)])
     assert 24.5e9 < sb < 24.9e9  # C3 = 24.72 GB / step
     assert LLAMA31_8B.kv_bytes_per_token == 131072
+
+
+def test_step_flags_and_chain_selection():
+    """Decode batches (distinct rows) set SUN_STEP_DISTINCT_ROWS and take the bf16 layer
+    chain; token-parallel prefill rows do neither; the env switch forces either way and
+    never applies to QSUN (mirrors sun_capi.cu use_chain)."""
+    from paper_2603_02599_b200 import _lib
+    from paper_2603_02599_b200.modules import PrefillModule, SharedDecodeModule, uses_gemm_chain
+
+    assert _lib.SUN_STEP_DISTINCT_ROWS == 2 and _lib.SUN_STEP_FEEDBACK == 1
+    hdr = open(os.path.join(os.path.dirname(GOLDEN), "..", "include", "sun_b200.h")).read()
+    assert "#define SUN_STEP_DISTINCT_ROWS 2" in hdr and "#define SUN_STEP_FEEDBACK 1" in hdr
+    assert SharedDecodeModule.distinct_rows and not PrefillModule.distinct_rows
+    assert uses_gemm_chain(16, True, None) and not uses_gemm_chain(16, False, None)
+    assert uses_gemm_chain(16, False, "1") and not uses_gemm_chain(16, True, "0")
+    assert not uses_gemm_chain(16, True, "x") and not uses_gemm_chain(4, True, "1") and not uses_gemm_chain(4, True, None)
