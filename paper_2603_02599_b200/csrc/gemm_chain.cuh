@@ -26,6 +26,9 @@ struct ChainArgs {
   GemmArgs ph[kChainMaxPhases];
   int epi[kChainMaxPhases];  // EpiKind per phase
   int nph;
+  int hw;  // 1: launched as 4-CTA clusters; split phases with vcluster == 0 (S = 4) reduce
+           // through DSMEM: ranks st.async the chunks their peers own into the peers'
+           // receive areas (smem after the barriers), completion on per-phase mbarriers
   unsigned long long* stamps;  // profiling: per CTA [16] = per phase p: [4p] activations ready,
                                // [4p+1] first MMA, [4p+2] last MMA issued, [4p+3] epilogue done
   unsigned* bar;  // [2]: phases completed x CTAs, CTAs exited (zeroed once, self-resetting)
@@ -73,9 +76,16 @@ SUN_DEVICE void epi_pair_bar() { asm volatile("bar.sync 4, 256;" ::: "memory"); 
 
 // One phase of the epilogue warps (both groups). Returns after every segment of
 // this CTA's range is written out and the TMEM buffers are released.
+SUN_DEVICE void st_async_f4(uint32_t addr, const float* v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(addr),
+               "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "r"(mbar)
+               : "memory");
+}
+
 template <int EPI>
 SUN_DEVICE void chain_epilogue_phase(const GemmArgs& a, const PhaseSched& ps, float* epi, uint32_t tmem_base,
-                                     uint64_t* tfull, uint64_t* tempty, int& buf, int& tphase) {
+                                     uint64_t* tfull, uint64_t* tempty, int& buf, int& tphase, float* recv,
+                                     uint64_t* rbar) {
   const int warp = static_cast<int>(threadIdx.x >> 5);
   const int q = warp & 3;
   const int row_local = q * 32 + (threadIdx.x & 31);
@@ -92,6 +102,70 @@ SUN_DEVICE void chain_epilogue_phase(const GemmArgs& a, const PhaseSched& ps, fl
       tc_fence_before();
       epi_bar();
       if (epi_lead_thread()) mbar_arrive(&tempty[buf]);
+    } else if (!a.vcluster) {
+      // hardware cluster (S = 4 ranks of one tile): send every chunk another rank owns
+      // (chunk c -> rank c % S, slot = our rank among its S - 1 senders) straight from
+      // TMEM into its receive area; the two groups take alternate chunks
+      const int S = ps.S, rank = ps.rank, nch = a.bn / 16, nmax = (nch + S - 1) / S;
+      int idx = 0;
+      for (int c = 0; c < nch; ++c) {
+        const int o = c % S;
+        if (o == rank) continue;
+        if ((idx++ & 1) != epi_grp()) continue;
+        const int slot = rank < o ? rank : rank - 1;
+        float v[16];
+        tmem_ld16(taddr + c * 16, v);
+        const float* dst = recv + (slot * nmax + c / S) * 2048;
+        const uint32_t mb = dsmem_addr(rbar, static_cast<uint32_t>(o));
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          st_async_f4(dsmem_addr(dst + part_index(0, j, row_local), static_cast<uint32_t>(o)), v + 4 * j, mb);
+      }
+      // reduce our chunks: rank order, our own partial read from TMEM (same sums as
+      // the L2 path: ((0 + p0) + p1) + ...)
+      mbar_wait(rbar, 0);
+      auto reduce_own = [&](int c, int q0, auto& v) {
+        constexpr int NQ = sizeof(v) / sizeof(float) / 4;
+        float own[4 * NQ];
+        if constexpr (NQ == 4) tmem_ld16(taddr + c * 16, own);
+        else tmem_ld8(taddr + c * 16 + 4 * q0, own);
+#pragma unroll
+        for (int j = 0; j < 4 * NQ; ++j) v[j] = 0.f;
+        for (int r = 0; r < S; ++r) {
+          if (r == rank) {
+#pragma unroll
+            for (int j = 0; j < 4 * NQ; ++j) v[j] += own[j];
+          } else {
+            const float* src = recv + ((r < rank ? r : r - 1) * nmax + c / S) * 2048;
+#pragma unroll
+            for (int j = 0; j < NQ; ++j) {
+              const float4 x = *reinterpret_cast<const float4*>(src + part_index(0, q0 + j, row_local));
+              v[4 * j] += x.x;
+              v[4 * j + 1] += x.y;
+              v[4 * j + 2] += x.z;
+              v[4 * j + 3] += x.w;
+            }
+          }
+        }
+      };
+      const int nmine = (nch - rank + S - 1) / S;
+      if (nmine == 1) {
+        float v[8];
+        reduce_own(rank, 2 * epi_grp(), v);
+        tc_fence_before();
+        epi_pair_bar();
+        if (epi_lead_thread()) mbar_arrive(&tempty[buf]);  // accumulator read: the MMA may reuse it
+        epi_chunk<EPI, 8>(a, tile, row_local, rank * 16 + 8 * epi_grp(), v, epi);
+      } else {
+        for (int c = rank + S * epi_grp(); c < nch; c += 2 * S) {
+          float v[16];
+          reduce_own(c, 0, v);
+          epi_chunk<EPI>(a, tile, row_local, c * 16, v, epi);
+        }
+        tc_fence_before();
+        epi_pair_bar();
+        if (epi_lead_thread()) mbar_arrive(&tempty[buf]);
+      }
     } else {
       // split phase: park this rank's partial in L2, meet the tile's S CTAs, reduce
       // this rank's columns (chunks rank, rank + S, ... alternate between the groups)
@@ -186,7 +260,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_chain_kernel(const __gri
   uint64_t* xempty = xfull + kMaxXStages;
   uint64_t* tfull = xempty + kMaxXStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rbar = tempty + 2;  // [kChainMaxPhases] hardware split phases: peers' chunks landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + kChainMaxPhases);
+  float* recv = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 1024);
   const int warp = warp_id_sync();
   const unsigned G = gridDim.x;
   const uint32_t ncols = tmem_cols_for(bn);
@@ -204,13 +280,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_chain_kernel(const __gri
       mbar_init(&tfull[j], 1);
       mbar_init(&tempty[j], 2);
     }
+    for (int p = 0; p < kChainMaxPhases; ++p) mbar_init(&rbar[p], 1);
     fence_barrier_init();
+    if (c.hw) {  // each hardware split phase: (S - 1) senders x our chunks x 8 KB
+      for (int p = 0; p < c.nph; ++p) {
+        const GemmArgs& a = c.ph[p];
+        if (a.splits > 1 && !a.vcluster) {
+          const int S = a.splits, r = static_cast<int>(blockIdx.x) % S, nch = a.bn / 16;
+          const int mine = r < nch ? (nch - r + S - 1) / S : 0;
+          mbar_arrive_expect_tx(&rbar[p], static_cast<uint32_t>(mine * (S - 1)) * 8192u);
+        }
+      }
+    }
   }
   if (warp == 1) tmem_alloc(tmem_slot, ncols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // hardware clusters: publish the receive barriers' init cluster-wide; the epilogue
+  // warps wait before their first st.async, the other warps before they exit
+  if (c.hw) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   pdl_launch_dependents();
 
   if (warp == 0 || warp == 6) {
@@ -310,6 +400,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_chain_kernel(const __gri
     }
   } else if (warp < 6 || warp >= 7) {
     // epilogue groups A (warps 2..5) and B (7..10)
+    if (c.hw) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     int buf = 0, tphase = 0;
     for (int p = 0; p < c.nph; ++p) {
       const GemmArgs& a = c.ph[p];
@@ -321,10 +412,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_chain_kernel(const __gri
         epi_pair_bar();
       }
       switch (c.epi[p]) {
-        case EPI_RESID_ADD: chain_epilogue_phase<EPI_RESID_ADD>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase); break;
-        case EPI_SWIGLU: chain_epilogue_phase<EPI_SWIGLU>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase); break;
-        case EPI_QKV_ROPE: chain_epilogue_phase<EPI_QKV_ROPE>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase); break;
-        default: chain_epilogue_phase<EPI_STORE_F32>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase); break;
+        case EPI_RESID_ADD: chain_epilogue_phase<EPI_RESID_ADD>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase, recv, &rbar[p]); break;
+        case EPI_SWIGLU: chain_epilogue_phase<EPI_SWIGLU>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase, recv, &rbar[p]); break;
+        case EPI_QKV_ROPE: chain_epilogue_phase<EPI_QKV_ROPE>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase, recv, &rbar[p]); break;
+        default: chain_epilogue_phase<EPI_STORE_F32>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase, recv, &rbar[p]); break;
       }
       epi_pair_bar();
       if (threadIdx.x == 64) {  // this CTA's outputs of phase p are written
@@ -334,6 +425,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_chain_kernel(const __gri
       }
     }
   }
+  if (c.hw && !(warp >= 2 && warp < 6) && warp < 7) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {

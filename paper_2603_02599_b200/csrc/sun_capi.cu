@@ -608,15 +608,38 @@ SunStatus run_chain(GemmArgs* ph, const int* epi, const GemmPlan* plans, const v
   memset(&c, 0, sizeof(c));
   const int bn = ph[0].bn;
   const int stages = gemm_stages(bn, false, 1), xstages = gemm_xstages(bn);
+  size_t smem = gemm_smem_bytes(bn, stages, xstages);
+  // 4-CTA clusters (SUN_CHAIN_CLUSTER, default on) when the DSMEM receive area
+  // ([3 senders][ceil(bn/64) chunks][8 KB]) fits and every cluster of the grid can be
+  // resident at once (the phase barriers need the whole grid): grid = 4 x clusters
+  static const int cl_env = [] { const char* e = getenv("SUN_CHAIN_CLUSTER"); return e ? atoi(e) : 1; }();
+  const size_t recv = size_t(3) * ((bn / 16 + 3) / 4) * 8192;
+  int G = kNumSms;
+  if (cl_env && smem + recv <= size_t(kSmemPerSm)) {
+    const int ncl = std::min(kNumSms / 4, max_active_clusters(4, smem + recv, false));
+    bool any = false;  // some phase must get one tile per cluster (else the smaller grid only costs)
+    for (int i = 0; i < nph; ++i)
+      any = any || (plans[i].m_tiles <= ncl && plans[i].ksteps >= 4 && 4 * ncl / plans[i].m_tiles >= 4);
+    if (ncl >= 32 && any) {
+      c.hw = 1;
+      G = 4 * ncl;
+      smem += recv;
+    }
+  }
   for (int i = 0; i < nph; ++i) {
     GemmArgs a = ph[i];
     const GemmPlan& p = plans[i];
     a.wblk = static_cast<const uint8_t*>(wblk[i]);
     a.stages = stages;
     a.xstages = xstages;
-    const int want = p.m_tiles <= kNumSms ? std::min(std::min(8, kNumSms / std::max(1, p.m_tiles)), p.ksteps) : 1;
-    a.splits = want;
-    a.vcluster = want > 1 ? 1 : 0;
+    const int want = p.m_tiles <= G ? std::min(std::min(8, G / std::max(1, p.m_tiles)), p.ksteps) : 1;
+    if (c.hw && want >= 4 && p.ksteps >= 4) {  // one tile per cluster, reduced through DSMEM
+      a.splits = 4;
+      a.vcluster = 0;
+    } else {
+      a.splits = want;
+      a.vcluster = want > 1 ? 1 : 0;
+    }
     a.sk_units = 0;
     c.ph[i] = a;
     c.epi[i] = epi[i];
@@ -625,9 +648,8 @@ SunStatus run_chain(GemmArgs* ph, const int* epi, const GemmPlan* plans, const v
   c.bar = bar;
   tl_assign(c);
   if (g_tl.stamps != nullptr && c.tl != nullptr && c.tl_idx == g_tl.stamp_idx) c.stamps = g_tl.stamps;
-  g_cluster = 1;
-  SUN_CUDA(launch(gemm_chain_kernel, dim3(kNumSms), dim3(kGemmThreads), gemm_smem_bytes(bn, stages, xstages), st,
-                  pdl, c));
+  g_cluster = c.hw ? 4u : 1u;
+  SUN_CUDA(launch(gemm_chain_kernel, dim3(G), dim3(kGemmThreads), smem, st, pdl, c));
   return SUN_OK;
 }
 

@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
-timeout 900 python bench.py > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
-timeout 900 python bench.py --config c2 --steps 30 --warmup 5 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
-timeout 900 python scripts/scale_emulation.py --config c3 --out gpurun_out/scale_emulation_c3.json > gpurun_out/scale_c3.log 2>&1
-timeout 900 python scripts/scale_emulation.py --config c5 --cap 40 --reps 10 --out gpurun_out/scale_emulation_c5.json > gpurun_out/scale_c5.log 2>&1
+run() { tag=$1; shift; e=(); while [[ "$1" == *=* ]]; do e+=("$1"); shift; done; env "${e[@]}" timeout 300 python bench.py --steps 50 --no-cpu --no-e2e "$@" > gpurun_out/x_$tag.json 2>gpurun_out/x_$tag.err; }
+for c in c5 c3 c2 c1; do for o in 1 0; do run ${c}hv$o SUN_CHAIN_CLUSTER=$o --config $c; done; done
+timeout 1500 python -m pytest -q -m gpu tests/ > gpurun_out/pt_hv.log 2>&1; echo "rc $?" >> gpurun_out/pt_hv.log
