@@ -103,10 +103,12 @@ SUN_DEVICE void chain_epilogue_phase(const GemmArgs& a, const PhaseSched& ps, fl
       epi_bar();
       if (epi_lead_thread()) mbar_arrive(&tempty[buf]);
     } else if (!a.vcluster) {
-      // hardware cluster (S = 4 ranks of one tile): send every chunk another rank owns
-      // (chunk c -> rank c % S, slot = our rank among its S - 1 senders) straight from
-      // TMEM into its receive area; the two groups take alternate chunks
+      // hardware cluster (S = 2 or 4 ranks of one tile, 4 / S tiles per 4-CTA cluster):
+      // send every chunk another rank owns (chunk c -> rank c % S, slot = our rank among
+      // its S - 1 senders) straight from TMEM into its receive area; the two groups take
+      // alternate chunks
       const int S = ps.S, rank = ps.rank, nch = a.bn / 16, nmax = (nch + S - 1) / S;
+      const int cta0 = static_cast<int>(blockIdx.x & 3u) - rank;  // cluster rank of the tile's rank 0
       int idx = 0;
       for (int c = 0; c < nch; ++c) {
         const int o = c % S;
@@ -116,10 +118,10 @@ SUN_DEVICE void chain_epilogue_phase(const GemmArgs& a, const PhaseSched& ps, fl
         float v[16];
         tmem_ld16(taddr + c * 16, v);
         const float* dst = recv + (slot * nmax + c / S) * 2048;
-        const uint32_t mb = dsmem_addr(rbar, static_cast<uint32_t>(o));
+        const uint32_t mb = dsmem_addr(rbar, static_cast<uint32_t>(cta0 + o));
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          st_async_f4(dsmem_addr(dst + part_index(0, j, row_local), static_cast<uint32_t>(o)), v + 4 * j, mb);
+          st_async_f4(dsmem_addr(dst + part_index(0, j, row_local), static_cast<uint32_t>(cta0 + o)), v + 4 * j, mb);
       }
       // reduce our chunks: rank order, our own partial read from TMEM (same sums as
       // the L2 path: ((0 + p0) + p1) + ...)

@@ -633,8 +633,9 @@ SunStatus run_chain(GemmArgs* ph, const int* epi, const GemmPlan* plans, const v
     a.stages = stages;
     a.xstages = xstages;
     const int want = p.m_tiles <= G ? std::min(std::min(8, G / std::max(1, p.m_tiles)), p.ksteps) : 1;
-    if (c.hw && want >= 4 && p.ksteps >= 4) {  // one tile per cluster, reduced through DSMEM
-      a.splits = 4;
+    static const int hw2 = [] { const char* e = getenv("SUN_CHAIN_HW2"); return e ? atoi(e) : 1; }();
+    if (c.hw && (want >= 4 || (want >= 2 && hw2)) && p.ksteps >= 4) {  // 4 / S tiles per cluster, DSMEM
+      a.splits = want >= 4 ? 4 : 2;
       a.vcluster = 0;
     } else {
       a.splits = want;
