@@ -8,13 +8,16 @@
 // ahead across phase boundaries — the next GEMM's weights stream into the ring
 // while the epilogue warps finish the current phase — and only the activation
 // producer waits for the grid-wide "phase p done" count before loading phase p's
-// input. Split phases reduce through L2 (virtual clusters, gemm_tc.cuh), whole-tile
-// phases use the TMEM double buffer across phase boundaries.
+// input. Whole-tile phases use the TMEM double buffer across phase boundaries. Split
+// phases reduce either through DSMEM (launched as 4-CTA clusters, c.hw: S = 4 or 2
+// ranks of a tile inside one cluster st.async the chunks their peers own into the
+// peers' receive areas) or through L2 (148 plain CTAs: virtual clusters, gemm_tc.cuh).
 //
-// Deadlock freedom: 148 CTAs x 1 per SM are co-resident once the previous kernel
-// drains (PDL: the dependent launch needs every CTA of this grid to have started);
-// the only cross-CTA waits are phase counts and per-tile split counters, both
-// produced by epilogue warps that never wait on anything but their own CTA's MMA.
+// Deadlock freedom: the host sizes the grid so that every CTA (every cluster) is
+// co-resident once the previous kernel drains (PDL: the dependent launch needs every
+// CTA of this grid to have started); the only cross-CTA waits are phase counts,
+// per-tile split counters and DSMEM receive barriers, all fed by epilogue warps that
+// never wait on anything but their own CTA's MMA and the previous phase.
 #pragma once
 #include "gemm_tc.cuh"
 
