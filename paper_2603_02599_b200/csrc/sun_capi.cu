@@ -620,7 +620,7 @@ SunStatus run_chain(GemmArgs* ph, const int* epi, const GemmPlan* plans, const v
     bool any = false;  // some phase must get one tile per cluster (else the smaller grid only costs)
     for (int i = 0; i < nph; ++i)
       any = any || (plans[i].m_tiles <= ncl && plans[i].ksteps >= 4 && 4 * ncl / plans[i].m_tiles >= 4);
-    if (ncl >= 32 && any) {
+    if (ncl >= 32 && (any || cl_env == 2)) {  // (2: clusters even without an S = 4 phase)
       c.hw = 1;
       G = 4 * ncl;
       smem += recv;

@@ -131,6 +131,24 @@ def test_tiny_mixed_batch_greedy_bit_exact(cuda, graph):
     check_parity(TINY, w_d, w_ps, prompts, [i % 2 for i in range(8)], 32, cuda, graph)
 
 
+def test_cluster_chain_shapes_mixed_batch(cuda):
+    """8B-wide layer (hidden 4096, 32 q / 8 kv heads of 128) at batch 40: the decode
+    step runs the 4-CTA cluster chain with S = 4 DSMEM phases (O, gate_up, down: 32
+    tiles) and an S = 2 phase (QKV: 48 tiles), single- and two-chunk owners (bn = 48),
+    end to end vs the oracle."""
+    from dataclasses import replace
+
+    from paper_2603_02599_b200.spec import TINY
+    from paper_2603_02599_b200.weights import init_weights, perturb
+
+    spec = replace(TINY, name="wide", vocab=1024, hidden=4096, n_layers=1, n_q_heads=32, n_kv_heads=8, head_dim=128,
+                   ffn=2048, rope_theta=5e5, lm_head_std=0.0125)
+    w_d = init_weights(spec, seed=0)
+    w_ps = [perturb(spec, w_d, seed=1), perturb(spec, w_d, seed=2)]
+    prompts = make_prompts(40, spec.vocab, lo=8, hi=24)
+    check_parity(spec, w_d, w_ps, prompts, [i % 2 for i in range(40)], 8, cuda, graph=True)
+
+
 def _dequantized_decoder_weights(spec, w):
     """QSUN oracle: θ_d's linear layers as the exact bf16(q * s) operands of SUN-W4."""
     from oracle import quant_ref
