@@ -329,19 +329,23 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
     for (int j = 0; j < NC; ++j) stage_f32[j * kTileM + row_local] = v[j];
     epi_bar();
     if constexpr (EPI == EPI_SWIGLU) {
-      if (row_local < 64) {
-        const int jo = m_tile * 64 + row_local;
-        if (jo < a.n_valid_out) {
+      // rows 0..63 of the tile are gate, 64..127 up: all 128 threads produce outputs,
+      // thread t the output row t % 64 for half of the chunk's columns (t / 64) — the
+      // sigmoid's division was the epilogue's critical path on 64 threads
+      const int jl = row_local & 63;
+      const int jo = m_tile * 64 + jl;
+      if (jo < a.n_valid_out) {
+        const int j0 = (row_local >> 6) * (NC / 2);
 #pragma unroll
-          for (int j = 0; j < NC; ++j) {
-            const int b = c0 + j;
-            if (b < B) {
-              const float g = v[j];
-              const float u = stage_f32[j * kTileM + row_local + 64];
-              const float s = g / (1.f + expf(-g));
-              *reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<uint8_t*>(a.out_bf16) + act_offset(b, jo, a.bn)) =
-                  __float2bfloat16_rn(s * u);
-            }
+        for (int jj = 0; jj < NC / 2; ++jj) {
+          const int j = j0 + jj;
+          const int b = c0 + j;
+          if (b < B) {
+            const float g = stage_f32[j * kTileM + jl];
+            const float u = stage_f32[j * kTileM + jl + 64];
+            const float s = g / (1.f + expf(-g));
+            *reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<uint8_t*>(a.out_bf16) + act_offset(b, jo, a.bn)) =
+                __float2bfloat16_rn(s * u);
           }
         }
       }
