@@ -357,7 +357,7 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
         const int half = d >> 1;
         const int qd = a.n_q_heads * d;
         const int kd = a.n_kv_heads * d;
-        const int i = row % d;
+        const int i = row & (d - 1);  // head_dim is 64 or 128 (sun_decoder_create)
         const int fi = i < half ? i : i - half;
         const int partner = i < half ? row_local + half : row_local - half;
         const bool is_v = row >= qd + kd;
@@ -383,7 +383,7 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
           }
         } else {
           const int kvsel = is_v ? 1 : 0;
-          const int g = (row - qd - kvsel * kd) / d;
+          const int g = (row - qd - kvsel * kd) >> (d == 128 ? 7 : 6);
           const long long inner = ((static_cast<long long>(a.layer * 2 + kvsel) * a.n_kv_heads + g) * a.page_size) * d + i;
 #pragma unroll
           for (int j = 0; j < NC; ++j) {
@@ -391,7 +391,7 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
               const float o = is_v ? v[j] : (lo_half ? (v[j] * cs[j] - pv[j] * sn[j]) : (v[j] * cs[j] + pv[j] * sn[j]));
               const int pos = meta[(c0 + j) & 255];
               const int page = meta[256 + ((c0 + j) & 255)];
-              a.kv_base[static_cast<long long>(page) * a.page_stride + inner + static_cast<long long>(pos % a.page_size) * d] =
+              a.kv_base[static_cast<long long>(page) * a.page_stride + inner + static_cast<long long>(pos & 15) * d] =
                   __float2bfloat16_rn(o);
             }
           }
@@ -471,7 +471,7 @@ SUN_DEVICE void epi_preload(const GemmArgs& a, int m_tile, int row_local, int c0
     pr.p1[0] = (a.norm_w != nullptr && in) ? __bfloat162float(a.norm_w[row]) : 0.f;
   } else if constexpr (EPI == EPI_QKV_ROPE) {
     const int d = a.head_dim, half = d >> 1, qd = a.n_q_heads * d, kd = a.n_kv_heads * d;
-    const int i = row % d;
+    const int i = row & (d - 1);
     const int fi = i < half ? i : i - half;
     const bool is_v = row >= qd + kd;
     const int* meta = epi_meta(epi);
@@ -494,7 +494,7 @@ SUN_DEVICE void load_qkv_meta(const GemmArgs& a, float* epi) {  // epilogue grou
     for (int b = threadIdx.x - 64; b < a.bn; b += 128) {
       const int pos = b < a.batch ? a.positions[b] : 0;
       meta[b] = pos;
-      meta[256 + b] = b < a.batch ? a.block_tables[static_cast<long long>(b) * a.bt_stride + pos / a.page_size] : 0;
+      meta[256 + b] = b < a.batch ? a.block_tables[static_cast<long long>(b) * a.bt_stride + (pos >> 4)] : 0;  // 16-token pages
     }
   }
   if (a.ss_in != nullptr) {
