@@ -101,7 +101,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ.get("SUN_LIB", LIB_PATH))  # (SUN_LIB: A/B builds)
     if not p.exists():
         raise RuntimeError(
             f"{p} is missing: build it with `python -m paper_2603_02599_b200.build` "
