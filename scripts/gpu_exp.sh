@@ -1,4 +1,6 @@
 mkdir -p gpurun_out
-timeout 900 python scripts/scale_emulation.py --config c3 --out gpurun_out/scale_emulation_c3.json > gpurun_out/scale_c3.log 2>&1
-timeout 900 python scripts/scale_emulation.py --config c5 --cap 40 --reps 10 --out gpurun_out/scale_emulation_c5.json > gpurun_out/scale_c5.log 2>&1
-timeout 300 python scripts/step_timeline.py --config c3 --stamp 4 > gpurun_out/tl_c3_chain.txt 2>&1
+timeout 600 python -m pytest -q -x -m gpu tests/test_decode_parity_gpu.py > gpurun_out/pt_p8b.log 2>&1; echo "rc $?" >> gpurun_out/pt_p8b.log
+run() { tag=$1; shift; e=(); while [[ "$1" == *=* ]]; do e+=("$1"); shift; done; env "${e[@]}" timeout 300 python bench.py --steps 50 --no-cpu --no-e2e "$@" > gpurun_out/x_$tag.json 2>gpurun_out/x_$tag.err; }
+P=SUN_LIB=$PWD/paper_2603_02599_b200/libsun_b200_prev.so
+for r in a b c; do run c3new$r --config c3; run c3old$r $P --config c3; done
+run c2new --config c2; run c2old $P --config c2
