@@ -70,9 +70,34 @@ SUN_DEVICE PhaseSched phase_sched(const GemmArgs& a) {
 #define SUN_CSTAMP(i) \
   do { if (c.stamps) c.stamps[blockIdx.x * 16 + (i)] = gtimer(); } while (0)
 
+// Cross-CTA waits carry a watchdog: a grid that cannot become resident as a whole
+// (e.g. another persistent kernel holding SMs) traps after 2 s — the launch fails with
+// an error instead of hanging the GPU.
+constexpr unsigned long long kChainWatchdogNs = 2000000000ull;
+
 SUN_DEVICE void chain_wait_phase(const unsigned* bar, unsigned target) {
   if (target == 0) return;
-  while (ld_acquire_u32(bar) < target) __nanosleep(64);
+  const unsigned long long t0 = gtimer();
+  while (ld_acquire_u32(bar) < target) {
+    __nanosleep(64);
+    if (gtimer() - t0 > kChainWatchdogNs) __trap();
+  }
+}
+
+SUN_DEVICE void chain_wait_mbar(uint64_t* bar, uint32_t parity) {
+  const unsigned long long t0 = gtimer();
+  for (;;) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (gtimer() - t0 > kChainWatchdogNs) __trap();
+  }
 }
 
 SUN_DEVICE void epi_pair_bar() { asm volatile("bar.sync 4, 256;" ::: "memory"); }  // both epilogue groups
@@ -128,7 +153,7 @@ SUN_DEVICE void chain_epilogue_phase(const GemmArgs& a, const PhaseSched& ps, fl
       }
       // reduce our chunks: rank order, our own partial read from TMEM (same sums as
       // the L2 path: ((0 + p0) + p1) + ...)
-      mbar_wait(rbar, 0);
+      chain_wait_mbar(rbar, 0);
       auto reduce_own = [&](int c, int q0, auto& v) {
         constexpr int NQ = sizeof(v) / sizeof(float) / 4;
         float own[4 * NQ];
@@ -193,8 +218,9 @@ SUN_DEVICE void chain_epilogue_phase(const GemmArgs& a, const PhaseSched& ps, fl
       unsigned* tile_cnt = a.sk_flags + tile;
       if (threadIdx.x == 64) {
         atomicAdd(tile_cnt, 1u);
-        while (ld_acquire_u32(tile_cnt) < static_cast<unsigned>(S)) {
-        }
+        const unsigned long long t0 = gtimer();
+        while (ld_acquire_u32(tile_cnt) < static_cast<unsigned>(S))
+          if (gtimer() - t0 > kChainWatchdogNs) __trap();
       }
       epi_pair_bar();
       const float* gpart = a.sk_part + static_cast<long long>(blockIdx.x - rank) * a.bn * kTileM;
