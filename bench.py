@@ -370,17 +370,23 @@ def gpu_arm(args, cfg):
         h_bt = pin(bt.clone())
         h_pos = pin(torch.tensor(pos_now, dtype=torch.int32))
         out = pin(torch.zeros(B, dtype=torch.int32))
-        for i in range(2):  # warm the non-feedback graph
-            dec.decode(h_tok, h_pos, h_bt, pages_per_split=args.pps, graph=graph)
-            out.copy_(dec.next_tokens[:B])
+        for i in range(2):  # warm (the first call also captures the host-copy graph)
+            if graph:
+                dec.decode_host(h_tok, h_pos, h_bt, out, pages_per_split=args.pps)
+            else:
+                dec.decode(h_tok, h_pos, h_bt, pages_per_split=args.pps, graph=False)
+                out.copy_(dec.next_tokens[:B])
             h_pos += 1
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         te = time.perf_counter()
         for i in range(args.steps):
-            nt = dec.decode(h_tok, h_pos, h_bt, pages_per_split=args.pps, graph=graph)
-            out.copy_(nt)  # D2H read of the step's result (synchronises)
+            if graph:  # H2D inputs + step + D2H next tokens as one graph launch, then synchronise
+                dec.decode_host(h_tok, h_pos, h_bt, out, pages_per_split=args.pps)
+            else:
+                nt = dec.decode(h_tok, h_pos, h_bt, pages_per_split=args.pps, graph=False)
+                out.copy_(nt)  # D2H read of the step's result (synchronises)
             h_tok.copy_(out)
             h_pos += 1
         torch.cuda.synchronize()
@@ -391,7 +397,8 @@ def gpu_arm(args, cfg):
         e2e = {"value": float(tok_all.item()) / float(t_e.item()), "unit": "tokens/s",
                "h2d_bytes_per_step": int(h_tok.numel() * 4 + h_pos.numel() * 4 + h_bt.numel() * 4),
                "d2h_bytes_per_step": int(out.numel() * 4),
-               "api": "SharedDecodeModule.decode(host pinned tokens/positions/block_tables) -> next tokens"}
+               "api": ("SharedDecodeModule.decode_host(pinned tokens/positions/block_tables) -> pinned next tokens"
+                       if graph else "SharedDecodeModule.decode(host pinned tokens/positions/block_tables) -> next tokens")}
 
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu:

@@ -182,6 +182,42 @@ class SharedDecodeModule(_StepRunner):
             self._graphs[key] = g
         g.replay()
 
+    def decode_host(self, tokens: torch.Tensor, positions: torch.Tensor, block_tables: torch.Tensor,
+                    out: torch.Tensor, pages_per_split: int = 0) -> torch.Tensor:
+        """Eq. 3 from pinned host buffers as ONE graph launch: the inputs' host->device
+        copies, the step and the next tokens' device->host copy into pinned ``out``;
+        returns ``out`` once the stream has synchronised. The host buffers are baked
+        into the captured graph (keyed by their addresses): reuse the same buffers
+        from step to step, as a serving loop does."""
+        b = int(tokens.shape[0])
+        if b < 1:
+            raise ValueError("decode batch must be non-empty")
+        if b > self.max_batch:
+            raise ValueError(f"batch {b} > max_batch {self.max_batch}")
+        for t in (tokens, positions, block_tables, out):
+            if t.device.type != "cpu" or not t.is_pinned() or t.dtype != torch.int32:
+                raise ValueError("decode_host takes pinned int32 host tensors")
+        npg = int(block_tables.shape[1])
+        key = ("host", b, npg, pages_per_split, tokens.data_ptr(), positions.data_ptr(), block_tables.data_ptr(),
+               out.data_ptr())
+        g = self._graphs.get(key)
+        if g is None:  # first call: run the step on the ordinary path, then capture for the next ones
+            self.decode(tokens, positions, block_tables, pages_per_split)
+            out.copy_(self.next_tokens[:b])
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.tokens[:b].copy_(tokens, non_blocking=True)
+                self.positions[:b].copy_(positions, non_blocking=True)
+                self.block_tables[:b, :npg].copy_(block_tables, non_blocking=True)
+                self.launch(self.tokens, self.positions, self.block_tables, b, self.next_tokens, self.logits,
+                            pages_per_split)
+                out.copy_(self.next_tokens[:b], non_blocking=True)
+            self._graphs[key] = g
+            return out
+        g.replay()
+        torch.cuda.current_stream().synchronize()
+        return out
+
     def decode(self, tokens: torch.Tensor, positions: torch.Tensor, block_tables: torch.Tensor,
                pages_per_split: int = 0, graph: bool = True) -> torch.Tensor:
         """Eq. 3 over a batch: copy inputs (host or device) into the static

@@ -66,10 +66,18 @@ def run_gpu(spec, w_d, w_ps, prompts, module_of, n_steps, cuda, graph=True):
     for i, p in enumerate(pages):
         bt[i, :len(p)] = torch.tensor(p, dtype=torch.int32)
     logits = [first_logits]
+    if graph == "host":  # decode_host: persistent pinned buffers, one graph with the copies
+        h_tk, h_pos = torch.zeros(B, dtype=torch.int32).pin_memory(), torch.zeros(B, dtype=torch.int32).pin_memory()
+        h_bt, h_out = bt.clone().pin_memory(), torch.zeros(B, dtype=torch.int32).pin_memory()
     for t in range(n_steps):
         tk = torch.tensor([x[-1] for x in toks], dtype=torch.int32)
         pos = torch.tensor([len(p) + t for p in prompts], dtype=torch.int32)
-        nxt = dec.decode(tk, pos, bt, graph=graph).cpu()
+        if graph == "host":
+            h_tk.copy_(tk)
+            h_pos.copy_(pos)
+            nxt = dec.decode_host(h_tk, h_pos, h_bt, h_out).clone()
+        else:
+            nxt = dec.decode(tk, pos, bt, graph=graph).cpu()
         logits.append(dec.logits[:B].cpu().clone())
         for i in range(B):
             toks[i].append(int(nxt[i]))
@@ -120,7 +128,7 @@ def check_parity(spec, w_d, w_ps, prompts, module_of, n_steps, cuda, graph=True,
     return worst, exempt, total
 
 
-@pytest.mark.parametrize("graph", [False, True])
+@pytest.mark.parametrize("graph", [False, True, "host"])
 def test_tiny_mixed_batch_greedy_bit_exact(cuda, graph):
     from paper_2603_02599_b200.spec import TINY
     from paper_2603_02599_b200.weights import init_weights, perturb
