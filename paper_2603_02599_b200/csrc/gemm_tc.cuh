@@ -732,6 +732,14 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
   const int nseg = n > 0 ? (u1 - 1) / KS - t_first + 1 : 0;
   const uint32_t ncols = W4 ? 512u : tmem_cols_for(a.bn);
   const int nbuf = acc_buffers(a.bn, W4);
+  // W4: converter warps 7..10 (TMEM lane groups 3, 0, 1, 2) become epilogue group B for
+  // this CTA's last segment once their conversions are done (not under stream-K)
+  const bool w4join = W4 && a.sk_units == 0;
+  auto last_full_tile = [&]() {
+    if (nseg == 0) return false;
+    const int t = t_first + nseg - 1;
+    return max(u0, t * KS) - t * KS == 0 && min(u1, (t + 1) * KS) - t * KS == KS;
+  };
   // W4: each converter / MMA iteration covers kp K blocks (2 when bn <= 128: halves the
   // per-block hand-off overhead that bounded the pipeline); A slot i = 64 kp TMEM
   // columns ending at column 512 - 64 kp i
@@ -984,7 +992,9 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
       if (threadIdx.x == 64 && seg == 0) SUN_STAMP(4);
       const uint32_t taddr = tmem_base + static_cast<uint32_t>(buf * a.bn) + (static_cast<uint32_t>(q * 32) << 16);
       if (!clustered) {
-        if (kb == 0 && ke == KS) direct_epilogue<EPI>(a, tile, taddr, epi, W4 ? 1 : 2);
+        const bool join = w4join && seg == nseg - 1 && kb == 0 && ke == KS;
+        if (join) asm volatile("bar.sync 4, 256;" ::: "memory");  // group B (converters) joins
+        if (kb == 0 && ke == KS) direct_epilogue<EPI>(a, tile, taddr, epi, (W4 && !join) ? 1 : 2);
         else if (epi_grp() == 0 && kb > 0) sk_store_partial(a, taddr, row_local);  // stream-K: group A only
         else if (epi_grp() == 0) sk_owner_epilogue<EPI>(a, tile, taddr, row_local, epi, stg, skbar);
         tc_fence_before();
@@ -1054,6 +1064,16 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
       seg_left -= nbk;
       if (seg_left == 0) seg_left = min(KS, n - j);
     }
+    if (w4join && !clustered && warp >= 7 && warp < 11 && last_full_tile()) {
+      // epilogue group B for the last tile: chunks alternate with group A
+      asm volatile("bar.sync 4, 256;" ::: "memory");
+      const int seg = nseg - 1, buf = seg % nbuf;
+      mbar_wait(&tfull[buf], (seg / nbuf) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + static_cast<uint32_t>(buf * a.bn) + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+      direct_epilogue<EPI>(a, t_first + seg, taddr, epi, 2);
+      tc_fence_before();
+    }
   }
 
   if (clustered) {
@@ -1090,7 +1110,7 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
       cluster_sync_all();  // every rank's partial is visible cluster-wide
     }
     if (threadIdx.x == 64) SUN_STAMP(9);
-    if ((warp >= 2 && warp < 6) || (!W4 && warp >= 7)) {
+    if ((warp >= 2 && warp < 6) || ((!W4 || w4join) && warp >= 7 && warp < 11)) {
       const int q = warp & 3;
       const int row_local = q * 32 + (threadIdx.x & 31);
       float* part = reinterpret_cast<float*>(smem);
@@ -1129,7 +1149,7 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
         }
       };
       const int nmine = (a.bn / 16 - static_cast<int>(rank) + static_cast<int>(S) - 1) / static_cast<int>(S);
-      if (!W4 && nmine == 1) {
+      if ((!W4 || w4join) && nmine == 1) {
         // one 16-column chunk for this rank: each epilogue group takes 8 columns
         const int c0 = static_cast<int>(rank) * 16 + 8 * epi_grp();
         float v[8];
@@ -1139,7 +1159,7 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
         else epi_chunk<EPI, 8>(a, t_first, row_local, c0, v, epi);
         if (threadIdx.x == 64) SUN_STAMP(11);
       } else {
-        const int ng = W4 ? 1 : 2;  // the rank's chunks alternate between the epilogue groups
+        const int ng = (W4 && !w4join) ? 1 : 2;  // the rank's chunks alternate between the epilogue groups
         for (int c0 = static_cast<int>(rank + S * epi_grp()) * 16; c0 < a.bn; c0 += static_cast<int>(S * ng) * 16) {
           float v[16];
           reduce_cols(c0, 0, v);
