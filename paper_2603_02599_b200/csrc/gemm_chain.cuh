@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_chain_kernel(const __gri
         case EPI_RESID_ADD: chain_epilogue_phase<EPI_RESID_ADD>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase, recv, &rbar[p]); break;
         case EPI_SWIGLU: chain_epilogue_phase<EPI_SWIGLU>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase, recv, &rbar[p]); break;
         case EPI_QKV_ROPE: chain_epilogue_phase<EPI_QKV_ROPE>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase, recv, &rbar[p]); break;
-        default: chain_epilogue_phase<EPI_STORE_F32>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase, recv, &rbar[p]); break;
+        default: __trap();  // the layer chain's phases are O / gate_up / down / QKV
       }
       epi_pair_bar();
       if (threadIdx.x == 64) {  // this CTA's outputs of phase p are written
