@@ -673,7 +673,9 @@ int auto_pages_per_split(const SunDecoderDims& d, int batch) {
   // pages (128 tokens) so a unit amortises its TMA ramp.
   const int max_pages = (d.max_context + kPageTokens - 1) / kPageTokens;
   const long long pairs = (long long)batch * d.n_kv_heads;
-  if (pairs >= 3LL * kNumSms && d.head_dim == 128) return max_pages;  // (d = 64: C2 0.99 vs 0.96 ms split)
+  // (d = 64 was split-faster before the attention prestaged its pages: C2 0.99 vs 0.96 ms;
+  // now unsplit wins there too, 1.541 vs 1.566 ms)
+  if (pairs >= 3LL * kNumSms) return max_pages;
   const long long want_units = 8LL * kNumSms;
   long long splits = (want_units + pairs - 1) / pairs;
   if (splits < 1) splits = 1;
