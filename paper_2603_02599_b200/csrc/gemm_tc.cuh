@@ -52,7 +52,7 @@ enum EpiKind : int {
 struct GemmArgs {
   const uint8_t* wblk;     // bf16 weights, SUN-BLK
   const uint8_t* w4_packed;  // QSUN: SUN-W4 packed int4 (tile-contiguous 128x64 B blocks)
-  const __nv_bfloat16* w4_scales;  // QSUN: [k/128][m_tiles*128]
+  const __nv_bfloat16* w4_scales;  // QSUN: tile-major [m_tiles][k/128][128]
   const uint8_t* xact;     // activations, SUN-ACT with bn rows per atom
   int n_out;         // rows of W (incl. zero padding rows for SWIGLU)
   int k;             // reduction length

@@ -2,7 +2,8 @@
 //
 // Storage format "SUN-W4" (restated bit-for-bit by oracle/quant_ref.py):
 //   * symmetric per-group quantisation along K, group = 128, one bf16 scale per
-//     (group, row) stored group-major: scales[K/128][round_up(rows,128)];
+//     (group, row) stored tile-major: scales[row tile][K/128][128], so the scales of
+//     one weight stage (consecutive K blocks of a tile) are one contiguous run;
 //   * q = clamp(rint(w / s), -8, 7), s = bf16(absmax / 7.5) (s = 0 -> q = 0);
 //   * packed bytes are tile-contiguous: block (row/128, k/128) is 8 KB (one bulk copy
 //     per stage) laid out [chunk 4][row 128][16 B], chunk c = k 32c..32c+31 of the row

@@ -22,6 +22,7 @@ from dataclasses import asdict, dataclass
 from typing import Iterable, Protocol
 
 import bisect
+import csv
 import json
 
 import numpy as np
@@ -139,6 +140,115 @@ class AnalyticBackend:
 
     def step_time(self, total_kv_bytes: float, decoder_weight_bytes: float, batch: int | None = None) -> float:
         return decode_step_time_from_totals(total_kv_bytes, decoder_weight_bytes, self.params, self.gpu)
+
+
+# --------------------------------------------------------------------------- calibration (costmodel.py:186-358)
+FLOPS_PER_PARAM = 2.0
+
+
+def single_request_ttft(model: ModelProfile, isl: int, params: CostParams, gpu: GpuSpec) -> float:
+    """Closed-form TTFT of an unqueued single request: prefill + transfer (costmodel.py:186-191)."""
+    kv = KvHandle(request_id=-1, resident_tokens=isl, bytes_per_token=model.kv_bytes_per_token)
+    return prefill_time(model, isl, params, gpu) + transfer_time(kv, gpu)
+
+
+@dataclass(frozen=True)
+class CalibrationTarget:
+    """One measured concurrency-1 operating point (costmodel.py:194-210)."""
+
+    param_count: float
+    kv_bytes_per_token: int
+    prefill_bits: int
+    decode_bits: int
+    isl: int
+    osl: int
+    ttft_s: float | None = None
+    tpot_s: float | None = None
+    label: str = ""
+
+
+def load_targets_csv(path: str, param_count: float, kv_bytes_per_token: int) -> list[CalibrationTarget]:
+    """costmodel.py:213-243: columns model, prefill_bits, decode_bits, isl, osl,
+    concurrency, ttft_ms, tpot_ms; rows at concurrency != 1 are skipped."""
+    out = []
+    with open(path, newline="") as fh:
+        for row in csv.DictReader(fh):
+            if int(row["concurrency"]) != 1:
+                continue
+            ttft, tpot = row.get("ttft_ms", "").strip(), row.get("tpot_ms", "").strip()
+            out.append(CalibrationTarget(param_count=param_count, kv_bytes_per_token=kv_bytes_per_token,
+                                         prefill_bits=int(row["prefill_bits"]), decode_bits=int(row["decode_bits"]),
+                                         isl=int(row["isl"]), osl=int(row["osl"]),
+                                         ttft_s=float(ttft) / 1000.0 if ttft else None,
+                                         tpot_s=float(tpot) / 1000.0 if tpot else None, label=row.get("model", "")))
+    return out
+
+
+def _target_profile(t: CalibrationTarget) -> ModelProfile:
+    return ModelProfile(model_id=0, param_count=t.param_count, prefill_weight_bits=t.prefill_bits,
+                        decode_weight_bits=t.decode_bits, kv_bytes_per_token=t.kv_bytes_per_token)
+
+
+def calibrate(targets: list[CalibrationTarget], gpu: GpuSpec, rel_tol: float = 0.03) -> CostParams:
+    """The reference's fit (costmodel.py:257-358): closed-form least squares of
+    TTFT - transfer = F + c*isl (c -> penalised q for low-bit prefill) and of
+    TPOT = D + beta * (W + mean resident KV bytes); mfu / mbu from the slopes;
+    ``CalibrationInfeasible`` on too few targets, unphysical constants or a
+    target reproduced worse than rel_tol. ``calibrate_decode`` below refits the
+    decode half to B200-measured whole steps instead."""
+    if len(targets) < 2:
+        raise CalibrationInfeasible("need at least 2 targets spanning both precisions")
+    ttft_rows = [t for t in targets if t.ttft_s is not None]
+    tpot_rows = [t for t in targets if t.tpot_s is not None]
+    if not ttft_rows or not tpot_rows:
+        raise CalibrationInfeasible("targets must include at least one TTFT and one TPOT")
+    lowbit = any(t.prefill_bits < 16 for t in ttft_rows)
+    a = np.zeros((len(ttft_rows), 3 if lowbit else 2))
+    z = np.zeros(len(ttft_rows))
+    for i, t in enumerate(ttft_rows):
+        z[i] = t.ttft_s - transfer_time(KvHandle(request_id=-1, resident_tokens=t.isl,
+                                                 bytes_per_token=t.kv_bytes_per_token), gpu)
+        a[i, 0] = 1.0
+        a[i, 2 if t.prefill_bits < 16 else 1] = t.isl
+    sol, *_ = np.linalg.lstsq(a, z, rcond=None)
+    overhead_p, per_token = float(sol[0]), float(sol[1])
+    penalty = float(sol[2] / sol[1]) if lowbit and sol[1] != 0 else 1.0
+    a2 = np.zeros((len(tpot_rows), 2))
+    y2 = np.zeros(len(tpot_rows))
+    for i, t in enumerate(tpot_rows):
+        a2[i] = (1.0, t.param_count * t.decode_bits / 8.0 + mean_decode_resident_tokens(t.isl, t.osl)
+                 * t.kv_bytes_per_token)
+        y2[i] = t.tpot_s
+    sol2, *_ = np.linalg.lstsq(a2, y2, rcond=None)
+    overhead_d, beta = float(sol2[0]), float(sol2[1])
+    if per_token <= 0 or beta <= 0:
+        raise CalibrationInfeasible("targets imply non-positive per-token cost; check TTFT/TPOT orderings")
+    flops_per_token = FLOPS_PER_PARAM * targets[0].param_count
+    mfu = flops_per_token / (per_token * gpu.flops)
+    if mfu > 1.0:
+        mfu, flops_per_token = 1.0, per_token * gpu.flops
+    mbu = 1.0 / (beta * gpu.hbm_bandwidth)
+    if mbu > 1.0:
+        raise CalibrationInfeasible(f"decode targets imply {1.0 / beta:.3e} B/s effective bandwidth, above "
+                                    f"the GPU peak {gpu.hbm_bandwidth:.3e} B/s")
+    params = CostParams(prefill_flops_per_token=flops_per_token, prefill_fixed_overhead=overhead_p,
+                        decode_fixed_overhead=overhead_d, dequant_compute_penalty=max(penalty, 1.0), mfu=mfu, mbu=mbu)
+    problems = params.validate()
+    if problems:
+        raise CalibrationInfeasible("fit produced invalid parameters: " + "; ".join(problems))
+    res = []
+    for t in targets:
+        prof = _target_profile(t)
+        name = t.label or f"{t.prefill_bits}/{t.decode_bits}@isl{t.isl}"
+        if t.ttft_s is not None:
+            res.append((f"{name}.ttft", (single_request_ttft(prof, t.isl, params, gpu) - t.ttft_s) / t.ttft_s))
+        if t.tpot_s is not None:
+            res.append((f"{name}.tpot", (single_request_tpot(prof, t.isl, t.osl, params, gpu) - t.tpot_s) / t.tpot_s))
+    worst = max(abs(e) for _, e in res)
+    if worst > rel_tol:
+        raise CalibrationInfeasible(f"best fit misses tolerance {rel_tol:.1%} (worst {worst:.2%})",
+                                    residuals=sorted(res, key=lambda r: -abs(r[1])))
+    return params
 
 
 # --------------------------------------------------------------------------- harness closure

@@ -125,8 +125,25 @@ class GpuSpec:
         return [f"{path}.{n}: must be > 0, got {getattr(self, n)}" for n in _GPU_FIELDS if not getattr(self, n) > 0]
 
     @classmethod
-    def b200(cls, hbm_gbs: float = 6548.2, bf16_tflops: float = 1667.2) -> "GpuSpec":
-        """Measured B200 (MEASURED_PEAKS.json) with NVLink-5 peer copy 770 GB/s."""
+    def b200(cls, hbm_gbs: float | None = None, bf16_tflops: float | None = None,
+             peaks_path: str | None = None) -> "GpuSpec":
+        """B200 with the driver-measured HBM copy bandwidth and bf16 GEMM burst
+        (MEASURED_PEAKS.json at the repo root; B200_PROFILING.md's fallback 6.65 TB/s
+        and 1.59 PFLOP/s when absent), NVLink-5 peer copy 770 GB/s, 180 GB."""
+        import json
+        import os
+
+        if hbm_gbs is None or bf16_tflops is None:
+            path = peaks_path or os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                              "MEASURED_PEAKS.json")
+            try:
+                with open(path) as f:
+                    peaks = json.load(f)
+                m_hbm, m_tf = float(peaks["hbm_gbs"]), float(peaks["bf16_tflops"])
+            except (OSError, KeyError, ValueError):
+                m_hbm, m_tf = 6650.0, 1590.0
+            hbm_gbs = m_hbm if hbm_gbs is None else hbm_gbs
+            bf16_tflops = m_tf if bf16_tflops is None else bf16_tflops
         return cls(flops=bf16_tflops * 1e12, hbm_bandwidth=hbm_gbs * 1e9, hbm_capacity=1.8e11,
                    interconnect_bandwidth=7.7e11, interconnect_latency=1.0e-5)
 

@@ -29,12 +29,13 @@ sys.dont_write_bytecode = True
 sys.path.insert(0, "/root/reference/pkg/src")
 
 import poolsim  # noqa: E402
-from poolsim import engine, routing  # noqa: E402
+from poolsim import engine, metrics, routing  # noqa: E402
 from poolsim.costmodel import (CostParams, decode_step_time, single_request_tpot,  # noqa: E402
                                transfer_time)
 from poolsim.domain import (ClusterConfig, DecodeRule, GpuSpec, InvalidConfig, KvHandle,  # noqa: E402
                             ModelProfile, PoolMode, Request, RoutingPolicy, validate_cluster)
-from poolsim.workload import ArrivalProcess, WorkloadSpec, generate_trace, write_trace, zipf_split  # noqa: E402
+from poolsim.workload import (ArrivalProcess, WorkloadSpec, generate_trace, measurement_filter,  # noqa: E402
+                              write_trace, zipf_split)
 
 OUT = os.path.dirname(os.path.abspath(__file__))
 
@@ -102,7 +103,7 @@ def engine_cases():
 
         routing.DecodeDispatcher.route = spy
         try:
-            res = engine.run(cluster, trace, SIMPLE_COST)
+            res = engine.run(cluster, trace, SIMPLE_COST, record_events=True)
         finally:
             routing.DecodeDispatcher.route = orig
         log = res.resource_log
@@ -114,6 +115,8 @@ def engine_cases():
             "steps": [[w, b, kvb] for (w, _t, _d, b, kvb) in log.steps],
             "charged_steps": log.charged_steps,
             "n_requests": len(trace),
+            "events": [[round(t * 1e9), k.name, rid, wid] for (t, k, rid, wid) in res.event_trace],
+            "summary": metrics.summarize(measurement_filter(res.completed, ws), cluster, ws).to_dict(),
         })
     return out
 
@@ -130,7 +133,18 @@ def costmodel_values():
           for t, b in ((1, 131072), (1024, 131072), (16384, 196608))]
     tp = [{"isl": i, "osl": o, "bits": m.decode_weight_bits, "tpot": single_request_tpot(m, i, o, SIMPLE_COST, SIMPLE_GPU)}
           for m in (m16, m4) for i, o in ((1024, 8), (512, 256))]
-    return {"decode_step_time": vals, "transfer_time": tr, "single_request_tpot": tp}
+    # calibrate() on the shipped A100 targets (pkg/configs/targets_llama8b.csv) and on a
+    # subset it cannot fit (CalibrationInfeasible); the CSV text travels in the fixture
+    from poolsim.costmodel import CalibrationInfeasible, calibrate, load_targets_csv
+    csv_path = "/root/reference/pkg/configs/targets_llama8b.csv"
+    targets = load_targets_csv(csv_path, 8.03e9, 131072)
+    cal = {"csv": open(csv_path).read(), "param_count": 8.03e9, "kv_bytes_per_token": 131072,
+           "params": calibrate(targets, GpuSpec()).to_dict()}
+    try:
+        calibrate(targets, GpuSpec(), rel_tol=0.001)
+    except CalibrationInfeasible as e:
+        cal["tight_error"] = str(e)
+    return {"decode_step_time": vals, "transfer_time": tr, "single_request_tpot": tp, "calibrate": cal}
 
 
 def workload_values():

@@ -41,6 +41,45 @@ def test_costmodel_values_match_reference():
         assert pricing.single_request_tpot(m, case["isl"], case["osl"], SIMPLE_COST, SIMPLE_GPU) == case["tpot"]
 
 
+def test_calibrate_matches_reference(tmp_path):
+    """pricing.calibrate on the reference's shipped A100 targets gives the reference's
+    CostParams exactly (costmodel.py:257-358; the A100 constants of
+    cluster_shared.toml:38-44), and a tolerance it cannot meet raises
+    CalibrationInfeasible with the same residual report."""
+    import paper_2603_02599_b200 as sun
+
+    g = json.load(open(os.path.join(GOLDEN, "engine_golden.json")))["costmodel"]["calibrate"]
+    path = tmp_path / "targets.csv"
+    path.write_text(g["csv"])
+    targets = sun.load_targets_csv(str(path), g["param_count"], g["kv_bytes_per_token"])
+    params = sun.calibrate(targets, sun.GpuSpec())
+    assert params.to_dict() == g["params"]
+    with pytest.raises(sun.CalibrationInfeasible) as ei:
+        sun.calibrate(targets, sun.GpuSpec(), rel_tol=0.001)
+    assert str(ei.value) == g["tight_error"]
+    with pytest.raises(sun.CalibrationInfeasible):
+        sun.calibrate(targets[:1], sun.GpuSpec())
+
+
+def test_package_root_names_cover_reference_api():
+    """poolsim.__all__ (pkg/src/poolsim/__init__.py:49-94) minus the out-of-scope
+    config / sweep names is importable from the package root."""
+    import paper_2603_02599_b200 as sun
+
+    ref_all = ["ArrivalProcess", "CalibrationInfeasible", "CalibrationTarget", "ClusterConfig", "CostParams",
+               "DecodeDispatcher", "DecodeRule", "EmptyPool", "EmptyWindow", "GpuSpec", "IncompleteRequest",
+               "InvalidConfig", "KvHandle", "MixedDecoderError", "ModelProfile", "PoolMode", "PoolSnapshot", "Request",
+               "RequestOutcome", "RoutingPolicy", "RunConfig", "RunSummary", "SimResult", "SimulationDiverged",
+               "SweepSpec", "UnknownModel", "WorkerRole", "WorkerState", "WorkloadSpec", "calibrate",
+               "decode_step_time", "generate_trace", "load_config", "measurement_filter", "per_request_metrics",
+               "prefill_time", "route_prefill", "run", "run_single", "run_sweep", "summarize", "transfer_time",
+               "validate_cluster", "zipf_split"]
+    out_of_scope = {"RunConfig", "SweepSpec", "load_config", "run_single", "run_sweep"}
+    for name in ref_all:
+        if name not in out_of_scope:
+            assert name in sun.__all__ and hasattr(sun, name), name
+
+
 def test_decode_step_time_errors_like_reference():
     a = ModelProfile(0, 8.03e9)
     b = ModelProfile(1, 8.03e9, decode_weight_bits=4)

@@ -44,6 +44,27 @@ def test_replay_matches_reference_engine_exactly():
         assert res.log.charged_steps == run["charged_steps"]
 
 
+def test_event_trace_and_summary_match_reference_engine():
+    """record_events=True gives the reference's event trace (engine.py:71-81, 301-303)
+    entry for entry, and summarize(window, cluster, spec) (metrics.py:102-150) the
+    reference's RunSummary field for field, on the same runs."""
+    from paper_2603_02599_b200.stats import summarize
+    from paper_2603_02599_b200.trace import measurement_filter
+
+    runs = json.load(open(os.path.join(GOLDEN, "engine_golden.json")))["runs"]
+    for run in runs:
+        sp = run["spec"]
+        cfg = cluster(sp["n_models"], sp["pool"], DecodeRule(sp["rule"]))
+        ws = WorkloadSpec(n_models=sp["n_models"], total_rps=sp["rps"], alpha=sp["alpha"], isl=sp["isl"],
+                          osl=sp["osl"], grace_period=1.0, measurement_window=4.0, seed=42)
+        res = scheduler.run(cfg, generate_trace(ws), COST, None, None, True)
+        assert res.resource_log is res.log
+        got = [[round(t * 1e9), k.name, rid, wid] for (t, k, rid, wid) in res.event_trace]
+        assert got == run["events"], sp
+        summ = summarize(measurement_filter(res.completed, ws), cfg, ws).to_dict()
+        assert summ == run["summary"], sp
+
+
 def test_single_request_chain_closed_form():
     cfg = cluster(1, 1, DecodeRule.LEAST_OUTSTANDING_TOKENS)
     m = cfg.models[0]
