@@ -93,7 +93,7 @@ def rope(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor:
 
 def argmax_lowest(logits: torch.Tensor) -> torch.Tensor:
     m = logits.max(dim=-1, keepdim=True).values
-    idx = torch.arange(logits.shape[-1]).expand_as(logits)
+    idx = torch.arange(logits.shape[-1], device=logits.device).expand_as(logits)
     return torch.where(logits == m, idx, torch.full_like(idx, logits.shape[-1])).min(dim=-1).values
 
 
@@ -104,12 +104,24 @@ class OracleDecoder:
     ffn_norm, wg [f,h], wu [f,h], wd [h,f].
     """
 
-    def __init__(self, spec: OracleSpec, weights: dict, max_pos: int, round_bf16: bool = True):
+    def __init__(self, spec: OracleSpec, weights: dict, max_pos: int, round_bf16: bool = True,
+                 device: str | torch.device = "cpu"):
         """round_bf16=False drops every bf16 storage rounding (pure fp32 model), the
-        mode used to pin the block definition against transformers' Llama / Qwen2."""
+        mode used to pin the block definition against transformers' Llama / Qwen2.
+
+        device: where the same fp32 arithmetic runs. "cpu" is the oracle proper;
+        the BASELINE-shape parity tests (contexts up to 16k, ~1e14 flop of prefill)
+        run these very torch ops on a CUDA device with TF32 disabled (fp32 cuBLAS /
+        elementwise, nothing from libsun_b200.so), pinned equal to the CPU run by
+        tests/test_oracle_device_gpu.py."""
         self.s = spec
-        self.w = {k: (v.float() if torch.is_tensor(v) else v) for k, v in weights.items()}
-        self.cos, self.sin = rope_tables(max_pos, spec.head_dim, spec.rope_theta)
+        self.dev = torch.device(device)
+        if self.dev.type == "cuda":
+            torch.backends.cuda.matmul.allow_tf32 = False
+            torch.backends.cudnn.allow_tf32 = False
+        self.w = {k: (v.to(self.dev).float() if torch.is_tensor(v) else v) for k, v in weights.items()}
+        cos, sin = rope_tables(max_pos, spec.head_dim, spec.rope_theta)
+        self.cos, self.sin = cos.to(self.dev), sin.to(self.dev)
         self.rnd = bf if round_bf16 else (lambda x: x)
 
     # -- one layer over T new positions of one sequence ------------------------------
@@ -134,11 +146,13 @@ class OracleDecoder:
         kcache[l], vcache[l] = K, V
         G = nq // nkv
         n_past = K.shape[0] - T
-        out = torch.empty(T, nq, d)
+        out = torch.empty(T, nq, d, device=self.dev)
+        causal = (torch.arange(K.shape[0], device=self.dev)[None, :] >
+                  (n_past + torch.arange(T, device=self.dev))[:, None]) if T > 1 else None
         for h in range(nq):
             sc = (q[:, h, :] @ K[:, h // G, :].t()) / math.sqrt(d)  # [T, ctx]
-            causal = torch.arange(K.shape[0])[None, :] > (n_past + torch.arange(T))[:, None]
-            sc = sc.masked_fill(causal, float("-inf"))
+            if causal is not None:
+                sc = sc.masked_fill(causal, float("-inf"))
             out[:, h, :] = torch.softmax(sc, dim=-1) @ V[:, h // G, :]
         attn = self.rnd(out.reshape(T, nq * d))
         resid = resid + attn @ w[f"l{l}.wo"].t()
@@ -157,8 +171,8 @@ class OracleDecoder:
         s, w = self.s, self.w
         if cache is None:
             cache = {"k": [None] * s.n_layers, "v": [None] * s.n_layers}
-        pos = torch.arange(start, start + len(tokens))
-        resid = w["embed"][torch.tensor(tokens)].clone()
+        pos = torch.arange(start, start + len(tokens), device=self.dev)
+        resid = w["embed"][torch.tensor(tokens, device=self.dev)].clone()
         for l in range(s.n_layers):
             resid = self._layer(l, resid, pos, cache["k"], cache["v"])
         xg, r = norm_factored(resid[-1:], w["final_norm"], s.rms_eps, self.rnd)

@@ -29,6 +29,14 @@ class DecoderSpec:
     group_size: int = 128
     init_std: float = 0.02
     lm_head_std: float = 0.02
+    # margin-engineered greedy (parity tests, SURVEY §7 hard part (b)): embedding rows
+    # ~ N(0, embed_std) and lm_head row v = N(0, lm_head_std) + greedy_margin / (hidden *
+    # embed_std) * embed[perm[v]] for a seeded permutation perm, so the logit of token
+    # perm^-1(x) carries ~greedy_margin * rho (rho = embed_std / rms(final residual)) on
+    # top of the random part: greedy decisions are far from ties while every logit still
+    # depends on the whole layer stack. 0 = plain random init.
+    embed_std: float | None = None
+    greedy_margin: float = 0.0
 
     @property
     def kv_bytes_per_token(self) -> int:

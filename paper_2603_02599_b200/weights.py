@@ -32,7 +32,8 @@ def init_weights(spec: DecoderSpec, seed: int = 0, device: str | torch.device = 
     h, d = spec.hidden, spec.head_dim
     qd, kd = spec.n_q_heads * d, spec.n_kv_heads * d
     s = spec.init_std
-    w = {"embed": _randn((spec.vocab, h), g, dev, s)}
+    es = spec.embed_std if spec.embed_std is not None else s
+    w = {"embed": _randn((spec.vocab, h), g, dev, es)}
     for l in range(spec.n_layers):
         w[f"l{l}.attn_norm"] = (1 + _randn((h,), g, dev, 0.02).float()).to(BF16)
         w[f"l{l}.wq"] = _randn((qd, h), g, dev, s)
@@ -49,6 +50,15 @@ def init_weights(spec: DecoderSpec, seed: int = 0, device: str | torch.device = 
         w[f"l{l}.wd"] = _randn((h, spec.ffn), g, dev, s)
     w["final_norm"] = torch.ones(h, dtype=BF16, device=dev)
     w["lm_head"] = w["embed"] if spec.tie_embeddings else _randn((spec.vocab, h), g, dev, spec.lm_head_std)
+    if spec.greedy_margin > 0:
+        if spec.tie_embeddings:
+            raise ValueError("greedy_margin needs an untied lm_head")
+        gp = torch.Generator(device=dev).manual_seed(seed * 7919 + 17)
+        perm = torch.randperm(spec.vocab, generator=gp, device=dev)
+        c = spec.greedy_margin / (h * es)
+        for i in range(0, spec.vocab, 8192):  # chunked: bounded fp32 temporaries at V ~ 150k
+            j = min(i + 8192, spec.vocab)
+            w["lm_head"][i:j] = (w["lm_head"][i:j].float() + c * w["embed"][perm[i:j]].float()).to(BF16)
     return w
 
 

@@ -136,6 +136,39 @@ def test_attention_decode_matches_fp32(cuda, d, nq, nkv, pps):
         torch.testing.assert_close(out.float().cpu(), ref, rtol=1e-2, atol=2e-3)
 
 
+@pytest.mark.parametrize("d,nq,nkv", [(64, 32, 8), (128, 32, 8), (128, 40, 8)])
+@pytest.mark.parametrize("pps", [0, 8, 37, 1024])
+def test_attention_decode_long_context(cuda, d, nq, nkv, pps):
+    """Contexts of the BASELINE configs (C4 ~4k, C5 ~16k) with many splits: pps 8 gives
+    up to 128 splits of one sequence merged by the split combine (online-softmax LSE
+    merge over 1,000+ pages), 37 an odd split boundary, 1024 one split."""
+    from paper_2603_02599_b200 import _lib, kernels
+
+    L, max_ctx = 1, 16400
+    ctxs = [16384, 4096, 4095, 9001, 16383, 1, 2049]
+    B = len(ctxs)
+    maxp = (max_ctx + 15) // 16
+    num_pages = sum((c + 15) // 16 for c in ctxs) + 4
+    g = torch.Generator(device="cpu").manual_seed(d * 3 + nq + pps)
+    pool = (torch.randn(num_pages, L, 2, nkv, 16, d, generator=g) * 1.5).to(torch.bfloat16)
+    perm = torch.randperm(num_pages, generator=g)
+    bt = torch.zeros(B, maxp, dtype=torch.int32)
+    used = 0
+    for b, c in enumerate(ctxs):
+        n = (c + 15) // 16
+        bt[b, :n] = perm[used:used + n].to(torch.int32)
+        used += n
+    positions = torch.tensor([c - 1 for c in ctxs], dtype=torch.int32)
+    q = (torch.randn(B, nq, d, generator=g) * 1.5).to(torch.bfloat16)
+    dims = _lib.SunDecoderDims(vocab=16, hidden=256, n_layers=L, n_q_heads=nq, n_kv_heads=nkv, head_dim=d,
+                               ffn=256, page_size=16, max_context=max_ctx, weight_bits=16, group_size=128,
+                               qkv_bias=0, rms_eps=1e-5)
+    out = kernels.attention_decode(dims, pool.to(cuda), 0, q.to(cuda), positions.to(cuda), bt.to(cuda),
+                                   pages_per_split=pps)
+    ref = _attn_ref(q, pool, 0, positions, bt, nq // nkv)
+    torch.testing.assert_close(out.float().cpu(), ref, rtol=1e-2, atol=2e-3)
+
+
 def test_rmsnorm_matches_fp32(cuda):
     from paper_2603_02599_b200 import kernels
 

@@ -1,0 +1,53 @@
+"""BASELINE-shape end-to-end parity on the B200 (see tests/parity_harness.py).
+
+C2: Llama-3.2-1B widths, all 16 layers, head_dim 64, 4 prefill modules, batch 64,
+    context ~2k.
+C3: Llama-3.1-8B widths (2 of 32 layers), 8 prefill modules, batch 64, context
+    1024-1279.
+C4: QSUN W4A16 g128 decoder at 8B widths (2 layers), bf16 prefill modules,
+    batch 128, context ~4k.
+C5: Qwen2.5-14B widths with QKV bias, GQA group 5 (2 layers), 16 prefill modules,
+    batch 32, context ~16k (split-K attention over ~1,000 pages).
+Every case: full vocabulary, >= 2 decode steps, margin-engineered greedy asserted
+token-for-token with zero near-tie exemptions, logits max-abs <= 2e-2.
+"""
+import random
+
+import pytest
+import torch
+
+from tests.parity_harness import CASES, LOGIT_TOL, assert_parity, margin_spec, oracle_spec, run_case
+
+pytestmark = pytest.mark.gpu
+
+
+def test_oracle_on_cuda_equals_cpu(cuda):
+    """The oracle's torch ops give the same logits and KV on the CUDA device (fp32,
+    TF32 off) as on the host: the BASELINE-shape cases may run them there."""
+    from oracle.decoder_ref import OracleDecoder
+    from paper_2603_02599_b200.spec import TINY
+    from paper_2603_02599_b200.weights import init_weights
+
+    spec = margin_spec(TINY, 4)
+    w = init_weights(spec, seed=0)
+    r = random.Random(5)
+    prompt = [r.randrange(spec.vocab) for _ in range(300)]
+    out = []
+    for dev in ("cpu", cuda):
+        o = OracleDecoder(oracle_spec(spec), w, 320, device=dev)
+        lg, c = o.prefill(prompt)
+        lg2, c = o.decode(int(lg.argmax()), len(prompt), c)
+        out.append((lg.cpu(), lg2.cpu(), torch.stack(c["k"]).cpu()))
+    (a0, a1, ak), (b0, b1, bk) = out
+    torch.testing.assert_close(a0, b0, rtol=0, atol=1e-4)
+    torch.testing.assert_close(a1, b1, rtol=0, atol=1e-4)
+    assert (ak - bk).abs().max().item() <= 2 ** -7 * max(1.0, ak.abs().max().item())  # bf16 flips at most
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_baseline_shape_parity(cuda, case):
+    res = run_case(case, cuda)
+    print(f"{case}: logits max-abs {res['logit_max_abs']:.3g} (tol {LOGIT_TOL}), {res['decisions']} greedy "
+          f"decisions, 0 exemptions, oracle min margin {res['oracle_min_top2_margin']:.3g}, KV rel err "
+          f"{res['kv_max_rel_err']:.3g}")
+    assert_parity(res)
