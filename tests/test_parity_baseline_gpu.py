@@ -23,7 +23,10 @@ pytestmark = pytest.mark.gpu
 
 def test_oracle_on_cuda_equals_cpu(cuda):
     """The oracle's torch ops give the same logits and KV on the CUDA device (fp32,
-    TF32 off) as on the host: the BASELINE-shape cases may run them there."""
+    TF32 off) as on the host up to the summation order of fp32 reductions, which
+    flips an occasional bf16 rounding of an intermediate: logits agree to 2e-3 (a
+    tenth of the parity bar), cached K/V to one bf16 ulp. The BASELINE-shape cases
+    may therefore run them there."""
     from oracle.decoder_ref import OracleDecoder
     from paper_2603_02599_b200.spec import TINY
     from paper_2603_02599_b200.weights import init_weights
@@ -39,9 +42,10 @@ def test_oracle_on_cuda_equals_cpu(cuda):
         lg2, c = o.decode(int(lg.argmax()), len(prompt), c)
         out.append((lg.cpu(), lg2.cpu(), torch.stack(c["k"]).cpu()))
     (a0, a1, ak), (b0, b1, bk) = out
-    torch.testing.assert_close(a0, b0, rtol=0, atol=1e-4)
-    torch.testing.assert_close(a1, b1, rtol=0, atol=1e-4)
-    assert (ak - bk).abs().max().item() <= 2 ** -7 * max(1.0, ak.abs().max().item())  # bf16 flips at most
+    torch.testing.assert_close(a0, b0, rtol=0, atol=2e-3)
+    torch.testing.assert_close(a1, b1, rtol=0, atol=2e-3)
+    assert int(a0.argmax()) == int(b0.argmax()) and int(a1.argmax()) == int(b1.argmax())
+    assert ((ak - bk).abs() <= 2 ** -7 * ak.abs().clamp(min=1.0)).all()  # at most one bf16 ulp
 
 
 @pytest.mark.parametrize("case", sorted(CASES))
