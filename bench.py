@@ -144,13 +144,14 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------- CPU baseline
 class CpuOracleStep:
-    """Oracle (CPU fp32, batched linear layers) on host cores, bounded sample:
-    one of the decoder's layers for the whole mixed batch + the lm_head,
-    extrapolated to the full layer count (set up once, then timed per step)."""
+    """The oracle (oracle/decoder_ref.py: CPU fp32, batched linear layers, attention
+    per sequence) decoding the workload's mixed batch on the host cores: every
+    layer of the decoder, the lm_head and the greedy argmax — one real full-depth
+    decode step per call, no extrapolation. KV caches are seeded random at the
+    workload's contexts (set up once, not timed)."""
 
-    def __init__(self, cfg):
+    def __init__(self, cfg, max_batch: int | None = None):
         import torch
-        from dataclasses import replace
 
         from oracle.decoder_ref import OracleDecoder, OracleSpec
         from paper_2603_02599_b200.spec import SPECS
@@ -158,66 +159,167 @@ class CpuOracleStep:
 
         torch.set_num_threads(os.cpu_count() or 1)
         self.threads = torch.get_num_threads()
-        self.spec = SPECS[cfg["spec"]]
-        one = replace(self.spec, n_layers=1)
-        self.one = one
-        w = init_weights(one, seed=0)
-        osp = OracleSpec(one.vocab, one.hidden, 1, one.n_q_heads, one.n_kv_heads, one.head_dim, one.ffn,
-                         one.rope_theta, one.rms_eps, one.qkv_bias)
-        self.B = cfg["batch"]
+        spec = SPECS[cfg["spec"]]
+        self.spec = spec
+        self.B = cfg["batch"] if max_batch is None else min(cfg["batch"], max_batch)
         self.ctx = contexts_for(cfg, self.B)
-        self.dec = OracleDecoder(osp, w, max(self.ctx) + 64)
+        osp = OracleSpec(spec.vocab, spec.hidden, spec.n_layers, spec.n_q_heads, spec.n_kv_heads, spec.head_dim,
+                         spec.ffn, spec.rope_theta, spec.rms_eps, spec.qkv_bias)
+        self.dec = OracleDecoder(osp, init_weights(spec, seed=0), max(self.ctx) + 256)
         g = torch.Generator().manual_seed(7)
-        self.caches = [{"k": [torch.randn(c, one.n_kv_heads, one.head_dim, generator=g)],
-                        "v": [torch.randn(c, one.n_kv_heads, one.head_dim, generator=g)]} for c in self.ctx]
-        self.toks = [int(x) for x in torch.randint(0, one.vocab, (self.B,), generator=g)]
+        L = spec.n_layers
+        self.caches = [{"k": [torch.randn(c, spec.n_kv_heads, spec.head_dim, generator=g) for _ in range(L)],
+                        "v": [torch.randn(c, spec.n_kv_heads, spec.head_dim, generator=g) for _ in range(L)]}
+                       for c in self.ctx]
+        self.toks = [int(x) for x in torch.randint(0, spec.vocab, (self.B,), generator=g)]
         self.i = 0
-        self.sample = (f"oracle decode of the {self.B}-sequence mixed batch through 1 of {self.spec.n_layers} "
-                       f"layers + lm_head (fp32, batched GEMMs, per-sequence attention over ctx "
-                       f"{min(self.ctx)}-{max(self.ctx)}), time x{self.spec.n_layers} layers + lm_head")
+        self.sample = (f"oracle decode steps of the {self.B}-sequence mixed batch, all {L} layers + lm_head + "
+                       f"argmax (fp32, batched GEMMs, per-sequence attention over ctx "
+                       f"{min(self.ctx)}-{max(self.ctx)}), {self.threads} threads")
 
     def step(self) -> float:
-        """Seconds of one extrapolated full decode step."""
-        from oracle.decoder_ref import decode_batch_layers, norm_factored
+        """Seconds of one full decode step (tokens fed back)."""
+        from oracle.decoder_ref import argmax_lowest, decode_batch_layers
 
         pos = [c + self.i for c in self.ctx]
         self.i += 1
         t0 = time.perf_counter()
-        resid = decode_batch_layers(self.dec, self.toks, pos, self.caches, range(1), lm_head=False)
-        t1 = time.perf_counter()
-        xg, r = norm_factored(resid, self.dec.w["final_norm"], self.one.rms_eps)
-        (xg @ self.dec.w["lm_head"].t()) * r
-        t2 = time.perf_counter()
-        return self.spec.n_layers * (t1 - t0) + (t2 - t1)
+        logits = decode_batch_layers(self.dec, self.toks, pos, self.caches, range(self.spec.n_layers))
+        self.toks = [int(x) for x in argmax_lowest(logits)]
+        return time.perf_counter() - t0
 
 
-def cpu_baseline(cfg, steps=2, warmup=1):
+def cpu_baseline(cfg, steps=5, warmup=1):
+    """Median of `steps` real full-depth oracle decode steps on the host cores."""
     o = CpuOracleStep(cfg)
     ts = [o.step() for _ in range(warmup + steps)][warmup:]
     t = statistics.median(ts)
-    return o.B / t, o.sample + f"; median of {steps}", o.threads, t
+    return o.B / t, o.sample + f"; median of {steps} steps after {warmup} warm-up", o.threads, t
+
+
+def simulator_wall(cfg, n_requests=2000):
+    """The restated simulator (scheduler.run = poolsim.engine.run's semantics, golden-
+    pinned) serving this config's Zipf trace with the reference's analytic step
+    price: wall time and simulated decode steps per second on one host core (SURVEY
+    §8(d)(2): it computes no tokens; a reported baseline of the control plane)."""
+    from paper_2603_02599_b200 import pricing, scheduler
+    from paper_2603_02599_b200.sun_types import ClusterConfig, GpuSpec, ModelProfile, PoolMode, RoutingPolicy
+    from paper_2603_02599_b200.trace import ArrivalProcess, WorkloadSpec, generate_trace
+
+    n = cfg["n_models"]
+    models = tuple(ModelProfile(model_id=i, param_count=8.03e9, kv_bytes_per_token=131072, shared_decoder=True)
+                   for i in range(n))
+    cluster = ClusterConfig(models=models, decode_pool_mode=PoolMode.SHARED, decode_pool_size=1,
+                            routing_policy=RoutingPolicy(), gpu_spec=GpuSpec.b200())
+    cost = pricing.CostParams(prefill_flops_per_token=1.606e10, prefill_fixed_overhead=0.0293,
+                              decode_fixed_overhead=0.00543, dequant_compute_penalty=1.242, mfu=0.753, mbu=0.953)
+    ws = WorkloadSpec(n_models=n, total_rps=20.0, alpha=cfg["alpha"], isl=cfg["isl"], osl=cfg["osl"],
+                      grace_period=0.0, measurement_window=n_requests / 20.0, drain_margin=0.0, seed=42,
+                      arrival_process=ArrivalProcess.POISSON)
+    trace = generate_trace(ws)
+    t0 = time.perf_counter()
+    res = scheduler.run(cluster, trace, cost)
+    wall = time.perf_counter() - t0
+    steps = len(res.log.steps)
+    return {"impl": "scheduler.run (restatement of poolsim engine.run, pinned to its golden runs)",
+            "requests": len(trace), "decode_steps": steps, "wall_s": wall, "steps_per_s": steps / wall, "cores": 1}
 
 
 def reference_arm(args, cfg):
     rank, world, _ = env_rank()
     if rank != 0:
         return
+    t_setup = time.perf_counter()
     o = CpuOracleStep(cfg)
+    setup_s = time.perf_counter() - t_setup
     for _ in range(args.warmup):
         o.step()
     times = [o.step() for _ in range(args.steps)]
-    t = sum(times) / len(times)
+    t = statistics.median(times)
     value = o.B / t
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg["workload"],
-                   "impl": "CPU oracle port (oracle/decoder_ref.py; the reference has no decoder code)"},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": o.threads, "kind": "port", "sample": o.sample},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "ms_per_step_mean": 1e3 * sum(times) /
+        len(times), "timed_s": sum(times), "setup_s": setup_s, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "decoder": o.spec.name, "batch_per_gpu": o.B,
+                   "global_batch": o.B, "ctx_min": min(o.ctx), "ctx_max": max(o.ctx), "routing": args.routing,
+                   "impl": "CPU oracle port (oracle/decoder_ref.py; the reference computes no tokens)"},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": o.threads, "kind": "port",
+                         "sample": o.sample + f"; median of {args.steps} timed steps"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    try:
+        line["simulator_wall"] = simulator_wall(cfg)
+    except Exception as e:  # a reported side number: never fail the arm on it
+        line["simulator_wall"] = {"error": repr(e)}
     print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- KV hand-off leg (N > 1)
+HANDOFF_PAGES = 64  # one C3 request: ISL 1024 = 64 pages of 16 tokens (128 MiB at 8B geometry)
+
+
+def handoff_leg(kv, rank, world, dev, spec, reps=5):
+    """Every rank hands one ISL-1024 request's KV (the last HANDOFF_PAGES pages of its
+    pool, reserved for this) to rank + 1 at the same time, two ways: (1) the
+    product path, a CUDA-IPC peer copy into the receiver's pages on the copy engines
+    (handoff.copy_pages: NVLink 5 / NVSwitch), (2) NCCL send/recv of the same bytes.
+    Device-timed (CUDA events), after the decode timing; returns per-transport GB/s
+    (min / mean over ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_02599_b200.handoff import RemotePool, copy_pages, export_pool
+
+    ctrl = dist.new_group(backend="gloo")
+    mine = export_pool(kv)
+    allh = [None] * world
+    dist.all_gather_object(allh, mine.numpy().tobytes(), group=ctrl)
+    nxt, prv = (rank + 1) % world, (rank - 1) % world
+    remote = RemotePool(torch.frombuffer(bytearray(allh[nxt]), dtype=torch.uint8))
+    src = list(range(kv.num_pages - HANDOFF_PAGES, kv.num_pages))
+    dst = list(range(remote.num_pages - HANDOFF_PAGES, remote.num_pages))
+    nbytes = HANDOFF_PAGES * kv.page_bytes
+    s = torch.cuda.Stream(device=dev)
+    out = {"bytes_per_request": nbytes, "pages": HANDOFF_PAGES}
+
+    def timed(fn):
+        for i in range(reps + 1):
+            dist.barrier(group=ctrl)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            fn()
+            e1.record(s)
+            e1.synchronize()
+            if i == 0:
+                best = float("inf")  # first rep warms the mapping / NCCL channels
+            else:
+                best = min(best, e0.elapsed_time(e1))
+        return best
+
+    ms = timed(lambda: copy_pages(kv, src, remote.struct, dst, s))
+    buf = torch.empty((HANDOFF_PAGES,) + tuple(kv.tensor.shape[1:]), dtype=kv.tensor.dtype, device=dev)
+
+    def nccl():
+        with torch.cuda.stream(s):
+            ops = [dist.P2POp(dist.isend, kv.tensor[src[0]:src[0] + HANDOFF_PAGES], nxt),
+                   dist.P2POp(dist.irecv, buf, prv)]
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+
+    ms_nccl = timed(nccl)
+    gb = torch.tensor([nbytes / (ms / 1e3) / 1e9, nbytes / (ms_nccl / 1e3) / 1e9], device=dev)
+    lo, tot = gb.clone(), gb.clone()
+    dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+    dist.all_reduce(tot)
+    remote.close()
+    out["peer_copy"] = {"gbps_min": float(lo[0]), "gbps_mean": float(tot[0]) / world,
+                        "transport": "CUDA IPC peer copy on the copy engines (sun_kv_handoff_copy)"}
+    out["nccl_p2p"] = {"gbps_min": float(lo[1]), "gbps_mean": float(tot[1]) / world,
+                       "transport": "NCCL send/recv (handoff.send_kv path)"}
+    out["pattern"] = "every rank sends one request to rank+1 simultaneously; best of 5 after 1 warm-up"
+    return out
 
 
 # --------------------------------------------------------------------------- GPU arm
@@ -279,7 +381,7 @@ def gpu_arm(args, cfg):
     w = init_weights(spec, seed=0, device=dev)
     dw = DeviceWeights(spec, w, dev, max_ctx, free_source=True)
     del w
-    kv = KvPool(spec, sum(pages_for(c + total_steps + args.steps + 2) for c in ctx) + 4, dev)
+    kv = KvPool(spec, sum(pages_for(c + total_steps + args.steps + 2) for c in ctx) + 4 + HANDOFF_PAGES, dev)
     kv.fill_random_(seed=1000 + rank)
     dec = SharedDecodeModule(spec, dw, kv, max_batch=B, max_context=max_ctx, use_pdl=not args.no_pdl)
     # block tables: contiguous page runs per member
@@ -400,9 +502,13 @@ def gpu_arm(args, cfg):
                "api": ("SharedDecodeModule.decode_host(pinned tokens/positions/block_tables) -> pinned next tokens"
                        if graph else "SharedDecodeModule.decode(host pinned tokens/positions/block_tables) -> next tokens")}
 
+    handoff = None
+    if world > 1 and not args.no_handoff:
+        handoff = handoff_leg(kv, rank, world, dev, spec)
+
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu:
-        v, sample, threads, _ = cpu_baseline(cfg, steps=2, warmup=1)
+        v, sample, threads, _ = cpu_baseline(cfg, steps=5, warmup=1)
         cpu = {"value": v, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": sample}
 
     if rank == 0:
@@ -434,10 +540,75 @@ def gpu_arm(args, cfg):
             "clocks": clk,
             "gpu_launches": gpu_launches,
             "setup_s": setup_s,
+            "handoff": handoff,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def dry_run_arm(args, cfg):
+    """The N-rank bench path without a GPU (gloo, CPU): the same LOT / PINNED routing
+    of the Zipf trace over the ranks, a stand-in step of fixed cost per row, the
+    barrier + max-over-ranks timing all-reduce and the JSON line. For CPU tests of
+    the multi-rank plumbing (tests/test_bench_ranks.py); reports nothing about a GPU."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world, _ = env_rank()
+    if world > 1:
+        dist.init_process_group("gloo")
+    mine = build_assignment(cfg, world, args.routing)[rank][:256]
+    B = len(mine)
+    for _ in range(args.warmup):
+        time.sleep(1e-5 * B)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        time.sleep(1e-5 * B)  # stand-in step
+    t = torch.tensor([time.perf_counter() - t0])
+    tok = torch.tensor([float(B * args.steps)])
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tok)
+    gathered = [None] * world
+    if world > 1:
+        dist.all_gather_object(gathered, sorted({m for _, m in mine}))
+    else:
+        gathered = [sorted({m for _, m in mine})]
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": float(tok) / float(t), "unit": "tokens/s", "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(t) * 1e3 / args.steps,
+                          "higher_is_better": True, "scaling": "weak", "dry_run": True,
+                          "config": {"workload": cfg["workload"], "batch_per_gpu": B,
+                                     "global_batch": int(float(tok)) // args.steps, "routing": args.routing,
+                                     "models_per_rank": gathered,
+                                     "parallelism": f"{world} shared decode workers (request-level DP)"}}),
+              flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def relaunch_ranks(args) -> int:
+    """`bench.py --gpus N` outside torchrun: start the N ranks ourselves, the way the
+    driver does (torch.distributed.run, one process per GPU, 127.0.0.1 rendezvous)."""
+    import socket
+    import subprocess
+
+    if not args.dry_run:
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible")
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -453,12 +624,21 @@ def main():
     ap.add_argument("--no-pdl", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-handoff", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="CPU/gloo run of the rank plumbing (tests)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_ranks(args))
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} launched with WORLD_SIZE={world}")
     if args.impl == "reference":
         reference_arm(args, cfg)
+    elif args.dry_run:
+        dry_run_arm(args, cfg)
     else:
         gpu_arm(args, cfg)
 

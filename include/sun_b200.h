@@ -29,7 +29,17 @@
 extern "C" {
 #endif
 
-#define SUN_ABI_VERSION 1
+#define SUN_ABI_VERSION 2
+
+/* Error bits of a decoder's device error word (sun_decoder_status). Every step
+ * validates its inputs on the device before any KV write: a bad token reads
+ * embedding row 0, a bad position is clamped and its KV append skipped, an
+ * out-of-range page is never written (attention reads it as zeros through the
+ * TMA bounds), so a bad block table cannot corrupt another sequence's KV. */
+#define SUN_STEP_ERR_TOKEN 1u    /* token outside [0, vocab)                                */
+#define SUN_STEP_ERR_POSITION 2u /* position outside [0, max_context)                       */
+#define SUN_STEP_ERR_PAGE 4u     /* a block-table entry for pages 0..pos/16 outside the pool */
+#define SUN_STEP_ERR_NAN 8u      /* a row's logits had no finite maximum (argmax -> 0)      */
 
 typedef enum SunStatus {
   SUN_OK = 0,
@@ -59,6 +69,7 @@ typedef struct SunDecoderDims {
   int32_t group_size;  /* 128 when weight_bits == 4 */
   int32_t qkv_bias;    /* 1 if the QKV projection has a bias (Qwen2.5) */
   float rms_eps;
+  float rope_theta;    /* RoPE base of the K cache this decoder reads and writes */
 } SunDecoderDims;
 
 /* SUN-BLK weight layout (bf16 linear layers and the lm_head as passed to the
@@ -106,11 +117,24 @@ typedef struct SunWeights {
  * construction). Page p holds page_size consecutive tokens of
  * one sequence for all layers: [n_layers][2 (K,V)][n_kv_heads][page_size][head_dim]
  * bf16; K is stored after RoPE. A sequence's pages are listed in its block-table
- * row (the physical form of KvHandle, domain.py:96-113). */
+ * row (the physical form of KvHandle, domain.py:96-113).
+ * The pool records the KV geometry it was laid out for: every decoder created over
+ * it (the shared decode module and each task prefill module) and every hand-off
+ * copy into it must match, else SUN_ERR_MIXED_DECODER — the device-side form of the
+ * reference's shared-decoder invariant (domain.py:266-279, costmodel.py:132-138). */
 typedef struct SunKvPool {
   void* base;
   int64_t num_pages;
+  int32_t n_layers;
+  int32_t n_kv_heads;
+  int32_t head_dim;
+  int32_t page_size;
+  float rope_theta;
+  int32_t device;      /* CUDA device ordinal the pages live on */
 } SunKvPool;
+
+/* Bytes of one page of a pool with this geometry. */
+SunStatus sun_kv_page_bytes(const SunKvPool* kv, size_t* bytes);
 
 typedef struct SunDecoder SunDecoder;
 
@@ -183,6 +207,40 @@ SunStatus sun_decode_step_timeline(SunDecoder* dec, const int32_t* tokens, const
 
 /* Number of kernels this thread has launched through the library so far. */
 SunStatus sun_launch_count(int64_t* launches);
+
+/* Read (and, if clear != 0, reset) the decoder's device error word: the OR of the
+ * SUN_STEP_ERR_* bits raised by the steps since the last clear. Synchronises the
+ * stream. *flags == 0: every step's inputs were valid. */
+SunStatus sun_decoder_status(SunDecoder* dec, uint32_t* flags, int32_t clear, void* stream);
+
+/* Whether sun_decode_step runs the persistent layer GEMM chain for these flags on
+ * this decoder (bf16, SUN_STEP_DISTINCT_ROWS, and a grid that fits this device's
+ * SMs co-resident — checked with the occupancy API at create). */
+SunStatus sun_decoder_uses_chain(SunDecoder* dec, int32_t flags, int32_t* uses_chain);
+
+/* ---- K8: prefill -> decode KV hand-off by peer copy (replaces transfer_time,
+ * costmodel.py:148-155; the transfer window engine.py:345-392) ----
+ * The decode worker exports its pool once; a prefill worker in another process
+ * (any GPU of the node, or the same GPU) imports it and copies a request's pages
+ * straight into the pages the decode worker reserved, with the copy engines:
+ * NVLink 5 / NVSwitch between GPUs, HBM within one. No SMs are taken from a
+ * decode step running concurrently (its persistent layer chain needs the whole
+ * GPU), unlike a kernel-based transport. */
+typedef struct SunKvPoolHandle {
+  uint8_t ipc[64];     /* cudaIpcMemHandle_t of the allocation holding the pages */
+  int64_t offset;      /* byte offset of page 0 inside that allocation          */
+  SunKvPool geometry;  /* base = NULL; num_pages, KV geometry, device             */
+} SunKvPoolHandle;
+SunStatus sun_kv_pool_export(const SunKvPool* kv, SunKvPoolHandle* out);
+/* Map an exported pool into this process (peer access enabled when it lives on
+ * another device); *out is a pool whose base is valid here. */
+SunStatus sun_kv_pool_import(const SunKvPoolHandle* handle, SunKvPool* out);
+SunStatus sun_kv_pool_close(SunKvPool* imported);
+/* Copy n_pages pages src_pages[i] of src into dst_pages[i] of dst (host int32
+ * arrays; consecutive runs on both sides become one copy each), asynchronously on
+ * stream. The pools' KV geometries must match (else SUN_ERR_MIXED_DECODER). */
+SunStatus sun_kv_handoff_copy(const SunKvPool* src, const int32_t* src_pages, const SunKvPool* dst,
+                              const int32_t* dst_pages, int32_t n_pages, void* stream);
 
 /* ---- kernel-level entry points (unit parity tests; same kernels as the step) ---- */
 

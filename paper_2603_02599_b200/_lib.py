@@ -30,6 +30,11 @@ SUN_ERR_CUDA = 4
 SUN_ERR_CAPACITY = 5
 SUN_STEP_FEEDBACK = 1
 SUN_STEP_DISTINCT_ROWS = 2
+SUN_STEP_ERR_TOKEN = 1
+SUN_STEP_ERR_POSITION = 2
+SUN_STEP_ERR_PAGE = 4
+SUN_STEP_ERR_NAN = 8
+ABI_VERSION = 2
 
 
 class SunDecoderDims(ctypes.Structure):
@@ -37,7 +42,7 @@ class SunDecoderDims(ctypes.Structure):
         ("vocab", c_i32), ("hidden", c_i32), ("n_layers", c_i32), ("n_q_heads", c_i32),
         ("n_kv_heads", c_i32), ("head_dim", c_i32), ("ffn", c_i32), ("page_size", c_i32),
         ("max_context", c_i32), ("weight_bits", c_i32), ("group_size", c_i32), ("qkv_bias", c_i32),
-        ("rms_eps", c_f32),
+        ("rms_eps", c_f32), ("rope_theta", c_f32),
     ]
 
 
@@ -57,7 +62,12 @@ class SunWeights(ctypes.Structure):
 
 
 class SunKvPool(ctypes.Structure):
-    _fields_ = [("base", c_vp), ("num_pages", c_i64)]
+    _fields_ = [("base", c_vp), ("num_pages", c_i64), ("n_layers", c_i32), ("n_kv_heads", c_i32),
+                ("head_dim", c_i32), ("page_size", c_i32), ("rope_theta", c_f32), ("device", c_i32)]
+
+
+class SunKvPoolHandle(ctypes.Structure):
+    _fields_ = [("ipc", ctypes.c_uint8 * 64), ("offset", c_i64), ("geometry", SunKvPool)]
 
 
 # symbol -> (restype, argtypes); every symbol declared in include/sun_b200.h
@@ -91,6 +101,13 @@ SIGNATURES = {
     "sun_block_weights_bf16": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_vp]),
     "sun_rmsnorm": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_f32, c_vp]),
     "sun_quantize_w4": (c_i32, [c_vp, c_i64, c_i64, c_i32, c_vp, c_vp, c_vp]),
+    "sun_decoder_status": (c_i32, [c_vp, ctypes.POINTER(ctypes.c_uint32), c_i32, c_vp]),
+    "sun_decoder_uses_chain": (c_i32, [c_vp, c_i32, ctypes.POINTER(c_i32)]),
+    "sun_kv_page_bytes": (c_i32, [ctypes.POINTER(SunKvPool), ctypes.POINTER(c_size)]),
+    "sun_kv_pool_export": (c_i32, [ctypes.POINTER(SunKvPool), ctypes.POINTER(SunKvPoolHandle)]),
+    "sun_kv_pool_import": (c_i32, [ctypes.POINTER(SunKvPoolHandle), ctypes.POINTER(SunKvPool)]),
+    "sun_kv_pool_close": (c_i32, [ctypes.POINTER(SunKvPool)]),
+    "sun_kv_handoff_copy": (c_i32, [ctypes.POINTER(SunKvPool), c_vp, ctypes.POINTER(SunKvPool), c_vp, c_i32, c_vp]),
 }
 
 _lib = None
@@ -112,7 +129,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.sun_abi_version() != 1:
+    if lib.sun_abi_version() != ABI_VERSION:
         raise RuntimeError("libsun_b200.so ABI version mismatch")
     _lib = lib
     return lib

@@ -48,7 +48,16 @@ struct AttnArgs {
   // kernel writes only each row's last page: the other pages are staged before
   // griddepcontrol.wait, i.e. while the QKV grid is still finishing (PDL)
   int prestage;
+  int max_ctx;             // tokens a block-table row can address (decoder max_context): positions
+                           // outside [0, max_ctx) are clamped, so a bad position cannot read past
+                           // its block-table row (sun_decode_step flags it in the error word)
 };
+
+// context length of row b (clamped; see AttnArgs::max_ctx)
+SUN_DEVICE int row_ctx(const AttnArgs& a, int b) {
+  const int p = a.positions[b];
+  return (p < 0 ? 0 : (p >= a.max_ctx ? a.max_ctx - 1 : p)) + 1;
+}
 
 template <int D>
 SUN_DEVICE void store_attn_out(const AttnArgs& a, int b, int head, int dim, float v) {
@@ -96,7 +105,7 @@ __global__ void __launch_bounds__(128)
     pdl_wait();
     pdl_launch_dependents();  // early: the next kernel may start its prologue / weight prefetch
   }
-  const int ctx = a.positions[b] + 1;
+  const int ctx = row_ctx(a, b);
   const int n_pages = (ctx + kPageTokens - 1) / kPageTokens;
   const int p0 = split * a.pages_per_split;
   if (p0 >= n_pages) {
@@ -342,7 +351,7 @@ __global__ void __launch_bounds__(128)
   const int nr = a.group_len[blockIdx.z];
   pdl_wait();
   pdl_launch_dependents();
-  const int ctx = a.positions[b0 + nr - 1] + 1;  // the group's longest context
+  const int ctx = row_ctx(a, b0 + nr - 1);  // the group's longest context
   const int n_pages = (ctx + kPageTokens - 1) / kPageTokens;
   const int p0 = split * a.pages_per_split;
   if (p0 >= n_pages) return;
@@ -364,8 +373,8 @@ __global__ void __launch_bounds__(128)
   const int r_lo = g / G, r_hi = (g + 8) / G;
   const bool v_lo = r_lo < nr, v_hi = r_hi < nr;
   const bool has_hi = nr * G > 8;  // warp-uniform
-  const int ctx_lo = v_lo ? a.positions[b0 + r_lo] + 1 : ctx;
-  const int ctx_hi = v_hi ? a.positions[b0 + r_hi] + 1 : ctx;
+  const int ctx_lo = v_lo ? row_ctx(a, b0 + r_lo) : ctx;
+  const int ctx_hi = v_hi ? row_ctx(a, b0 + r_hi) : ctx;
 
   const int n_my = (p1 - p0 - warp + C::kWarps - 1) / C::kWarps > 0 ? (p1 - p0 - warp + C::kWarps - 1) / C::kWarps : 0;
   const int* bt = a.block_tables + static_cast<long long>(b0) * a.bt_stride;
@@ -511,7 +520,7 @@ __global__ void __launch_bounds__(128)
     const int b = b0 + qr / G;
     const int head = kvh * G + qr % G;
     // this row's own split count (the combine kernel uses the same rule)
-    const int npr = (a.positions[b] + 1 + kPageTokens - 1) / kPageTokens;
+    const int npr = (row_ctx(a, b) + kPageTokens - 1) / kPageTokens;
     const int nsr = (npr + a.pages_per_split - 1) / a.pages_per_split;
     if (split >= nsr) continue;  // wholly past this row's causal limit
     float mm = -INFINITY;
@@ -546,7 +555,7 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(const AttnArgs a) {
   pdl_launch_dependents();
   const int head = blockIdx.x;
   const int b = blockIdx.y;
-  const int ctx = a.positions[b] + 1;
+  const int ctx = row_ctx(a, b);
   const int n_pages = (ctx + kPageTokens - 1) / kPageTokens;
   const int n_splits = (n_pages + a.pages_per_split - 1) / a.pages_per_split;
   if (n_splits == 1) return;  // the attention kernel emitted this sequence's output directly

@@ -2,11 +2,24 @@
 // the first RMSNorm, RMSNorm producing the bf16 GEMM operand, and the final
 // greedy argmax over the lm_head tiles' (max, index) partials.
 #pragma once
+#include "../../include/sun_b200.h"  // SUN_STEP_ERR_* bits
 #include "gemm_tc.cuh"  // act_offset (SUN-ACT layout)
 
 namespace sun {
 
 constexpr int kRowThreads = 256;
+
+// What embed_norm_kernel validates at the start of a step (SUN_STEP_ERR_* bits of
+// include/sun_b200.h into err).
+struct StepCheck {
+  const int* positions;
+  const int* block_tables;
+  int bt_stride;
+  int vocab;
+  int max_ctx;
+  long long num_pages;
+  unsigned* err;
+};
 
 SUN_DEVICE float block_sum(float v, float* red) {
 #pragma unroll
@@ -70,12 +83,29 @@ __global__ void __launch_bounds__(kRowThreads)
 __global__ void __launch_bounds__(kRowThreads)
     embed_norm_kernel(const int* __restrict__ tokens, const __nv_bfloat16* __restrict__ embed,
                       float* __restrict__ resid, const __nv_bfloat16* __restrict__ g, __nv_bfloat16* __restrict__ xg,
-                      float* __restrict__ ss, int h, int act_rows, int ss_tiles) {
+                      float* __restrict__ ss, int h, int act_rows, int ss_tiles, StepCheck chk) {
   __shared__ float red[kRowThreads / 32];
   pdl_wait();
   pdl_launch_dependents();
   const int b = blockIdx.x;
-  const __nv_bfloat16* e = embed + static_cast<long long>(tokens[b]) * h;
+  // input validation (the step's error word, sun_decoder_status): a bad token reads
+  // embedding row 0; bad positions / pages are clamped / skipped by the consumers
+  int tok = tokens[b];
+  const int pos = chk.positions[b];
+  unsigned bits = 0;
+  if (tok < 0 || tok >= chk.vocab) {
+    bits |= SUN_STEP_ERR_TOKEN;
+    tok = 0;
+  }
+  if (pos < 0 || pos >= chk.max_ctx) {
+    bits |= SUN_STEP_ERR_POSITION;
+  } else {
+    const int* bt = chk.block_tables + static_cast<long long>(b) * chk.bt_stride;
+    for (int j = threadIdx.x; j <= (pos >> 4); j += kRowThreads)
+      if (bt[j] < 0 || static_cast<long long>(bt[j]) >= chk.num_pages) bits |= SUN_STEP_ERR_PAGE;
+  }
+  if (bits) atomicOr(chk.err, bits);
+  const __nv_bfloat16* e = embed + static_cast<long long>(tok) * h;
   float* x = resid + static_cast<long long>(b) * h;
   float acc = 0.f;
   for (int i = threadIdx.x * 4; i < h; i += kRowThreads * 4) {
@@ -104,7 +134,8 @@ __global__ void __launch_bounds__(kRowThreads)
 // feedback, also tokens[b] = next[b] and positions[b] += 1 (graph-replayable loop).
 __global__ void __launch_bounds__(kRowThreads)
     argmax_reduce_kernel(const float* __restrict__ val, const int* __restrict__ idx, int m_tiles, int bn,
-                         int* __restrict__ next, int* __restrict__ feedback_tokens, int* __restrict__ positions) {
+                         int* __restrict__ next, int* __restrict__ feedback_tokens, int* __restrict__ positions,
+                         unsigned* __restrict__ err) {
   __shared__ float sv[kRowThreads / 32];
   __shared__ int si[kRowThreads / 32];
   pdl_wait();
@@ -140,6 +171,10 @@ __global__ void __launch_bounds__(kRowThreads)
         bv = sv[w];
         bi = si[w];
       }
+    }
+    if (bi == 0x7fffffff) {  // no finite maximum (NaN / -inf logits): token 0, flagged
+      bi = 0;
+      if (err != nullptr) atomicOr(err, SUN_STEP_ERR_NAN);
     }
     next[b] = bi;
     if (feedback_tokens != nullptr) {  // device-resident autoregressive loop

@@ -93,6 +93,8 @@ struct GemmArgs {
   int n_kv_heads;
   int head_dim;
   int page_size;
+  int max_pos;                // positions are clamped to [0, max_pos) for the RoPE tables
+  long long kv_pages;         // pool size: an append page outside [0, kv_pages) is not written
   // LOGITS
   float* amax_val;  // [m_tiles][bn]
   int* amax_idx;    // [m_tiles][bn]
@@ -391,6 +393,7 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
               const float o = is_v ? v[j] : (lo_half ? (v[j] * cs[j] - pv[j] * sn[j]) : (v[j] * cs[j] + pv[j] * sn[j]));
               const int pos = meta[(c0 + j) & 255];
               const int page = meta[256 + ((c0 + j) & 255)];
+              if (page < 0) continue;  // invalid append page (flagged at step start): no write
               a.kv_base[static_cast<long long>(page) * a.page_stride + inner + static_cast<long long>(pos & 15) * d] =
                   __float2bfloat16_rn(o);
             }
@@ -492,9 +495,13 @@ SUN_DEVICE void load_qkv_meta(const GemmArgs& a, float* epi) {  // epilogue grou
   int* meta = epi_meta(epi);
   if constexpr (EPI == EPI_QKV_ROPE) {
     for (int b = threadIdx.x - 64; b < a.bn; b += 128) {
-      const int pos = b < a.batch ? a.positions[b] : 0;
+      int pos = b < a.batch ? a.positions[b] : 0;
+      const bool pos_ok = pos >= 0 && pos < a.max_pos;  // (flagged by embed_norm_kernel)
+      pos = pos_ok ? pos : 0;
+      int page = (b < a.batch && pos_ok) ? a.block_tables[static_cast<long long>(b) * a.bt_stride + (pos >> 4)] : -1;
+      if (page < 0 || static_cast<long long>(page) >= a.kv_pages) page = -1;  // 16-token pages; -1: no append
       meta[b] = pos;
-      meta[256 + b] = b < a.batch ? a.block_tables[static_cast<long long>(b) * a.bt_stride + (pos >> 4)] : 0;  // 16-token pages
+      meta[256 + b] = page;
     }
   }
   if (a.ss_in != nullptr) {

@@ -67,6 +67,19 @@ PFN_encodeTiled_t encode_fn() {
   return fn;
 }
 
+typedef CUresult (*PFN_getAddressRange_t)(CUdeviceptr*, size_t*, CUdeviceptr);
+PFN_getAddressRange_t address_range_fn() {  // allocation containing a device pointer (IPC export / close)
+  static PFN_getAddressRange_t fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    return (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+               ? reinterpret_cast<PFN_getAddressRange_t>(p)
+               : nullptr;
+  }();
+  return fn;
+}
+
 // 2-D bf16 [rows][cols] (row stride ld elements), box {64 cols, box_rows}, SW128.
 SunStatus make_map_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
                       uint32_t box_rows, CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
@@ -317,7 +330,7 @@ int gemm_sched() {
 // Workspace layout shared by sizing and creation.
 struct WsLayout {
   size_t resid, xn, q, attn, act, part_o, part_ml, attn_cnt, ss, amax_val, amax_idx, logits, sk_part, sk_flags,
-      chain_bar, total;
+      chain_bar, err, total;
   int max_splits;
 };
 
@@ -354,6 +367,7 @@ WsLayout layout_ws(const SunDecoderDims& d, int max_batch) {
   w.sk_part = take(sk_part_bytes(bmp));
   w.sk_flags = take(kMaxGemmCtas * 4);
   w.chain_bar = take(64);
+  w.err = take(64);
   w.total = off;
   return w;
 }
@@ -378,6 +392,34 @@ SunStatus check_dims(const SunDecoderDims* d) {
   return SUN_OK;
 }
 
+// The shared-decoder invariant at the device boundary: a decoder (shared decode
+// module or task prefill module) only reads / writes a pool laid out for its KV
+// geometry (domain.py:266-279 shared models agree on the decoder; costmodel.py:132-138).
+SunStatus check_kv_geometry(const SunDecoderDims& d, const SunKvPool& kv) {
+  if (kv.n_layers != d.n_layers || kv.n_kv_heads != d.n_kv_heads || kv.head_dim != d.head_dim ||
+      kv.page_size != d.page_size || kv.rope_theta != d.rope_theta)
+    return fail(SUN_ERR_MIXED_DECODER,
+                "KV pool geometry (layers %d, kv heads %d, head_dim %d, page %d, rope theta %g) does not match the "
+                "decoder's (%d, %d, %d, %d, %g)",
+                kv.n_layers, kv.n_kv_heads, kv.head_dim, kv.page_size, (double)kv.rope_theta, d.n_layers,
+                d.n_kv_heads, d.head_dim, d.page_size, (double)d.rope_theta);
+  if (kv.num_pages < 1 || kv.base == nullptr) return fail(SUN_ERR_VALUE, "empty KV pool");
+  return SUN_OK;
+}
+
+size_t kv_page_bytes(const SunKvPool& kv) {
+  return size_t(kv.n_layers) * 2 * kv.n_kv_heads * kv.page_size * kv.head_dim * 2;
+}
+
+int device_sms() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return kNumSms;
+  }
+  return n;
+}
+
 }  // namespace
 
 struct SunDecoder {
@@ -400,6 +442,9 @@ struct SunDecoder {
   float* sk_part;
   unsigned* sk_flags;
   unsigned* chain_bar;
+  unsigned* err;  // SUN_STEP_ERR_* bits (sun_decoder_status)
+  int num_sms = kNumSms;
+  bool chain_ok = false;  // the layer chain's grid fits this device co-resident (chain_fits)
   GemmPlan p_qkv, p_o, p_gu, p_down, p_lm;
 };
 
@@ -602,8 +647,21 @@ bool use_chain(int flags, bool w4) {
   return !w4 && (v == 1 || (v < 0 && (flags & SUN_STEP_DISTINCT_ROWS)));
 }
 
+// Can every CTA of the chain's grid be resident at once on this device (one per SM,
+// at the chain's shared-memory size)? Checked once per decoder; without it the
+// chain's phase barriers could not make progress, so the step uses separate launches.
+bool chain_fits(int num_sms) {
+  int per_sm = 0;
+  const size_t smem = gemm_smem_bytes(16, gemm_stages(16, false, 1), gemm_xstages(16));
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemm_chain_kernel, kGemmThreads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return per_sm >= 1 && num_sms >= 16;
+}
+
 SunStatus run_chain(GemmArgs* ph, const int* epi, const GemmPlan* plans, const void* const* wblk, int nph,
-                    unsigned* bar, cudaStream_t st, bool pdl) {
+                    unsigned* bar, cudaStream_t st, bool pdl, int num_sms) {
   ChainArgs c;
   memset(&c, 0, sizeof(c));
   const int bn = ph[0].bn;
@@ -614,9 +672,9 @@ SunStatus run_chain(GemmArgs* ph, const int* epi, const GemmPlan* plans, const v
   // resident at once (the phase barriers need the whole grid): grid = 4 x clusters
   static const int cl_env = [] { const char* e = getenv("SUN_CHAIN_CLUSTER"); return e ? atoi(e) : 1; }();
   const size_t recv = size_t(3) * ((bn / 16 + 3) / 4) * 8192;
-  int G = kNumSms;
+  int G = num_sms;  // L2 chain: one CTA per SM of this device (all co-resident)
   if (cl_env && smem + recv <= size_t(kSmemPerSm)) {
-    const int ncl = std::min(kNumSms / 4, max_active_clusters(4, smem + recv, false));
+    const int ncl = std::min(num_sms / 4, max_active_clusters(4, smem + recv, false));
     bool any = false;  // some phase must get one tile per cluster (else the smaller grid only costs)
     for (int i = 0; i < nph; ++i)
       any = any || (plans[i].m_tiles <= ncl && plans[i].ksteps >= 4 && 4 * ncl / plans[i].m_tiles >= 4);
@@ -746,8 +804,11 @@ SunStatus sun_decoder_create(const SunDecoderDims* dims, const SunWeights* weigh
   if (st != SUN_OK) return st;
   if (!weights || !kv || !out || !weights->layers) return fail(SUN_ERR_VALUE, "null argument");
   if (max_batch < 1 || max_batch > 256) return fail(SUN_ERR_VALUE, "max_batch must be in [1,256]");
+  if ((st = check_kv_geometry(*dims, *kv)) != SUN_OK) return st;
   init_kernel_attrs();
   SunDecoder* dec = new SunDecoder();
+  dec->num_sms = device_sms();
+  dec->chain_ok = chain_fits(dec->num_sms);
   dec->d = *dims;
   dec->max_batch = max_batch;
   dec->bmp = round16(max_batch);
@@ -779,6 +840,7 @@ SunStatus sun_decoder_create(const SunDecoderDims* dims, const SunWeights* weigh
   dec->sk_part = reinterpret_cast<float*>(ws + dec->L.sk_part);
   dec->sk_flags = reinterpret_cast<unsigned*>(ws + dec->L.sk_flags);
   dec->chain_bar = reinterpret_cast<unsigned*>(ws + dec->L.chain_bar);
+  dec->err = reinterpret_cast<unsigned*>(ws + dec->L.err);
 
   const SunDecoderDims& d = *dims;
   const int qd = d.n_q_heads * d.head_dim;
@@ -794,6 +856,7 @@ SunStatus sun_decoder_create(const SunDecoderDims* dims, const SunWeights* weigh
   if (e == cudaSuccess) e = cudaMemset(ws + dec->L.attn_cnt, 0, size_t(max_batch) * d_cnt_heads(*dims) * 4);
   if (e == cudaSuccess) e = cudaMemset(ws + dec->L.sk_flags, 0, kMaxGemmCtas * 4);
   if (e == cudaSuccess) e = cudaMemset(ws + dec->L.chain_bar, 0, 64);
+  if (e == cudaSuccess) e = cudaMemset(ws + dec->L.err, 0, 64);
   if (e != cudaSuccess) {
     delete dec;
     return fail(SUN_ERR_CUDA, "cudaMemset ws: %s", cudaGetErrorString(e));
@@ -848,6 +911,7 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
   aa.act_rows = bn;
   aa.counters = dec->attn_cnt;
   aa.fused_combine = attn_fused_combine();
+  aa.max_ctx = d.max_context;
   static const int prestage_env = [] { const char* e = getenv("SUN_ATTN_PRESTAGE"); return e ? atoi(e) : 1; }();
   aa.prestage = (flags & SUN_STEP_DISTINCT_ROWS) && g_groups.start == nullptr && prestage_env ? 1 : 0;
 
@@ -867,10 +931,11 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     g.ss_out = dec->ss;
   };
   // embedding gather + the first (attention) norm's operand
+  StepCheck chk{positions, block_tables, bt_stride, d.vocab, d.max_context, (long long)dec->kv.num_pages, dec->err};
   SUN_CUDA(launch(embed_norm_kernel, dim3(batch), dim3(kRowThreads), 0, st, pdl, tokens,
                   static_cast<const __nv_bfloat16*>(dec->w.embed), dec->resid,
                   static_cast<const __nv_bfloat16*>(dec->layers[0].attn_norm), dec->xn, dec->ss, d.hidden, bn,
-                  ss_tiles));
+                  ss_tiles, chk));
   auto qkv_args = [&](int l) {  // QKV (* r_b) + bias + RoPE + KV append
     const SunLayerWeights& lw = dec->layers[l];
     GemmArgs a = base_args(dec->p_qkv, qkv_rows(d), d.hidden, batch, bn, dec->xn, dec->sk_part, dec->sk_flags);
@@ -890,6 +955,8 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     a.n_kv_heads = d.n_kv_heads;
     a.head_dim = d.head_dim;
     a.page_size = d.page_size;
+    a.max_pos = d.max_context;
+    a.kv_pages = dec->kv.num_pages;
     return a;
   };
   auto o_args = [&](int l) {  // O projection + residual; emits the FFN norm's operand
@@ -914,7 +981,7 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     produce_norm(a, l + 1 < d.n_layers ? dec->layers[l + 1].attn_norm : dec->w.final_norm);
     return a;
   };
-  const bool chain = use_chain(flags, w4);
+  const bool chain = use_chain(flags, w4) && dec->chain_ok;
   for (int l = 0; l < d.n_layers; ++l) {
     const SunLayerWeights& lw = dec->layers[l];
     GemmArgs a;
@@ -939,7 +1006,7 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
         wb[3] = dec->layers[l + 1].w_qkv;
         nph = 4;
       }
-      if ((s = run_chain(ph, epi, plans, wb, nph, dec->chain_bar, st, pdl)) != SUN_OK) return s;
+      if ((s = run_chain(ph, epi, plans, wb, nph, dec->chain_bar, st, pdl, dec->num_sms)) != SUN_OK) return s;
       continue;
     }
     a = o_args(l);
@@ -970,7 +1037,7 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
   SUN_CUDA(launch(argmax_reduce_kernel, dim3(batch), dim3(kRowThreads), 0, st, pdl, (const float*)dec->amax_val,
                   (const int*)dec->amax_idx, dec->p_lm.m_tiles, bn, next_tokens,
                   (flags & SUN_STEP_FEEDBACK) ? const_cast<int*>(tokens) : (int*)nullptr,
-                  const_cast<int*>(positions)));
+                  const_cast<int*>(positions), dec->err));
   return SUN_OK;
 }
 
@@ -1149,11 +1216,115 @@ SunStatus sun_attention_decode(const SunDecoderDims* dims, const SunKvPool* kv, 
   aa.part_ml = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + align_up(po, 1024));
   aa.counters = reinterpret_cast<unsigned*>(static_cast<uint8_t*>(workspace) + align_up(po, 1024) + align_up(pm, 1024));
   aa.fused_combine = attn_fused_combine();
+  aa.max_ctx = d.max_context;
   aa.out = static_cast<__nv_bfloat16*>(out);
   aa.ld_out = d.n_q_heads * d.head_dim;
   CUtensorMap tm;
   if ((s = make_map_kv(&tm, d, *kv)) != SUN_OK) return s;
   return run_attention(d, tm, aa, batch, static_cast<cudaStream_t>(stream), false);
+}
+
+SunStatus sun_decoder_status(SunDecoder* dec, uint32_t* flags, int32_t clear, void* stream) {
+  if (!dec || !flags) return fail(SUN_ERR_VALUE, "null argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned v = 0;
+  SUN_CUDA(cudaMemcpyAsync(&v, dec->err, 4, cudaMemcpyDeviceToHost, st));
+  if (clear) SUN_CUDA(cudaMemsetAsync(dec->err, 0, 4, st));
+  SUN_CUDA(cudaStreamSynchronize(st));
+  *flags = v;
+  return SUN_OK;
+}
+
+SunStatus sun_decoder_uses_chain(SunDecoder* dec, int32_t flags, int32_t* uses) {
+  if (!dec || !uses) return fail(SUN_ERR_VALUE, "null argument");
+  *uses = (use_chain(flags, dec->d.weight_bits == 4) && dec->chain_ok) ? 1 : 0;
+  return SUN_OK;
+}
+
+SunStatus sun_kv_page_bytes(const SunKvPool* kv, size_t* bytes) {
+  if (!kv || !bytes || kv->n_layers < 1 || kv->n_kv_heads < 1 || kv->head_dim < 1 || kv->page_size < 1)
+    return fail(SUN_ERR_VALUE, "bad KV pool geometry");
+  *bytes = kv_page_bytes(*kv);
+  return SUN_OK;
+}
+
+// ---- K8 hand-off by peer copy -------------------------------------------------
+SunStatus sun_kv_pool_export(const SunKvPool* kv, SunKvPoolHandle* out) {
+  if (!kv || !out || !kv->base) return fail(SUN_ERR_VALUE, "null argument");
+  const PFN_getAddressRange_t range_fn = address_range_fn();
+  if (!range_fn) return fail(SUN_ERR_CUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range_fn(&base, &size, reinterpret_cast<CUdeviceptr>(kv->base)) != CUDA_SUCCESS)
+    return fail(SUN_ERR_CUDA, "cuMemGetAddressRange failed for the KV pool");
+  cudaIpcMemHandle_t h;
+  SUN_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  static_assert(sizeof(h) <= sizeof(out->ipc), "IPC handle size");
+  memset(out, 0, sizeof(*out));
+  memcpy(out->ipc, &h, sizeof(h));
+  out->offset = static_cast<int64_t>(reinterpret_cast<CUdeviceptr>(kv->base) - base);
+  out->geometry = *kv;
+  out->geometry.base = nullptr;
+  return SUN_OK;
+}
+
+SunStatus sun_kv_pool_import(const SunKvPoolHandle* handle, SunKvPool* out) {
+  if (!handle || !out) return fail(SUN_ERR_VALUE, "null argument");
+  int here = 0;
+  SUN_CUDA(cudaGetDevice(&here));
+  const int peer = handle->geometry.device;
+  if (peer != here) {  // copy engines reach the peer's HBM over NVLink
+    int can = 0;
+    SUN_CUDA(cudaDeviceCanAccessPeer(&can, here, peer));
+    if (!can) return fail(SUN_ERR_UNSUPPORTED, "device %d cannot access device %d's memory", here, peer);
+    const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) SUN_CUDA(e);
+    cudaGetLastError();
+  }
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle->ipc, sizeof(h));
+  void* base = nullptr;
+  SUN_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  *out = handle->geometry;
+  out->base = static_cast<uint8_t*>(base) + handle->offset;
+  return SUN_OK;
+}
+
+SunStatus sun_kv_pool_close(SunKvPool* imported) {
+  if (!imported || !imported->base) return fail(SUN_ERR_VALUE, "null argument");
+  // the mapping starts `offset` bytes before page 0: close the mapped allocation's base
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (address_range_fn() == nullptr ||
+      address_range_fn()(&base, &size, reinterpret_cast<CUdeviceptr>(imported->base)) != CUDA_SUCCESS)
+    return fail(SUN_ERR_CUDA, "cuMemGetAddressRange failed for the imported pool");
+  SUN_CUDA(cudaIpcCloseMemHandle(reinterpret_cast<void*>(base)));
+  imported->base = nullptr;
+  return SUN_OK;
+}
+
+SunStatus sun_kv_handoff_copy(const SunKvPool* src, const int32_t* src_pages, const SunKvPool* dst,
+                              const int32_t* dst_pages, int32_t n_pages, void* stream) {
+  if (!src || !dst || (n_pages > 0 && (!src_pages || !dst_pages))) return fail(SUN_ERR_VALUE, "null argument");
+  if (n_pages < 0) return fail(SUN_ERR_VALUE, "negative page count");
+  if (src->n_layers != dst->n_layers || src->n_kv_heads != dst->n_kv_heads || src->head_dim != dst->head_dim ||
+      src->page_size != dst->page_size || src->rope_theta != dst->rope_theta)
+    return fail(SUN_ERR_MIXED_DECODER, "hand-off between KV pools of different geometry (not decoder-compatible)");
+  const size_t pb = kv_page_bytes(*src);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int i = 0; i < n_pages; ++i)  // validate everything before the first copy
+    if (src_pages[i] < 0 || src_pages[i] >= src->num_pages || dst_pages[i] < 0 || dst_pages[i] >= dst->num_pages)
+      return fail(SUN_ERR_VALUE, "hand-off page %d -> %d outside the pools", src_pages[i], dst_pages[i]);
+  for (int i = 0; i < n_pages;) {
+    const int s0 = src_pages[i], d0 = dst_pages[i];
+    int n = 1;  // maximal run consecutive on both sides: one copy
+    while (i + n < n_pages && src_pages[i + n] == s0 + n && dst_pages[i + n] == d0 + n) ++n;
+    SUN_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(dst->base) + size_t(d0) * pb,
+                             static_cast<const uint8_t*>(src->base) + size_t(s0) * pb, size_t(n) * pb,
+                             cudaMemcpyDefault, st));
+    i += n;
+  }
+  return SUN_OK;
 }
 
 SunStatus sun_blocked_bytes(int64_t rows, int64_t k, size_t* bytes) {

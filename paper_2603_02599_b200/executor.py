@@ -42,6 +42,17 @@ class B200Executor:
         self.keep_logits = keep_logits
         self.logits: dict[int, list] = {}  # request id -> [first-token logits, step logits...] (testing)
 
+    def fits(self, m: Member, batch: int) -> str:
+        """Physical admission (scheduler.StepExecutor.fits): the final-footprint pages
+        and the decoder's context / batch limits of this GPU."""
+        r = m.request
+        need = pages_for(r.isl + r.target_osl - 1)
+        if need > self.alloc.num_pages or r.isl + r.target_osl - 1 > self.dec.max_context:
+            return "never"
+        if batch >= self.dec.max_batch or need > self.alloc.free_pages:
+            return "never" if batch == 0 else "wait"
+        return "ok"
+
     def admit(self, m: Member) -> None:
         r = m.request
         m.kv.pages = self.alloc.alloc(pages_for(r.isl + r.target_osl - 1))

@@ -99,7 +99,8 @@ def attention_decode(dims: _lib.SunDecoderDims, kv_pool: torch.Tensor, layer: in
     max_pages = (dims.max_context + 15) // 16
     ws = torch.zeros(batch * dims.n_q_heads * max_pages * (dims.head_dim + 2) * 4 + batch * dims.n_kv_heads * 4 + 8192,
                      dtype=torch.uint8, device=q.device)  # zeroed: split counters must start at 0
-    pool = _lib.SunKvPool(kv_pool.data_ptr(), kv_pool.shape[0])
+    pool = _lib.SunKvPool(kv_pool.data_ptr(), kv_pool.shape[0], dims.n_layers, dims.n_kv_heads, dims.head_dim,
+                          dims.page_size, dims.rope_theta, q.device.index or 0)
     lib = _lib.load()
     _lib.check(lib.sun_attention_decode(ctypes.byref(dims), ctypes.byref(pool), layer, q.data_ptr(),
                                         positions.data_ptr(), block_tables.data_ptr(), block_tables.stride(0),

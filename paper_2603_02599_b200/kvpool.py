@@ -34,6 +34,16 @@ class KvPool:
                                   dtype=torch.bfloat16, device=device)
         self.page_bytes = spec.n_layers * 2 * spec.n_kv_heads * PAGE_TOKENS * spec.head_dim * 2
 
+    def struct(self):
+        """The C ``SunKvPool`` (include/sun_b200.h): base, size and the KV geometry every
+        decoder over this pool must match (SUN_ERR_MIXED_DECODER otherwise)."""
+        from . import _lib
+
+        dev = self.tensor.device
+        return _lib.SunKvPool(self.tensor.data_ptr(), self.num_pages, self.spec.n_layers, self.spec.n_kv_heads,
+                              self.spec.head_dim, PAGE_TOKENS, float(self.spec.rope_theta),
+                              dev.index if dev.type == "cuda" and dev.index is not None else 0)
+
     @classmethod
     def for_bytes(cls, spec: DecoderSpec, nbytes: int, device) -> "KvPool":
         page_bytes = spec.n_layers * 2 * spec.n_kv_heads * PAGE_TOKENS * spec.head_dim * 2

@@ -50,13 +50,13 @@ class _StepRunner:
             vocab=spec.vocab, hidden=spec.hidden, n_layers=spec.n_layers, n_q_heads=spec.n_q_heads,
             n_kv_heads=spec.n_kv_heads, head_dim=spec.head_dim, ffn=spec.ffn, page_size=PAGE_TOKENS,
             max_context=self.max_context, weight_bits=spec.weight_bits, group_size=spec.group_size,
-            qkv_bias=int(spec.qkv_bias), rms_eps=spec.rms_eps)
+            qkv_bias=int(spec.qkv_bias), rms_eps=spec.rms_eps, rope_theta=spec.rope_theta)
         nb = ctypes.c_size_t()
         _lib.check(lib.sun_decoder_workspace_bytes(ctypes.byref(self.dims), self.max_batch, ctypes.byref(nb)),
                    "workspace sizing")
         dev = weights.device
         self.workspace = torch.zeros(nb.value, dtype=torch.uint8, device=dev)
-        self._pool = _lib.SunKvPool(kv.tensor.data_ptr(), kv.num_pages)
+        self._pool = kv.struct()
         h = ctypes.c_void_p()
         _lib.check(lib.sun_decoder_create(ctypes.byref(self.dims), ctypes.byref(weights.struct),
                                           ctypes.byref(self._pool), self.workspace.data_ptr(), self.workspace.numel(),
@@ -65,7 +65,44 @@ class _StepRunner:
         self._lib = lib
         import os as _os
         self.fused_combine = _os.environ.get("SUN_ATTN_FUSED_COMBINE", "0") == "1"
-        self.gemm_chain = uses_gemm_chain(spec.weight_bits, self.distinct_rows, _os.environ.get("SUN_GEMM_CHAIN"))
+        flags = _lib.SUN_STEP_DISTINCT_ROWS if self.distinct_rows else 0
+        chain = ctypes.c_int32()
+        _lib.check(lib.sun_decoder_uses_chain(h, flags, ctypes.byref(chain)), "sun_decoder_uses_chain")
+        self.gemm_chain = bool(chain.value)  # (the library also checks the grid fits this device)
+
+    def status(self, clear: bool = True) -> int:
+        """The decoder's device error word (SUN_STEP_ERR_* bits raised by the steps
+        since the last clear; synchronises the current stream)."""
+        v = ctypes.c_uint32()
+        _lib.check(self._lib.sun_decoder_status(self._h, ctypes.byref(v), int(clear),
+                                                torch.cuda.current_stream().cuda_stream), "sun_decoder_status")
+        return v.value
+
+    def check(self) -> None:
+        """Raise ValueError if a step since the last check saw invalid inputs."""
+        bits = self.status(clear=True)
+        if bits:
+            names = [n for b, n in ((_lib.SUN_STEP_ERR_TOKEN, "token outside the vocabulary"),
+                                    (_lib.SUN_STEP_ERR_POSITION, "position outside [0, max_context)"),
+                                    (_lib.SUN_STEP_ERR_PAGE, "block-table page outside the KV pool"),
+                                    (_lib.SUN_STEP_ERR_NAN, "logits without a finite maximum")) if bits & b]
+            raise ValueError("decode step inputs invalid: " + "; ".join(names))
+
+    def validate_host(self, tokens: torch.Tensor, positions: torch.Tensor, block_tables: torch.Tensor) -> None:
+        """Host-side bounds of a batch given in host memory (the device re-checks)."""
+        if tokens.device.type != "cpu":
+            return
+        if tokens.numel() and (int(tokens.min()) < 0 or int(tokens.max()) >= self.spec.vocab):
+            raise ValueError("token outside the vocabulary")
+        if positions.numel() and (int(positions.min()) < 0 or int(positions.max()) >= self.max_context):
+            raise ValueError(f"position outside [0, {self.max_context})")
+        npg = (positions.to(torch.int64) // PAGE_TOKENS + 1).clamp(max=block_tables.shape[1])
+        used = torch.arange(block_tables.shape[1])[None, :] < npg[:, None]
+        pages = block_tables[used]
+        if pages.numel() and (int(pages.min()) < 0 or int(pages.max()) >= self.kv.num_pages):
+            raise ValueError("block-table page outside the KV pool")
+        if int((positions.to(torch.int64) // PAGE_TOKENS).max()) >= block_tables.shape[1]:
+            raise ValueError("block table shorter than a position needs")
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -165,10 +202,12 @@ class SharedDecodeModule(_StepRunner):
         key = (batch, pages_per_split, feedback)
         g = self._graphs.get(key)
         if g is None:
-            # warm (TMA descriptor cache for this batch bucket) then capture
+            # warm (TMA descriptor cache for this batch bucket) then capture; the
+            # inputs are saved before the side stream is ordered after the current one,
+            # so the warm launch (whose feedback advances them) runs after the clones
+            saved = (self.tokens.clone(), self.positions.clone())
             s = torch.cuda.Stream()
             s.wait_stream(torch.cuda.current_stream())
-            saved = (self.tokens.clone(), self.positions.clone())
             with torch.cuda.stream(s):
                 self.launch(self.tokens, self.positions, self.block_tables, batch, self.next_tokens, self.logits,
                             pages_per_split, feedback)
@@ -198,6 +237,8 @@ class SharedDecodeModule(_StepRunner):
             if t.device.type != "cpu" or not t.is_pinned() or t.dtype != torch.int32:
                 raise ValueError("decode_host takes pinned int32 host tensors")
         npg = int(block_tables.shape[1])
+        if npg > self.max_pages:
+            raise ValueError(f"block table width {npg} > {self.max_pages} pages")
         key = ("host", b, npg, pages_per_split, tokens.data_ptr(), positions.data_ptr(), block_tables.data_ptr(),
                out.data_ptr())
         g = self._graphs.get(key)
@@ -219,7 +260,7 @@ class SharedDecodeModule(_StepRunner):
         return out
 
     def decode(self, tokens: torch.Tensor, positions: torch.Tensor, block_tables: torch.Tensor,
-               pages_per_split: int = 0, graph: bool = True) -> torch.Tensor:
+               pages_per_split: int = 0, graph: bool = True, validate: bool = True) -> torch.Tensor:
         """Eq. 3 over a batch: copy inputs (host or device) into the static
         buffers, run the step, return next tokens (device int32 view [B])."""
         b = int(tokens.shape[0])
@@ -227,6 +268,10 @@ class SharedDecodeModule(_StepRunner):
             raise ValueError("decode batch must be non-empty")
         if b > self.max_batch:
             raise ValueError(f"batch {b} > max_batch {self.max_batch}")
+        if block_tables.shape[1] > self.max_pages:
+            raise ValueError(f"block table width {block_tables.shape[1]} > {self.max_pages} pages")
+        if validate:
+            self.validate_host(tokens, positions, block_tables)
         self.tokens[:b].copy_(tokens, non_blocking=True)
         self.positions[:b].copy_(positions, non_blocking=True)
         self.block_tables[:b, :block_tables.shape[1]].copy_(block_tables, non_blocking=True)

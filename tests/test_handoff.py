@@ -127,3 +127,61 @@ def test_kv_handoff_async_overlap_gloo():
     for payload, g in zip(sent, got):
         assert (payload == g[2]).all()
         assert len(page_runs(g[1])) == 1 and min(g[1]) >= 5  # fresh pages, one contiguous run each
+
+
+def _peer_worker(rank, port, q, shared):
+    """Peer-copy hand-off protocol (handoff.peer_send_kv / peer_recv_kv): the decode
+    rank reserves pages and answers their ids, the prefill rank writes its pages
+    straight into them (here a shared-memory CPU tensor stands in for the decode
+    GPU's IPC-mapped pool and the copy engine), then reports them landed."""
+    from paper_2603_02599_b200.handoff import peer_recv_kv, peer_send_kv
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        if rank == 0:  # prefill side
+            pool = KvPool(TINY, 16, "cpu")
+            g = torch.Generator().manual_seed(300)
+            pool.tensor.copy_(torch.randn(pool.tensor.shape, generator=g).to(torch.bfloat16))
+
+            def copier(src, src_pages, remote, dst_pages):
+                remote[dst_pages] = src.tensor[src_pages]
+
+            out = []
+            for rid, pages in ((21, [3, 4, 5]), (22, [9, 1])):
+                h = KvHandle(request_id=rid, resident_tokens=len(pages) * 16 - 1,
+                             bytes_per_token=TINY.kv_bytes_per_token, pages=pages, model_id=rid % 3)
+                dst = peer_send_kv(h, pool, shared, 1, copier=copier)
+                out.append((dst, pool.tensor[pages].float().numpy().copy()))
+            q.put(("sent", out))
+        else:  # decode side: owns `shared`
+            alloc = PageAllocator(shared.shape[0])
+            alloc.alloc(2)
+            got = []
+            for _ in range(2):
+                p_ = peer_recv_kv(alloc, 0)
+                h = p_.wait()
+                got.append((h.request_id, h.resident_tokens, h.model_id, list(h.pages),
+                            shared[h.pages].float().numpy().copy()))
+            q.put(("recv", got))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_kv_handoff_peer_copy_protocol_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    shared = torch.zeros((20,) + tuple(KvPool(TINY, 1, "cpu").tensor.shape[1:]), dtype=torch.bfloat16).share_memory_()
+    procs = [ctx.Process(target=_peer_worker, args=(r, port, q, shared)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((m[0], m[1:]) for m in (q.get(timeout=120), q.get(timeout=120)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    sent, got = res["sent"][0], res["recv"][0]
+    assert [g[0] for g in got] == [21, 22] and got[0][1] == 47 and got[1][2] == 1
+    for (dst, payload), g in zip(sent, got):
+        assert dst == g[3] and min(dst) >= 2 and len(page_runs(dst)) == 1
+        assert (payload == g[4]).all()

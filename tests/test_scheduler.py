@@ -119,3 +119,51 @@ def test_token_conservation_random_configs():
         for r in done:
             chain = r.timestamp_chain()
             assert chain == sorted(chain)
+
+
+class _PagedExecutor:
+    """CPU stand-in for B200Executor's physical admission: a page pool and a batch limit."""
+
+    def __init__(self, pages, max_batch, max_context=10_000):
+        from paper_2603_02599_b200.kvpool import PageAllocator
+
+        self.alloc = PageAllocator(pages)
+        self.max_batch, self.max_context = max_batch, max_context
+        self.max_seen = 0
+
+    def fits(self, m, batch):
+        from paper_2603_02599_b200.kvpool import pages_for
+
+        r = m.request
+        need = pages_for(r.isl + r.target_osl - 1)
+        if need > self.alloc.num_pages or r.isl + r.target_osl - 1 > self.max_context:
+            return "never"
+        if batch >= self.max_batch or need > self.alloc.free_pages:
+            return "never" if batch == 0 else "wait"
+        return "ok"
+
+    def admit(self, m):
+        from paper_2603_02599_b200.kvpool import pages_for
+
+        m.kv.pages = self.alloc.alloc(pages_for(m.request.isl + m.request.target_osl - 1))
+
+    def step(self, members):
+        self.max_seen = max(self.max_seen, len(members))
+        return [0] * len(members)
+
+    def retire(self, m):
+        self.alloc.free(m.kv.pages)
+
+
+def test_physical_admission_blocks_and_rejects():
+    """The executor's page pool / batch limit gate admission like the virtual HBM
+    capacity does (head-of-line blocking, reject-if-never-fits): the loop never asks
+    the GPU for more pages or rows than it has, and everything else completes."""
+    cfg = cluster(1, 1, DecodeRule.LEAST_OUTSTANDING_TOKENS)
+    trace = [Request(id=i, model_id=0, arrival_time=0.01 * i, isl=64, target_osl=17) for i in range(12)]
+    trace.append(Request(id=12, model_id=0, arrival_time=0.2, isl=4000, target_osl=8))  # > the whole pool
+    ex = _PagedExecutor(pages=20, max_batch=3)  # 5 pages per request: at most 3 resident (batch limit)
+    res = scheduler.run(cfg, trace, COST, executors={1: ex})
+    assert ex.max_seen <= 3
+    assert res.log.rejected_ids == [12]
+    assert len(res.completed) == 12 and ex.alloc.free_pages == 20
