@@ -671,6 +671,11 @@ SUN_DEVICE void w4_dequant_row(uint32_t pk, uint32_t sc, int row, int part, uint
   __nv_bfloat16 sb;
   *reinterpret_cast<unsigned short*>(&sb) = sraw;
   const __nv_bfloat162 s2 = __bfloat162bfloat162(sb);
+#ifdef SUN_W4_NO_CVT  // probe: skip the arithmetic (timing only, results invalid)
+#pragma unroll
+  for (int q = 0; q < 16 * kW4Chunks; ++q) o[q] = words[q & (4 * kW4Chunks - 1)] ^ sraw;
+  return;
+#endif
 #pragma unroll
   for (int q = 0; q < 4 * kW4Chunks; ++q) {
 #pragma unroll
@@ -842,6 +847,9 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
     const uint32_t idesc = make_idesc_bf16(kTileM, a.bn);
     int ks = u0 % KS, seg_left = min(KS - ks, n);
     int xslot = 0, xphase = 0, xpos = 0, aslot = 0, aphase = 0, buf = 0, tphase = 0;
+#ifdef SUN_W4_ROLE_CLOCKS  // probe: MMA warp waits on X / A -> stamps [9], [10], issue [11]
+    long long mk_x = 0, mk_a = 0, mk_i = 0, mk0 = clock64();
+#endif
     for (int j = 0; j < n;) {
       const int nbk = min(kp, seg_left);  // K blocks this iteration (never straddles a segment / stage)
       const bool first = j == 0 || ks == 0, last = seg_left == nbk;
@@ -851,24 +859,35 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
         tc_fence_after();
       }
       if (xpos == 0) mbar_wait(&xfull[xslot], xphase);
+#ifdef SUN_W4_ROLE_CLOCKS
+      { const long long t_ = clock64(); mk_x += t_ - mk0; mk0 = t_; }
+#endif
       mbar_wait(&dfull[aslot], aphase);
       tc_fence_after();
+#ifdef SUN_W4_ROLE_CLOCKS
+      { const long long t_ = clock64(); mk_a += t_ - mk0; mk0 = t_; }
+#endif
       if (j == 0 && threadIdx.x == 32) SUN_STAMP(2);
       if (elect_one()) {
         const uint32_t xa = smem_u32(xstg + xslot * xsb) + static_cast<uint32_t>(xpos) * 2u * a.bn * 128u;
         const uint32_t tacc = tmem_base + static_cast<uint32_t>(buf * a.bn);
         const uint32_t ta = tmem_base + static_cast<uint32_t>(512 - 64 * kp * (aslot + 1));
+#ifndef SUN_W4_NO_MMA  // probe: skip the MMAs (timing only, results invalid)
         for (int b = 0; b < nbk; ++b)
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
             umma_bf16_ta(tacc, ta + b * 64 + kk * 8,
                          make_sw128_desc(xa + (2 * b + (kk >> 2)) * (a.bn * 128u) + (kk & 3) * 32), idesc,
                          (first && b == 0 && kk == 0) ? 0u : 1u);
+#endif
         umma_commit(&dempty[aslot]);
         if (xlast) umma_commit(&xempty[xslot]);
         if (last) umma_commit(&tfull[buf]);
       }
       __syncwarp();
+#ifdef SUN_W4_ROLE_CLOCKS
+      { const long long t_ = clock64(); mk_i += t_ - mk0; mk0 = t_; }
+#endif
       if (++aslot == na) {
         aslot = 0;
         aphase ^= 1;
@@ -895,6 +914,13 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
       }
     }
     if (threadIdx.x == 32) SUN_STAMP(3);
+#ifdef SUN_W4_ROLE_CLOCKS
+    if (threadIdx.x == 32 && a.stamps) {
+      a.stamps[blockIdx.x * 16 + 9] = mk_x;
+      a.stamps[blockIdx.x * 16 + 10] = mk_a;
+      a.stamps[blockIdx.x * 16 + 11] = mk_i;
+    }
+#endif
   } else if (!W4 && (warp == 0 || warp == 6)) {
     // ---------------- bf16 producers (blocking, one per ring): warp 0 streams the
     // weight stages (32 KB: one 128-wide K step of SUN-BLK), warp 6 the activation
@@ -1034,15 +1060,25 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
     const uint32_t lane_off = static_cast<uint32_t>(lg * 32) << 16;
     int ks = u0 % KS, seg_left = min(KS - ks, n);
     int wslot = 0, wphase = 0, wpos = 0, aslot = 0, aphase = 0, it = 0;
+#ifdef SUN_W4_ROLE_CLOCKS  // probe: per-role cycle split of converter warp 6 -> stamps [12..15]
+    long long ck_w = 0, ck_c = 0, ck_a = 0, ck_s = 0, ck0 = clock64();
+#define SUN_CK(acc) do { const long long t_ = clock64(); acc += t_ - ck0; ck0 = t_; } while (0)
+#else
+#define SUN_CK(acc) do {} while (0)
+#endif
     for (int j = 0; j < n;) {
       const int nbk = min(kp, seg_left);
       if (wpos == 0) mbar_wait(&full[wslot], wphase);
+      SUN_CK(ck_w);
       const bool wlast = wpos + nbk == wg || seg_left == nbk;
       const uint32_t st = smem_u32(stg + wslot * sb);
       uint32_t o0[16 * kW4Chunks], o1[16 * kW4Chunks];
+#ifndef SUN_W4_PROBE_STREAM  // probe: converters only pass the stages through (timing only)
       w4_dequant_row(st + wpos * kW4PackedBytes, st + wg * kW4PackedBytes + wpos * 256u, row, part, o0);
       if (nbk == 2)
         w4_dequant_row(st + (wpos + 1) * kW4PackedBytes, st + wg * kW4PackedBytes + (wpos + 1) * 256u, row, part, o1);
+#endif
+      SUN_CK(ck_c);
       if (wlast) {  // this warp is done reading the weight stage
         __syncwarp();
         if (elect_one()) mbar_arrive(&empty[wslot]);
@@ -1056,12 +1092,18 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
       }
       if (it >= na) mbar_wait(&dempty[aslot], aphase ^ 1);  // MMA it-na done with this A slot
       tc_fence_after();
+      SUN_CK(ck_a);
       const uint32_t ta = tmem_base + lane_off + static_cast<uint32_t>(512 - 64 * kp * (aslot + 1) + 16 * kW4Chunks * part);
+#if !defined(SUN_W4_PROBE_STREAM) && !defined(SUN_W4_PROBE_NOTST)  // probes: no TMEM stores (timing only)
       tmem_st(ta, o0);
       if (nbk == 2) tmem_st(ta + 64, o1);
+#else
+      if (o0[0] == 0x12345u && o1[0] == 0x12345u) asm volatile("trap;");  // keep the dequant live
+#endif
       tc_fence_before();
       __syncwarp();
       if (elect_one()) mbar_arrive(&dfull[aslot]);
+      SUN_CK(ck_s);
       if (++aslot == na) {
         aslot = 0;
         aphase ^= 1;
@@ -1071,6 +1113,15 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
       seg_left -= nbk;
       if (seg_left == 0) seg_left = min(KS, n - j);
     }
+#ifdef SUN_W4_ROLE_CLOCKS
+    if (warp == 6 && (threadIdx.x & 31) == 0 && a.stamps) {
+      a.stamps[blockIdx.x * 16 + 12] = ck_w;
+      a.stamps[blockIdx.x * 16 + 13] = ck_c;
+      a.stamps[blockIdx.x * 16 + 14] = ck_a;
+      a.stamps[blockIdx.x * 16 + 15] = ck_s;
+    }
+#endif
+#undef SUN_CK
     if (w4join && !clustered && warp >= 7 && warp < 11 && last_full_tile()) {
       // epilogue group B for the last tile: chunks alternate with group A
       asm volatile("bar.sync 4, 256;" ::: "memory");
