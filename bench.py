@@ -435,9 +435,9 @@ def gpu_arm(args, cfg):
     # launches inside the timed region: graph replays do not pass through the
     # library's host launch counter, so count the kernels of one captured step
     prof = dec.profile(dec.tokens, dec.positions, dec.block_tables, B, dec.next_tokens, None, args.pps)
-    names = dec.kernel_names()
+    names = dec.kernel_names(batch=B)
     if len(names) != len(prof):  # unsplit attention: no combine launches
-        names = dec.kernel_names(combine=False)
+        names = dec.kernel_names(combine=False, batch=B)
     per_step_launches = len(names)
     gpu_launches = per_step_launches * args.steps
 

@@ -165,8 +165,9 @@ SunStatus sun_decoder_destroy(SunDecoder* dec);
 /* flags: every row is a different sequence (a decode batch; not token-parallel prefill
  * rows of one prompt): the step's KV append then touches only each row's last page,
  * so the attention stages the other pages while the QKV kernel is still finishing */
-#define SUN_STEP_DISTINCT_ROWS 2 /* (bf16: also selects the persistent layer GEMM chain, which
-                                     needs the whole GPU: one such step in flight per GPU) */
+#define SUN_STEP_DISTINCT_ROWS 2 /* (also selects the persistent layer GEMM chain — bf16, and
+                                     QSUN for batches up to 128 — which needs the whole GPU: one
+                                     such step in flight per GPU) */
 SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t* positions,
                           const int32_t* block_tables, int32_t bt_stride, int32_t batch,
                           int32_t pages_per_split, float* logits, int32_t* next_tokens, int32_t flags,
@@ -214,8 +215,9 @@ SunStatus sun_launch_count(int64_t* launches);
 SunStatus sun_decoder_status(SunDecoder* dec, uint32_t* flags, int32_t clear, void* stream);
 
 /* Whether sun_decode_step runs the persistent layer GEMM chain for these flags on
- * this decoder (bf16, SUN_STEP_DISTINCT_ROWS, and a grid that fits this device's
- * SMs co-resident — checked with the occupancy API at create). */
+ * this decoder (SUN_STEP_DISTINCT_ROWS, and a grid that fits this device's SMs
+ * co-resident — checked with the occupancy API at create; QSUN decoders: for batches
+ * up to 128, larger ones use separate GEMM launches). */
 SunStatus sun_decoder_uses_chain(SunDecoder* dec, int32_t flags, int32_t* uses_chain);
 
 /* ---- K8: prefill -> decode KV hand-off by peer copy (replaces transfer_time,

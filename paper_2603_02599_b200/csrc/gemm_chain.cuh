@@ -470,4 +470,478 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_chain_kernel(const __gri
   tl_end(c.tl, c.tl_idx);
 }
 
+// Arrive on the mbarrier at cluster-shared address `remote` (another CTA of the
+// cluster), releasing this CTA's prior shared-memory writes at cluster scope.
+SUN_DEVICE void mbar_arrive_cluster(uint32_t remote) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+SUN_DEVICE void chain_wait_mbar_cluster(uint64_t* bar, uint32_t parity) {  // acquire at cluster scope
+  const unsigned long long t0 = gtimer();
+  for (;;) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (gtimer() - t0 > kChainWatchdogNs) __trap();
+  }
+}
+
+#ifdef SUN_W4_SEG_STAMPS  // probe: O-phase segment epilogue split -> chain stamps [12..15] (overwrites QKV's)
+#define SUN_SEGSTAMP(i) \
+  do { if (seg_stamps && threadIdx.x == 64) seg_stamps[blockIdx.x * 16 + (i)] = gtimer(); } while (0)
+#else
+#define SUN_SEGSTAMP(i) do {} while (0)
+#endif
+template <int EPI>
+SUN_DEVICE void w4_chain_segment(const GemmArgs& a, const PhaseSched& ps, int tile, uint32_t taddr, float* epi,
+                                 uint64_t* tempty_buf, float* park, uint64_t* pbar,
+                                 unsigned long long* seg_stamps = nullptr) {
+  SUN_SEGSTAMP(12);
+  const int q = static_cast<int>(threadIdx.x >> 5) & 3;
+  const int row_local = q * 32 + (threadIdx.x & 31);
+  auto bar = [&]() { epi_bar(); };
+  if (ps.S == 1) {
+    direct_epilogue<EPI>(a, tile, taddr, epi, 1);
+    tc_fence_before();
+    bar();
+    if (threadIdx.x == 64) mbar_arrive(tempty_buf);
+    return;
+  }
+  const int S = ps.S, rank = ps.rank;
+  if (!a.vcluster) {
+    // hardware cluster (S = 2 or 4 ranks of the tile in one 4-CTA cluster), pull mode:
+    // park the partial in this CTA's idle activation ring (its last MMA of the phase is
+    // done; the next phase's activations wait for every CTA's epilogue), tell the S - 1
+    // peers, then reduce our chunks reading the peers' partials over DSMEM in rank order
+    // (the L2 path's sums). The peers' rings stay untouched until the phase count.
+    const int cta0 = static_cast<int>(blockIdx.x & 3u) - rank;  // cluster rank of the tile's rank 0
+    {
+      float v[16];
+      for (int c0 = 0; c0 < a.bn; c0 += 16) {
+        tmem_ld16(taddr + c0, v);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          *reinterpret_cast<float4*>(park + part_index(c0, j, row_local)) =
+              make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      }
+    }
+    tc_fence_before();
+    bar();
+    SUN_SEGSTAMP(13);
+    if (threadIdx.x == 64) {
+      mbar_arrive(tempty_buf);  // accumulator read: the MMA may reuse it
+      asm volatile("fence.acq_rel.cluster;" ::: "memory");
+      for (int r = 0; r < S; ++r)
+        if (r != rank) mbar_arrive_cluster(dsmem_addr(pbar, static_cast<uint32_t>(cta0 + r)));
+    }
+    chain_wait_mbar_cluster(pbar, 0);  // every peer's partial is parked
+    SUN_SEGSTAMP(14);
+    auto reduce_cols = [&](int c0, int q0, auto& v) {
+      constexpr int NQ = sizeof(v) / sizeof(float) / 4;
+      float4 x[4][NQ];
+      const int cbase = c0 & ~15;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int j = 0; j < NQ; ++j)
+          x[u][j] = u >= S ? make_float4(0.f, 0.f, 0.f, 0.f)
+                           : ld_dsmem_f4(dsmem_addr(park + part_index(cbase, q0 + j, row_local), static_cast<uint32_t>(cta0 + u)));
+#pragma unroll
+      for (int j = 0; j < 4 * NQ; ++j) v[j] = 0.f;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) {
+          v[4 * j] += x[u][j].x;
+          v[4 * j + 1] += x[u][j].y;
+          v[4 * j + 2] += x[u][j].z;
+          v[4 * j + 3] += x[u][j].w;
+        }
+    };
+    for (int c0 = rank * 16; c0 < a.bn; c0 += S * 16) {
+      float v[16];
+      reduce_cols(c0, 0, v);
+      epi_chunk<EPI>(a, tile, row_local, c0, v, epi);
+    }
+    bar();
+    SUN_SEGSTAMP(15);
+    return;
+  }
+  float* part = a.sk_part + static_cast<long long>(blockIdx.x) * a.bn * kTileM;
+  {
+    float v[16];
+    for (int c0 = 0; c0 < a.bn; c0 += 16) {
+      tmem_ld16(taddr + c0, v);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        __stcg(reinterpret_cast<float4*>(part + part_index(c0, j, row_local)),
+               make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+    }
+  }
+  __threadfence();
+  tc_fence_before();
+  bar();
+  if (threadIdx.x == 64) mbar_arrive(tempty_buf);  // accumulator parked: the MMA may reuse it
+  unsigned* tile_cnt = a.sk_flags + tile;
+  if (threadIdx.x == 64) {
+    atomicAdd(tile_cnt, 1u);
+    const unsigned long long t0 = gtimer();
+    while (ld_acquire_u32(tile_cnt) < static_cast<unsigned>(S))
+      if (gtimer() - t0 > kChainWatchdogNs) __trap();
+  }
+  bar();
+  const float* gpart = a.sk_part + static_cast<long long>(blockIdx.x - rank) * a.bn * kTileM;
+  auto reduce_cols = [&](int c0, int q0, auto& v) {
+    constexpr int NQ = sizeof(v) / sizeof(float) / 4;
+    float4 x[4][NQ];
+#pragma unroll
+    for (int j = 0; j < 4 * NQ; ++j) v[j] = 0.f;
+    const int cbase = c0 & ~15;
+    for (int r0 = 0; r0 < S; r0 += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int j = 0; j < NQ; ++j)
+          x[u][j] = (r0 + u >= S) ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                  : __ldcg(reinterpret_cast<const float4*>(gpart + static_cast<long long>(r0 + u) * a.bn * kTileM +
+                                                                           part_index(cbase, q0 + j, row_local)));
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) {
+          v[4 * j] += x[u][j].x;
+          v[4 * j + 1] += x[u][j].y;
+          v[4 * j + 2] += x[u][j].z;
+          v[4 * j + 3] += x[u][j].w;
+        }
+    }
+  };
+  for (int c0 = rank * 16; c0 < a.bn; c0 += S * 16) {
+    float v[16];
+    reduce_cols(c0, 0, v);
+    epi_chunk<EPI>(a, tile, row_local, c0, v, epi);
+  }
+  bar();  // the last of the tile's 2S arrivals rearms its counter
+  if (threadIdx.x == 64 && atomicAdd(tile_cnt, 1u) == 2u * S - 1u) *tile_cnt = 0u;
+}
+
+SUN_DEVICE void w4_segment(int epi_kind, const GemmArgs& a, const PhaseSched& ps, int tile, uint32_t taddr, float* epi,
+                           uint64_t* tempty_buf, float* park, uint64_t* pbar, unsigned long long* seg_stamps) {
+  switch (epi_kind) {
+    case EPI_RESID_ADD: w4_chain_segment<EPI_RESID_ADD>(a, ps, tile, taddr, epi, tempty_buf, park, pbar, seg_stamps); break;
+    case EPI_SWIGLU: w4_chain_segment<EPI_SWIGLU>(a, ps, tile, taddr, epi, tempty_buf, park, pbar); break;
+    case EPI_QKV_ROPE: w4_chain_segment<EPI_QKV_ROPE>(a, ps, tile, taddr, epi, tempty_buf, park, pbar); break;
+    default: __trap();
+  }
+}
+
+// QSUN layer chain: the same phases (O -> gate_up -> down -> next QKV) over SUN-W4
+// weights, one persistent launch of plain CTAs (one per SM; split phases reduce
+// through L2). Warp roles as gemm_kernel<EPI, true>: 0 = weight producer (packed +
+// scales stages of wgroup K blocks), 1 = MMA issuer (A from TMEM), 2..5 = epilogue,
+// 6..13 = converters (dequantise into the TMEM A ring), 14 = activation producer.
+// Every ring (weights, activations, TMEM A tiles, TMEM accumulators) runs across
+// the phase boundaries: the converters dequantise the next phase's first weight
+// blocks while the epilogue finishes the current phase, so a phase boundary costs
+// the grid-wide count and the first activation load, not a launch, a TMEM
+// allocation, a ring ramp and the separate kernels' tails.
+__global__ void __launch_bounds__(kW4Threads, 1) gemm_chain_w4_kernel(const __grid_constant__ ChainArgs c) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  tl_begin(c.tl, c.tl_idx);
+  const GemmArgs& a0 = c.ph[0];
+  const int stages = a0.stages, xstages = a0.xstages, bn = a0.bn, wg = a0.wgroup, xk = a0.xk;
+  const uint32_t sb = w4_wstage_bytes(wg);
+  const uint32_t xsb = w4_xstage_bytes(bn, xk);
+  uint8_t* stg = smem;
+  uint8_t* xstg = stg + ((stages * sb + 1023u) & ~1023u);
+  float* epi = reinterpret_cast<float*>(xstg + xstages * xsb);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(epi) + kEpiSmemBytes);
+  uint64_t* empty = full + kMaxWStages;
+  uint64_t* xfull = empty + kMaxWStages;
+  uint64_t* xempty = xfull + kMaxXStages;
+  uint64_t* tfull = xempty + kMaxXStages;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* dfull = tempty + 2;
+  uint64_t* dempty = dfull + kW4MaxABufs;
+  uint64_t* pbar = dempty + kW4MaxABufs;  // [kChainMaxPhases] hardware split phases: the peers' partials are parked
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pbar + kChainMaxPhases);
+  float* park = reinterpret_cast<float*>(xstg);  // split-K partial, in the activation ring (idle at a phase tail)
+  const int warp = warp_id_sync();
+  const unsigned G = gridDim.x;
+  constexpr int kXProd = 6 + kW4ConvThreads / 32;
+  // K blocks per converter / MMA iteration and the TMEM A ring (as gemm_kernel<EPI, true>)
+  const int kp = (bn <= 128 && xk % 2 == 0 && wg % 2 == 0) ? 2 : 1;
+  const int na = min(kW4MaxABufs, (512 - 2 * bn) / (64 * kp));
+
+  if (warp == 0 && elect_one()) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kW4ConvThreads / 32);
+    }
+    for (int s = 0; s < xstages; ++s) {
+      mbar_init(&xfull[s], 1);
+      mbar_init(&xempty[s], 1);
+    }
+    for (int j = 0; j < 2; ++j) {
+      mbar_init(&tfull[j], 1);
+      mbar_init(&tempty[j], 1);
+    }
+    for (int j = 0; j < kW4MaxABufs; ++j) {
+      mbar_init(&dfull[j], kW4ConvThreads / 32);
+      mbar_init(&dempty[j], 1);
+    }
+    for (int p = 0; p < kChainMaxPhases; ++p)  // S - 1 peer arrivals per hardware split phase
+      mbar_init(&pbar[p], (p < c.nph && c.ph[p].splits > 1 && !c.ph[p].vcluster) ? c.ph[p].splits - 1 : 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  // hardware clusters: publish the parked-partial barriers' init cluster-wide; the
+  // epilogue warps wait before their first remote arrive, every other warp before exit
+  if (c.hw) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  pdl_launch_dependents();
+
+  if (warp == 0 || warp == kXProd) {
+    // producers: warp 0 streams every phase's weight stages back to back (no waits but
+    // ring slots); the last warp loads a phase's activations once all CTAs finished the
+    // previous phase (phase 0: once the previous kernel completed)
+    if (elect_one()) {
+      const bool wprod = warp == 0;
+      const int grp = wprod ? wg : xk;
+      const int depth = wprod ? stages : xstages;
+      uint64_t* fb = wprod ? full : xfull;
+      uint64_t* eb = wprod ? empty : xempty;
+      int slot = 0, phase = 0, issued = 0;
+      for (int p = 0; p < c.nph; ++p) {
+        const GemmArgs& a = c.ph[p];
+        const PhaseSched ps = phase_sched(a);
+        if (!wprod) {
+          if (p == 0) pdl_wait();
+          else chain_wait_phase(c.bar, G * p);
+#ifdef SUN_W4_SEG_STAMPS
+          if (p < 3)
+#endif
+          SUN_CSTAMP(4 * p);
+        }
+        const int KS = a.ksteps;
+        int ks = ps.n > 0 ? ps.u0 % KS : 0, seg_left = min(KS - ks, ps.n);
+        for (int j = 0; j < ps.n;) {
+          const int len = min(grp, seg_left);
+          if (issued >= depth) mbar_wait(&eb[slot], phase ^ 1);
+          if (wprod) {
+            const long long blk = static_cast<long long>(ps.u0 + j);  // = tile * KS + ks
+            uint8_t* st = stg + slot * sb;
+            mbar_arrive_expect_tx(&fb[slot], static_cast<uint32_t>(len) * (kW4PackedBytes + 256u));
+            bulk_load_hint(st, a.w4_packed + blk * kW4PackedBytes, len * kW4PackedBytes, &fb[slot], kEvictFirst);
+            bulk_load_hint(st + wg * kW4PackedBytes, a.w4_scales + blk * kTileM, len * 256u, &fb[slot], kEvictFirst);
+          } else {
+            mbar_arrive_expect_tx(&fb[slot], static_cast<uint32_t>(len) * a.bn * 256u);
+            bulk_load_hint(xstg + slot * xsb, a.xact + static_cast<long long>(2 * ks) * a.bn * 128, len * a.bn * 256u,
+                           &fb[slot], kEvictLast);
+          }
+          ++issued;
+          j += len;
+          ks += len;
+          seg_left -= len;
+          if (seg_left == 0) {
+            ks = 0;
+            seg_left = min(KS, ps.n - j);
+          }
+          if (++slot == depth) {
+            slot = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // MMA issuer: A (dequantised weights) from the TMEM ring, X from smem; one TMEM
+    // accumulator double buffer across all phases
+    const uint32_t idesc = make_idesc_bf16(kTileM, bn);
+    int xslot = 0, xphase = 0, xpos = 0, aslot = 0, aphase = 0, buf = 0, tphase = 0;
+    for (int p = 0; p < c.nph; ++p) {
+      const GemmArgs& a = c.ph[p];
+      const PhaseSched ps = phase_sched(a);
+      const int KS = a.ksteps;
+      int ks = ps.n > 0 ? ps.u0 % KS : 0, seg_left = min(KS - ks, ps.n);
+      for (int j = 0; j < ps.n;) {
+        const int nbk = min(kp, seg_left);
+        const bool first = j == 0 || ks == 0, last = seg_left == nbk;
+        const bool xlast = xpos + nbk == xk || last;
+        if (first) {
+          mbar_wait(&tempty[buf], tphase ^ 1);
+          tc_fence_after();
+        }
+        if (xpos == 0) mbar_wait(&xfull[xslot], xphase);
+        mbar_wait(&dfull[aslot], aphase);
+        tc_fence_after();
+#ifdef SUN_W4_SEG_STAMPS
+        if (p < 3)
+#endif
+        if (j == 0 && threadIdx.x == 32) SUN_CSTAMP(4 * p + 1);
+        if (elect_one()) {
+          const uint32_t xa = smem_u32(xstg + xslot * xsb) + static_cast<uint32_t>(xpos) * 2u * bn * 128u;
+          const uint32_t tacc = tmem_base + static_cast<uint32_t>(buf * bn);
+          const uint32_t ta = tmem_base + static_cast<uint32_t>(512 - 64 * kp * (aslot + 1));
+          for (int b = 0; b < nbk; ++b)
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+              umma_bf16_ta(tacc, ta + b * 64 + kk * 8,
+                           make_sw128_desc(xa + (2 * b + (kk >> 2)) * (bn * 128u) + (kk & 3) * 32), idesc,
+                           (first && b == 0 && kk == 0) ? 0u : 1u);
+          umma_commit(&dempty[aslot]);
+          if (xlast) umma_commit(&xempty[xslot]);
+          if (last) umma_commit(&tfull[buf]);
+        }
+        __syncwarp();
+#ifdef SUN_W4_SEG_STAMPS
+        if (p < 3)
+#endif
+        if (j + nbk == ps.n && threadIdx.x == 32) SUN_CSTAMP(4 * p + 2);
+        if (++aslot == na) {
+          aslot = 0;
+          aphase ^= 1;
+        }
+        if (xlast) {
+          xpos = 0;
+          if (++xslot == xstages) {
+            xslot = 0;
+            xphase ^= 1;
+          }
+        } else {
+          xpos += nbk;
+        }
+        ks += nbk;
+        j += nbk;
+        seg_left -= nbk;
+        if (seg_left == 0) {
+          ks = 0;
+          seg_left = min(KS, ps.n - j);
+          if (++buf == 2) {
+            buf = 0;
+            tphase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp < 6) {
+    // epilogue (warps 2..5; a second group taken from the converter warps for each
+    // phase's last segment measured slower: it delays the next phase's first conversions)
+    if (c.hw) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    int buf = 0, tphase = 0;
+    for (int p = 0; p < c.nph; ++p) {
+      const GemmArgs& a = c.ph[p];
+      const PhaseSched ps = phase_sched(a);
+      if (p == 0) {
+        pdl_wait();
+      } else {  // this phase's input, norm statistics and positions are final: one thread polls
+        if (threadIdx.x == 64) chain_wait_phase(c.bar, G * p);
+        epi_bar();
+      }
+      switch (c.epi[p]) {
+        case EPI_RESID_ADD: load_qkv_meta<EPI_RESID_ADD>(a, epi); break;
+        case EPI_SWIGLU: load_qkv_meta<EPI_SWIGLU>(a, epi); break;
+        case EPI_QKV_ROPE: load_qkv_meta<EPI_QKV_ROPE>(a, epi); break;
+        default: __trap();
+      }
+      for (int seg = 0; seg < ps.nseg; ++seg) {
+        mbar_wait(&tfull[buf], tphase);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + static_cast<uint32_t>(buf * bn) + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+        w4_segment(c.epi[p], a, ps, ps.t_first + seg, taddr, epi, &tempty[buf], park, &pbar[p],
+                   p == 0 ? c.stamps : nullptr);
+        if (++buf == 2) {
+          buf = 0;
+          tphase ^= 1;
+        }
+      }
+      epi_bar();
+      if (threadIdx.x == 64) {  // this CTA's outputs of phase p are written
+#ifdef SUN_W4_SEG_STAMPS
+        if (p < 3)
+#endif
+        SUN_CSTAMP(4 * p + 3);
+        __threadfence();
+        atomicAdd(c.bar, 1u);
+      }
+    }
+  } else if (warp < kXProd) {
+    // converters: TMEM lane group warp % 4, K part (warp - 6) / 4
+    const int lg = warp & 3;
+    const int row = lg * 32 + (threadIdx.x & 31);
+    const int part = (warp - 6) >> 2;
+    const uint32_t lane_off = static_cast<uint32_t>(lg * 32) << 16;
+    int wslot = 0, wphase = 0, wpos = 0, aslot = 0, aphase = 0, it = 0;
+    for (int p = 0; p < c.nph; ++p) {
+      const GemmArgs& a = c.ph[p];
+      const PhaseSched ps = phase_sched(a);
+      const int KS = a.ksteps;
+      int seg_left = min(KS - (ps.n > 0 ? ps.u0 % KS : 0), ps.n);
+      for (int j = 0; j < ps.n;) {
+        const int nbk = min(kp, seg_left);
+        if (wpos == 0) mbar_wait(&full[wslot], wphase);
+        const bool wlast = wpos + nbk == wg || seg_left == nbk;
+        const uint32_t st = smem_u32(stg + wslot * sb);
+        uint32_t o0[16 * kW4Chunks], o1[16 * kW4Chunks];
+        w4_dequant_row(st + wpos * kW4PackedBytes, st + wg * kW4PackedBytes + wpos * 256u, row, part, o0);
+        if (nbk == 2)
+          w4_dequant_row(st + (wpos + 1) * kW4PackedBytes, st + wg * kW4PackedBytes + (wpos + 1) * 256u, row, part, o1);
+        if (wlast) {  // this warp is done reading the weight stage
+          __syncwarp();
+          if (elect_one()) mbar_arrive(&empty[wslot]);
+          wpos = 0;
+          if (++wslot == stages) {
+            wslot = 0;
+            wphase ^= 1;
+          }
+        } else {
+          wpos += nbk;
+        }
+        if (it >= na) mbar_wait(&dempty[aslot], aphase ^ 1);  // MMA it-na done with this A slot
+        tc_fence_after();
+        const uint32_t ta =
+            tmem_base + lane_off + static_cast<uint32_t>(512 - 64 * kp * (aslot + 1) + 16 * kW4Chunks * part);
+        tmem_st(ta, o0);
+        if (nbk == 2) tmem_st(ta + 64, o1);
+        tc_fence_before();
+        __syncwarp();
+        if (elect_one()) mbar_arrive(&dfull[aslot]);
+        if (++aslot == na) {
+          aslot = 0;
+          aphase ^= 1;
+        }
+        ++it;
+        j += nbk;
+        seg_left -= nbk;
+        if (seg_left == 0) seg_left = min(KS, ps.n - j);
+      }
+    }
+  }
+  if (c.hw) {  // nobody exits while a peer may still read its parked partial
+    if (!(warp >= 2 && warp < 6)) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+  if (threadIdx.x == 0 && atomicAdd(c.bar + 1, 1u) == G - 1) {  // last CTA out rearms the counters
+    c.bar[0] = 0u;
+    c.bar[1] = 0u;
+  }
+  tl_end(c.tl, c.tl_idx);
+}
+
 }  // namespace sun

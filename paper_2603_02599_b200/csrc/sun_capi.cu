@@ -196,6 +196,7 @@ void init_kernel_attrs() {
     set_max_smem(gemm_kernel<EPI_QKV_ROPE, true>);
     set_max_smem(gemm_kernel<EPI_SWIGLU, true>);
     set_max_smem(gemm_chain_kernel);
+    set_max_smem(gemm_chain_w4_kernel);
     set_max_smem(attn_group_kernel<64>);
     set_max_smem(attn_group_kernel<128>);
     set_max_smem(attn_decode_kernel<64>);
@@ -444,7 +445,8 @@ struct SunDecoder {
   unsigned* chain_bar;
   unsigned* err;  // SUN_STEP_ERR_* bits (sun_decoder_status)
   int num_sms = kNumSms;
-  bool chain_ok = false;  // the layer chain's grid fits this device co-resident (chain_fits)
+  bool chain_ok = false;     // the layer chain's grid fits this device co-resident (chain_fits)
+  bool chain_w4_ok = false;  // same for the QSUN chain (chain_w4_fits)
   GemmPlan p_qkv, p_o, p_gu, p_down, p_lm;
 };
 
@@ -639,12 +641,34 @@ SunStatus run_gemm(const void* wblk, const void* packed, const void* scales, Gem
 // SUN_GEMM_CHAIN=0 / 1 forces it off / on. Its grid-count phase barriers need all
 // 148 CTAs resident together: one step in flight per GPU (the workspace is not
 // re-entrant anyway), no second persistent decoder on another stream.
-bool use_chain(int flags, bool w4) {
+// QSUN (W4) decode batches run the W4 layer chain (gemm_chain_w4_kernel) up to bn = 128:
+// its TMEM holds two accumulators next to the dequantised A ring only up to there.
+constexpr int kW4ChainMaxBn = 128;
+
+bool use_chain(int flags, bool w4, int bn = 16) {
   static int v = [] {
     const char* e = getenv("SUN_GEMM_CHAIN");
     return e ? atoi(e) : -1;
   }();
-  return !w4 && (v == 1 || (v < 0 && (flags & SUN_STEP_DISTINCT_ROWS)));
+  if (w4 && bn > kW4ChainMaxBn) return false;
+  return v == 1 || (v < 0 && (flags & SUN_STEP_DISTINCT_ROWS));
+}
+
+// QSUN chain ring geometry for a batch width (as launch_cfg's W4 defaults): weight
+// stages of 4 K blocks, activation stages of xk blocks, weights fill the rest.
+struct W4ChainCfg {
+  int wgroup, xk, xstages, stages;
+  size_t smem;
+};
+W4ChainCfg w4_chain_cfg(int bn) {
+  W4ChainCfg c{};
+  c.wgroup = 4;
+  c.xk = bn <= 32 ? 4 : 2;
+  c.xstages = bn > 64 ? 2 : 3;
+  const int budget = kSmemPerSm - 2048 - 2048 - int(kEpiSmemBytes) - 1024 - c.xstages * int(w4_xstage_bytes(bn, c.xk));
+  c.stages = std::max(2, std::min(kMaxWStages, budget / int(w4_wstage_bytes(c.wgroup))));
+  c.smem = gemm_smem_bytes_w4(bn, c.wgroup, c.stages, c.xk, c.xstages);
+  return c;
 }
 
 // Can every CTA of the chain's grid be resident at once on this device (one per SM,
@@ -658,6 +682,97 @@ bool chain_fits(int num_sms) {
     return false;
   }
   return per_sm >= 1 && num_sms >= 16;
+}
+
+// Co-resident 4-CTA clusters of the QSUN chain at this shared-memory size (cached).
+int max_active_clusters_w4chain(size_t smem) {
+  static std::map<size_t, int> cache;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(smem);
+  if (it != cache.end()) return it->second;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(4 * kNumSms / 4);
+  cfg.blockDim = dim3(kW4Threads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 4;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, gemm_chain_w4_kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  cache[smem] = n;
+  return n;
+}
+
+bool chain_w4_fits(int num_sms) {
+  int per_sm = 0;
+  const W4ChainCfg w = w4_chain_cfg(kW4ChainMaxBn);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemm_chain_w4_kernel, kW4Threads, w.smem) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return per_sm >= 1 && num_sms >= 16;
+}
+
+// QSUN layer chain: one CTA per SM, split phases (<= G tiles) as virtual clusters
+// reduced through L2, whole tiles otherwise; packed[i] / scales[i] per phase.
+SunStatus run_chain_w4(GemmArgs* ph, const int* epi, const GemmPlan* plans, const void* const* packed,
+                       const void* const* scales, int nph, unsigned* bar, cudaStream_t st, bool pdl, int num_sms) {
+  ChainArgs c;
+  memset(&c, 0, sizeof(c));
+  const int bn = ph[0].bn;
+  const W4ChainCfg w = w4_chain_cfg(bn);
+  // 4-CTA clusters (SUN_CHAIN_CLUSTER, default on) when every cluster of the grid can be
+  // resident at once: split phases with S = 4 or 2 reduce over DSMEM (partials parked in
+  // the idle activation ring), the rest through L2; else 148 plain CTAs, L2 only
+  static const int cl_env = [] { const char* e = getenv("SUN_CHAIN_CLUSTER"); return e ? atoi(e) : 1; }();
+  int G = num_sms;
+  if (cl_env) {
+    const int ncl = std::min(num_sms / 4, max_active_clusters_w4chain(w.smem));
+    bool any = false;
+    for (int i = 0; i < nph; ++i)
+      any = any || (plans[i].m_tiles <= ncl && plans[i].ksteps >= 4 && 4 * ncl / plans[i].m_tiles >= 4);
+    if (ncl >= 16 && (any || cl_env == 2)) {
+      c.hw = 1;
+      G = 4 * ncl;
+    }
+  }
+  for (int i = 0; i < nph; ++i) {
+    GemmArgs a = ph[i];
+    const GemmPlan& p = plans[i];
+    a.wblk = nullptr;
+    a.w4_packed = static_cast<const uint8_t*>(packed[i]);
+    a.w4_scales = static_cast<const __nv_bfloat16*>(scales[i]);
+    a.stages = w.stages;
+    a.xstages = w.xstages;
+    a.wgroup = w.wgroup;
+    a.xk = w.xk;
+    const int want = p.m_tiles <= G ? std::min(std::min(8, G / std::max(1, p.m_tiles)), p.ksteps) : 1;
+    if (c.hw && want >= 2 && p.ksteps >= 4) {  // 4 / S tiles per cluster, DSMEM
+      a.splits = want >= 4 ? 4 : 2;
+      a.vcluster = 0;
+    } else {
+      a.splits = want;
+      a.vcluster = want > 1 ? 1 : 0;
+    }
+    a.sk_units = 0;
+    c.ph[i] = a;
+    c.epi[i] = epi[i];
+  }
+  c.nph = nph;
+  c.bar = bar;
+  tl_assign(c);
+  if (g_tl.stamps != nullptr && c.tl != nullptr && c.tl_idx == g_tl.stamp_idx) c.stamps = g_tl.stamps;
+  g_cluster = c.hw ? 4u : 1u;
+  SUN_CUDA(launch(gemm_chain_w4_kernel, dim3(G), dim3(kW4Threads), w.smem, st, pdl, c));
+  return SUN_OK;
 }
 
 SunStatus run_chain(GemmArgs* ph, const int* epi, const GemmPlan* plans, const void* const* wblk, int nph,
@@ -809,6 +924,7 @@ SunStatus sun_decoder_create(const SunDecoderDims* dims, const SunWeights* weigh
   SunDecoder* dec = new SunDecoder();
   dec->num_sms = device_sms();
   dec->chain_ok = chain_fits(dec->num_sms);
+  dec->chain_w4_ok = chain_w4_fits(dec->num_sms);
   dec->d = *dims;
   dec->max_batch = max_batch;
   dec->bmp = round16(max_batch);
@@ -981,7 +1097,7 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     produce_norm(a, l + 1 < d.n_layers ? dec->layers[l + 1].attn_norm : dec->w.final_norm);
     return a;
   };
-  const bool chain = use_chain(flags, w4) && dec->chain_ok;
+  const bool chain = use_chain(flags, w4, bn) && (w4 ? dec->chain_w4_ok : dec->chain_ok);
   for (int l = 0; l < d.n_layers; ++l) {
     const SunLayerWeights& lw = dec->layers[l];
     GemmArgs a;
@@ -1000,13 +1116,17 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
       int epi[4] = {EPI_RESID_ADD, EPI_SWIGLU, EPI_RESID_ADD, EPI_QKV_ROPE};
       GemmPlan plans[4] = {dec->p_o, dec->p_gu, dec->p_down, dec->p_qkv};
       const void* wb[4] = {lw.w_o, lw.w_gate_up, lw.w_down, nullptr};
+      const void* sc[4] = {lw.s_o, lw.s_gate_up, lw.s_down, nullptr};
       int nph = 3;
       if (l + 1 < d.n_layers) {
         ph[3] = qkv_args(l + 1);
         wb[3] = dec->layers[l + 1].w_qkv;
+        sc[3] = dec->layers[l + 1].s_qkv;
         nph = 4;
       }
-      if ((s = run_chain(ph, epi, plans, wb, nph, dec->chain_bar, st, pdl, dec->num_sms)) != SUN_OK) return s;
+      s = w4 ? run_chain_w4(ph, epi, plans, wb, sc, nph, dec->chain_bar, st, pdl, dec->num_sms)
+             : run_chain(ph, epi, plans, wb, nph, dec->chain_bar, st, pdl, dec->num_sms);
+      if (s != SUN_OK) return s;
       continue;
     }
     a = o_args(l);
@@ -1237,7 +1357,8 @@ SunStatus sun_decoder_status(SunDecoder* dec, uint32_t* flags, int32_t clear, vo
 
 SunStatus sun_decoder_uses_chain(SunDecoder* dec, int32_t flags, int32_t* uses) {
   if (!dec || !uses) return fail(SUN_ERR_VALUE, "null argument");
-  *uses = (use_chain(flags, dec->d.weight_bits == 4) && dec->chain_ok) ? 1 : 0;
+  const bool w4 = dec->d.weight_bits == 4;  // QSUN: for batches up to kW4ChainMaxBn
+  *uses = (use_chain(flags, w4) && (w4 ? dec->chain_w4_ok : dec->chain_ok)) ? 1 : 0;
   return SUN_OK;
 }
 

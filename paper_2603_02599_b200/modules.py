@@ -20,10 +20,14 @@ from .spec import DecoderSpec
 from .weights import DeviceWeights
 
 
-def uses_gemm_chain(weight_bits: int, distinct_rows: bool, env: str | None) -> bool:
+W4_CHAIN_MAX_BATCH = 128  # sun_capi.cu kW4ChainMaxBn: QSUN chain up to bn = 128
+
+
+def uses_gemm_chain(weight_bits: int, distinct_rows: bool, env: str | None, batch: int = 1) -> bool:
     """Whether sun_decode_step runs the persistent layer GEMM chain (mirrors
-    sun_capi.cu use_chain): bf16 decode batches by default, SUN_GEMM_CHAIN=0/1 forces."""
-    if weight_bits != 16:
+    sun_capi.cu use_chain): decode batches by default (QSUN: up to 128 rows),
+    SUN_GEMM_CHAIN=0/1 forces."""
+    if weight_bits == 4 and (batch + 15) // 16 * 16 > W4_CHAIN_MAX_BATCH:
         return False
     if env is not None:
         try:
@@ -148,12 +152,15 @@ class _StepRunner:
             ctypes.byref(n)), "sun_decode_step_profile")
         return [buf[i] for i in range(min(n.value, cap))]
 
-    def kernel_names(self, combine: bool | None = None) -> list[str]:
-        """Launch order of one step (matches sun_decode_step). The split combine
-        is launched unless fused or the attention ran unsplit (combine=False)."""
+    def kernel_names(self, combine: bool | None = None, batch: int | None = None) -> list[str]:
+        """Launch order of one step of `batch` rows (default max_batch; matches
+        sun_decode_step). The split combine is launched unless fused or the attention
+        ran unsplit (combine=False)."""
         combine = (not self.fused_combine) if combine is None else combine
+        batch = self.max_batch if batch is None else batch
+        chain = self.gemm_chain and (self.spec.weight_bits == 16 or (batch + 15) // 16 * 16 <= W4_CHAIN_MAX_BATCH)
         names = ["embed_norm"]
-        if self.gemm_chain:  # O -> gate_up -> down -> next QKV as one launch per layer
+        if chain:  # O -> gate_up -> down -> next QKV as one launch per layer
             names.append("gemm_qkv_rope_kv")
             for _ in range(self.spec.n_layers):
                 names += ["attention"] + (["attn_combine"] if combine else []) + ["gemm_chain"]

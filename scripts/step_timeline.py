@@ -54,7 +54,7 @@ t0 = t[:, 0].min()
 t = (t - t0) / 1e3
 short = {"gemm_qkv_rope_kv": "qkv", "attention": "attn", "gemm_o_resid_norm": "o", "gemm_gate_up_swiglu": "gate_up",
          "gemm_down_resid_norm": "down", "gemm_chain": "chain", "gemm_lm_head_argmax": "lm_head"}
-lab = [short[k] for k in dec.kernel_names(combine=False) if k in short]  # the launches that record a timeline slot
+lab = [short[k] for k in dec.kernel_names(combine=False, batch=B) if k in short]  # the launches that record a timeline slot
 assert len(lab) == n.value, (len(lab), n.value)
 print(f"{args.config}: {n.value} launches, step span {t[:, 1].max():.1f} us")
 tot = {}
@@ -81,6 +81,8 @@ if args.stamp >= 0:
           "reduced", "epi_chunk", "qkv_bar1", "qkv_bar2", "qkv_loads"]
     if lab[args.stamp] == "chain":  # per phase (O, gate_up, down, next QKV)
         nm = [f"{ph}:{ev}" for ph in ("o", "gate_up", "down", "qkv") for ev in ("x_ready", "first_mma", "last_mma", "epi_done")]
+        if os.environ.get("SEG_STAMPS"):  # -DSUN_W4_SEG_STAMPS build: O-phase segment epilogue split in slots 12..15
+            nm[12:16] = ["o:seg_start", "o:parked", "o:peers_in", "o:reduced+epi"]
     for i, name in enumerate(nm):
         if name == "-" or (sv[:, i] == 0).all():
             continue

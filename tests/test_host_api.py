@@ -158,7 +158,7 @@ def test_step_bytes_model():
 def test_step_flags_and_chain_selection():
     """Decode batches (distinct rows) set SUN_STEP_DISTINCT_ROWS and take the bf16 layer
     chain; token-parallel prefill rows do neither; the env switch forces either way and
-    never applies to QSUN (mirrors sun_capi.cu use_chain)."""
+    (QSUN: up to 128 rows; mirrors sun_capi.cu use_chain)."""
     from paper_2603_02599_b200 import _lib
     from paper_2603_02599_b200.modules import PrefillModule, SharedDecodeModule, uses_gemm_chain
 
@@ -168,4 +168,7 @@ def test_step_flags_and_chain_selection():
     assert SharedDecodeModule.distinct_rows and not PrefillModule.distinct_rows
     assert uses_gemm_chain(16, True, None) and not uses_gemm_chain(16, False, None)
     assert uses_gemm_chain(16, False, "1") and not uses_gemm_chain(16, True, "0")
-    assert not uses_gemm_chain(16, True, "x") and not uses_gemm_chain(4, True, "1") and not uses_gemm_chain(4, True, None)
+    assert not uses_gemm_chain(16, True, "x") and not uses_gemm_chain(4, True, "0")
+    # QSUN: the W4 layer chain up to 128 rows, separate launches above
+    assert uses_gemm_chain(4, True, None, batch=128) and not uses_gemm_chain(4, True, None, batch=129)
+    assert uses_gemm_chain(4, False, "1", batch=1) and not uses_gemm_chain(4, True, "1", batch=256)

@@ -58,7 +58,7 @@ def test_gemm_deterministic_stream_k(cuda):
         assert torch.equal(a, kernels.gemm_bf16(w, x, 64))
 
 
-@pytest.mark.parametrize("sched", ["0", "2", "vcl2", "novcl", "push", "nochain"])
+@pytest.mark.parametrize("sched", ["0", "2", "vcl2", "novcl", "push", "nochain", "l2chain"])
 def test_gemm_schedules_subprocess(sched):
     """The GEMM kernel tests and the end-to-end decode parity under the other
     schedules: 0 = cluster split-K / whole tiles only, 2 = stream-K on every
@@ -66,7 +66,9 @@ def test_gemm_schedules_subprocess(sched):
     vcl2 = L2-reduced virtual clusters wherever a split pays, novcl = hardware
     clusters only, push = hardware-cluster partials pushed to their owners by DSMEM bulk
     copies (instead of pulled after a cluster barrier), nochain = separate GEMM launches
-    instead of the persistent per-layer GEMM chain kernel (the bf16 decode default)."""
+    instead of the persistent per-layer GEMM chain kernels (the decode default, bf16 and
+    QSUN), l2chain = the chains over plain CTAs with every split phase reduced through L2
+    (instead of 4-CTA clusters reducing over DSMEM)."""
     import os
     import subprocess
     import sys
@@ -81,6 +83,8 @@ def test_gemm_schedules_subprocess(sched):
         env["SUN_GEMM_PUSH"] = "1"
     elif sched == "nochain":
         env["SUN_GEMM_CHAIN"] = "0"
+    elif sched == "l2chain":
+        env["SUN_CHAIN_CLUSTER"] = "0"
     else:
         env["SUN_GEMM_SCHED"] = sched
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", "(gemm or tiny) and not subprocess",
