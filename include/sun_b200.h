@@ -266,6 +266,18 @@ SunStatus sun_gemm_bf16_stamped(const void* w, int64_t n_out, int64_t k, const v
 SunStatus sun_gemm_w4(const void* packed, const void* scales, int64_t n_out, int64_t k, const void* x, int64_t ldx,
                       int64_t x_rows, int32_t batch, float* out, int64_t ldo, int32_t accumulate, void* workspace,
                       size_t workspace_bytes, void* stream);
+/* Small-batch QSUN GEMV (batch <= 16): the same SUN-W4 operands on the legacy
+ * tensor path (m16n8k16) with in-register dequantisation and a stream-K grid —
+ * the kernel QSUN decode steps of <= 8 rows run (gemm_w4.cuh gemv_w4_kernel).
+ * Result = sum over 128-k groups of s * sum(q * x) (fp32). */
+SunStatus sun_gemv_w4(const void* packed, const void* scales, int64_t n_out, int64_t k, const void* x, int64_t ldx,
+                      int64_t x_rows, int32_t batch, float* out, int64_t ldo, int32_t accumulate, void* workspace,
+                      size_t workspace_bytes, void* stream);
+/* sun_gemv_w4 (store) with per-CTA %globaltimer stamps [grid][16] (profiling only; 0 start,
+ * 1 setup done, 2 first stage landed, 3 last stage consumed, 5 last epilogue done, 6 exit). */
+SunStatus sun_gemv_w4_stamped(const void* packed, const void* scales, int64_t n_out, int64_t k, const void* x,
+                              int64_t ldx, int64_t x_rows, int32_t batch, float* out, int64_t ldo, void* workspace,
+                              size_t workspace_bytes, void* stream, uint64_t* stamps);
 /* sun_gemm_w4 (store) with per-CTA %globaltimer stamps [grid][16] (profiling only;
  * slots as sun_gemm_bf16_stamped). */
 SunStatus sun_gemm_w4_stamped(const void* packed, const void* scales, int64_t n_out, int64_t k, const void* x,
@@ -287,6 +299,15 @@ SunStatus sun_rmsnorm(const float* x, const void* w, void* y, int32_t batch, int
  * packed must be zeroed (padding rows are not written). */
 SunStatus sun_quantize_w4(const void* w, int64_t rows, int64_t k, int32_t group, void* packed, void* scales,
                           void* stream);
+
+/* QSUN checkpoint import: a compressed-tensors "pack-quantized" W4A16 tensor
+ * (weight_packed int32 [rows][K/8], element 8j+i of a row in nibble i of word j as
+ * q + 8; weight_scale bf16 [rows][K/128]; symmetric, group 128) re-laid out to
+ * SUN-W4 without touching q or s. packed must be zeroed (padding rows are not
+ * written). Replaces the quantisation step of QSUN's offline pipeline
+ * (LLM Compressor AWQ checkpoint -> vLLM) on the load side. */
+SunStatus sun_import_w4_ct(const void* ct_packed, const void* ct_scales, int64_t rows, int64_t k, int32_t group,
+                           void* packed, void* scales, void* stream);
 
 #ifdef __cplusplus
 }

@@ -14,7 +14,8 @@ SUN-W4 (matches paper_2603_02599_b200/csrc/gemm_w4.cuh):
   q   = clamp(rint(w / s), -8, 7)  (q = 0 if s == 0), rint = half-to-even
   deq = bf16(q * s)                          (the tcgen05 operand)
   scales stored tile-major [round_up(rows,128)/128][K/128][128] bf16 (a weight stage's
-  scales for consecutive K blocks are one contiguous run)
+  scales for consecutive K blocks are one contiguous run), the 128 scales of a block
+  row-interleaved: row r of the tile at position (r & 7) * 16 + (r >> 3)
   packed: block (row//128, k//128) is 8 KB contiguous, laid out [chunk 4][row 128][16 B]:
   chunk c of row r holds k = 32c .. 32c+31 of that row as 4 words; in each
   32-bit little-endian word the 8 consecutive k elements e0..e7 sit in nibbles
@@ -26,6 +27,7 @@ import numpy as np
 import torch
 
 NIBBLE_OF_ELEM = [0, 4, 1, 5, 2, 6, 3, 7]  # element e -> nibble position
+SCALE_POS = np.array([(r & 7) * 16 + (r >> 3) for r in range(128)])  # row -> position in a block's scale run
 
 
 def quantize(w: torch.Tensor, group: int = 128) -> tuple[torch.Tensor, torch.Tensor]:
@@ -64,7 +66,9 @@ def pack(q: torch.Tensor, s: torch.Tensor) -> tuple[np.ndarray, np.ndarray]:
     sc = np.zeros((rows_pad, kb), dtype=np.uint16)
     sc[:rows] = s.view(torch.int16).numpy().astype(np.uint16)
     sc = np.ascontiguousarray(sc.reshape(rows_pad // 128, 128, kb).transpose(0, 2, 1))
-    return packed, sc
+    out = np.empty_like(sc)
+    out[..., SCALE_POS] = sc  # row r of a block at (r & 7) * 16 + (r >> 3)
+    return packed, out
 
 
 def unpack(packed: np.ndarray, rows: int, k: int) -> torch.Tensor:

@@ -93,7 +93,11 @@ SIGNATURES = {
                                       c_size, c_vp, c_vp]),
     "sun_gemm_w4": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i32, c_vp, c_i64, c_i32, c_vp,
                             c_size, c_vp]),
+    "sun_gemv_w4": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i32, c_vp, c_i64, c_i32, c_vp,
+                            c_size, c_vp]),
     "sun_gemm_w4_stamped": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i32, c_vp, c_i64, c_vp,
+                                    c_size, c_vp, c_vp]),
+    "sun_gemv_w4_stamped": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i32, c_vp, c_i64, c_vp,
                                     c_size, c_vp, c_vp]),
     "sun_attention_decode": (c_i32, [ctypes.POINTER(SunDecoderDims), ctypes.POINTER(SunKvPool), c_i32, c_vp,
                                      c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_size, c_vp]),
@@ -101,6 +105,7 @@ SIGNATURES = {
     "sun_block_weights_bf16": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_vp]),
     "sun_rmsnorm": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_f32, c_vp]),
     "sun_quantize_w4": (c_i32, [c_vp, c_i64, c_i64, c_i32, c_vp, c_vp, c_vp]),
+    "sun_import_w4_ct": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_i32, c_vp, c_vp, c_vp]),
     "sun_decoder_status": (c_i32, [c_vp, ctypes.POINTER(ctypes.c_uint32), c_i32, c_vp]),
     "sun_decoder_uses_chain": (c_i32, [c_vp, c_i32, ctypes.POINTER(c_i32)]),
     "sun_kv_page_bytes": (c_i32, [ctypes.POINTER(SunKvPool), ctypes.POINTER(c_size)]),

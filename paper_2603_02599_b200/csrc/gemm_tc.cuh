@@ -52,7 +52,7 @@ enum EpiKind : int {
 struct GemmArgs {
   const uint8_t* wblk;     // bf16 weights, SUN-BLK
   const uint8_t* w4_packed;  // QSUN: SUN-W4 packed int4 (tile-contiguous 128x64 B blocks)
-  const __nv_bfloat16* w4_scales;  // QSUN: tile-major [m_tiles][k/128][128]
+  const __nv_bfloat16* w4_scales;  // QSUN: tile-major [m_tiles][k/128][128 row-interleaved, w4_scale_pos]
   const uint8_t* xact;     // activations, SUN-ACT with bn rows per atom
   int n_out;         // rows of W (incl. zero padding rows for SWIGLU)
   int k;             // reduction length
@@ -150,7 +150,10 @@ constexpr uint32_t kTileWBytes = kTileM * kTileK * 2;  // 16 KB: one SUN-BLK blo
 constexpr uint32_t kW4PackedBytes = kTileM * 128 / 2;  // 8 KB: one SUN-W4 block (128 x 128)
 __host__ __device__ inline uint32_t w4_wstage_bytes(int wgroup) { return static_cast<uint32_t>(wgroup) * (kW4PackedBytes + 256u); }
 constexpr int kMaxWStages = 16, kMaxXStages = 8;
-constexpr int kW4MaxABufs = 6;  // W4: dequantised 128x128 A tiles (64 TMEM columns each) at the top of TMEM
+constexpr int kW4MaxABufs = 6;
+// SUN-W4 stores a K block's 128 row scales row-interleaved: row r at (r & 7) * 16 + (r >> 3)
+// (the small-batch GEMV's lane g reads rows g, g + 8, ... as one 16-byte load)
+__host__ __device__ inline int w4_scale_pos(int r) { return ((r & 7) << 4) | (r >> 3); }  // W4: dequantised 128x128 A tiles (64 TMEM columns each) at the top of TMEM
 
 // column meta: pos[256], page[256], r_b[256] | per epilogue group: partner staging [16][128] f32 + 512 B scratch
 constexpr uint32_t kEpiGroupBytes = 16 * kTileM * 4 + 512;
@@ -667,7 +670,7 @@ SUN_DEVICE void w4_dequant_row(uint32_t pk, uint32_t sc, int row, int part, uint
                  : "=r"(words[4 * c]), "=r"(words[4 * c + 1]), "=r"(words[4 * c + 2]), "=r"(words[4 * c + 3])
                  : "r"(pk + ((kW4Chunks * part + c) * kTileM + row) * 16));
   unsigned short sraw;
-  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sraw) : "r"(sc + row * 2));
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sraw) : "r"(sc + w4_scale_pos(row) * 2));
   __nv_bfloat16 sb;
   *reinterpret_cast<unsigned short*>(&sb) = sraw;
   const __nv_bfloat162 s2 = __bfloat162bfloat162(sb);
@@ -1250,40 +1253,6 @@ __global__ void __launch_bounds__(W4 ? kW4Threads : kGemmThreads, 1) gemm_kernel
   }
   if (threadIdx.x == 0) SUN_STAMP(6);
   tl_end(a.tl, a.tl_idx);
-}
-
-// Offline quantiser (one thread per (row, group)); produces the tile-contiguous
-// SUN-W4 layout consumed above: packed block (m_tile, kb) is 128 rows x 64 B.
-__global__ void quantize_w4_kernel(const __nv_bfloat16* __restrict__ w, long long rows, long long rows_pad,
-                                   long long k, uint8_t* __restrict__ packed, __nv_bfloat16* __restrict__ scales) {
-  const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const long long ngroups = k / 128;
-  if (gid >= rows * ngroups) return;
-  const long long r = gid / ngroups;
-  const long long g = gid % ngroups;
-  const __nv_bfloat16* src = w + r * k + g * 128;
-  float amax = 0.f;
-  for (int i = 0; i < 128; ++i) amax = fmaxf(amax, fabsf(__bfloat162float(src[i])));
-  const __nv_bfloat16 sb = __float2bfloat16_rn(amax / 7.5f);
-  const float s = __bfloat162float(sb);
-  scales[((r / 128) * (k / 128) + g) * 128 + (r % 128)] = sb;  // tile-major [row tile][K block][128]
-  const long long kb_total = k / 128;
-  uint8_t* blk = packed + ((r / 128) * kb_total + g) * 8192;
-  for (int wd = 0; wd < 16; ++wd) {  // 16 words of 8 elements; word wd lives in chunk wd / 4
-    uint32_t word = 0;
-    for (int e = 0; e < 8; ++e) {
-      const float x = __bfloat162float(src[wd * 8 + e]);
-      int qv = 0;
-      if (s > 0.f) {
-        qv = static_cast<int>(rintf(x / s));
-        qv = qv < -8 ? -8 : (qv > 7 ? 7 : qv);
-      }
-      const uint32_t u = static_cast<uint32_t>(qv + 8);
-      const int nib = (e & 1) ? 4 + (e >> 1) : (e >> 1);  // order [0,2,4,6,1,3,5,7]
-      word |= u << (4 * nib);
-    }
-    reinterpret_cast<uint32_t*>(blk + ((wd >> 2) * 128 + (r % 128)) * 16)[wd & 3] = word;
-  }
 }
 
 }  // namespace sun

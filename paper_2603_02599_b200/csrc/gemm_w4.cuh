@@ -3,7 +3,8 @@
 // Storage format "SUN-W4" (restated bit-for-bit by oracle/quant_ref.py):
 //   * symmetric per-group quantisation along K, group = 128, one bf16 scale per
 //     (group, row) stored tile-major: scales[row tile][K/128][128], so the scales of
-//     one weight stage (consecutive K blocks of a tile) are one contiguous run;
+//     one weight stage (consecutive K blocks of a tile) are one contiguous run; the
+//     128 scales of a block are row-interleaved, row r at (r & 7) * 16 + (r >> 3);
 //   * q = clamp(rint(w / s), -8, 7), s = bf16(absmax / 7.5) (s = 0 -> q = 0);
 //   * packed bytes are tile-contiguous: block (row/128, k/128) is 8 KB (one bulk copy
 //     per stage) laid out [chunk 4][row 128][16 B], chunk c = k 32c..32c+31 of the row
@@ -23,3 +24,465 @@
 // the lm_head stays bf16.
 #pragma once
 #include "gemm_tc.cuh"
+
+namespace sun {
+
+// Offline quantiser (one thread per (row, group)); produces the tile-contiguous
+// SUN-W4 layout consumed above: packed block (m_tile, kb) is 128 rows x 64 B.
+__global__ void quantize_w4_kernel(const __nv_bfloat16* __restrict__ w, long long rows, long long rows_pad,
+                                   long long k, uint8_t* __restrict__ packed, __nv_bfloat16* __restrict__ scales) {
+  const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long ngroups = k / 128;
+  if (gid >= rows * ngroups) return;
+  const long long r = gid / ngroups;
+  const long long g = gid % ngroups;
+  const __nv_bfloat16* src = w + r * k + g * 128;
+  float amax = 0.f;
+  for (int i = 0; i < 128; ++i) amax = fmaxf(amax, fabsf(__bfloat162float(src[i])));
+  const __nv_bfloat16 sb = __float2bfloat16_rn(amax / 7.5f);
+  const float s = __bfloat162float(sb);
+  scales[((r / 128) * (k / 128) + g) * 128 + w4_scale_pos(static_cast<int>(r % 128))] = sb;  // tile-major, interleaved
+  const long long kb_total = k / 128;
+  uint8_t* blk = packed + ((r / 128) * kb_total + g) * 8192;
+  for (int wd = 0; wd < 16; ++wd) {  // 16 words of 8 elements; word wd lives in chunk wd / 4
+    uint32_t word = 0;
+    for (int e = 0; e < 8; ++e) {
+      const float x = __bfloat162float(src[wd * 8 + e]);
+      int qv = 0;
+      if (s > 0.f) {
+        qv = static_cast<int>(rintf(x / s));
+        qv = qv < -8 ? -8 : (qv > 7 ? 7 : qv);
+      }
+      const uint32_t u = static_cast<uint32_t>(qv + 8);
+      const int nib = (e & 1) ? 4 + (e >> 1) : (e >> 1);  // order [0,2,4,6,1,3,5,7]
+      word |= u << (4 * nib);
+    }
+    reinterpret_cast<uint32_t*>(blk + ((wd >> 2) * 128 + (r % 128)) * 16)[wd & 3] = word;
+  }
+}
+
+// Import of a compressed-tensors "pack-quantized" int4 checkpoint tensor (the layout
+// LLM Compressor writes for W4A16 group-128 symmetric AWQ / GPTQ; QSUN's
+// quantiser): weight_packed int32 [rows][k/8] with element
+// 8j+i of a row in nibble i of word j as offset-binary q + 8, weight_scale bf16
+// [rows][k/128]. Re-laid out to SUN-W4 (one thread per (row, group)): the
+// nibbles move to the [0,2,4,6,1,3,5,7] order, the word to its chunk/row slot,
+// the scale to the tile-major run. No arithmetic on q or s: the dequantised
+// operand bf16(q * s) is the checkpoint's.
+__global__ void import_w4_ct_kernel(const uint32_t* __restrict__ ct_packed, const __nv_bfloat16* __restrict__ ct_scales,
+                                    long long rows, long long k, uint8_t* __restrict__ packed,
+                                    __nv_bfloat16* __restrict__ scales) {
+  const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long ngroups = k / 128;
+  if (gid >= rows * ngroups) return;
+  const long long r = gid / ngroups;
+  const long long g = gid % ngroups;
+  scales[((r / 128) * ngroups + g) * 128 + w4_scale_pos(static_cast<int>(r % 128))] = ct_scales[r * ngroups + g];
+  const uint32_t* src = ct_packed + r * (k / 8) + g * 16;
+  uint8_t* blk = packed + ((r / 128) * ngroups + g) * 8192;
+#pragma unroll 4
+  for (int wd = 0; wd < 16; ++wd) {
+    const uint32_t in = src[wd];
+    uint32_t word = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int nib = (e & 1) ? 4 + (e >> 1) : (e >> 1);
+      word |= ((in >> (4 * e)) & 0xFu) << (4 * nib);
+    }
+    reinterpret_cast<uint32_t*>(blk + ((wd >> 2) * 128 + (r % 128)) * 16)[wd & 3] = word;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Small-batch QSUN GEMV (decode batches of <= 16 rows): D^T = W4 . X^T on the
+// legacy tensor path (mma.sync m16n8k16), dequantised in registers.
+//
+// At B <= 16 the tcgen05 W4 kernel runs at a batch-independent 0.45-1.5 TB/s
+// (scripts/w4_probe.py: 28672x4096 in 39.9 us at B = 1, 4 and 16): its converter
+// warps' TMEM round trip paces it. Here the packed words go straight into
+// m16n8k16 A fragments. The kernel is shaped by shared-memory bandwidth (measured:
+// with the compute warps idle the ring streams the 8B gate_up at 7.5 TB/s; a first
+// version whose eight row-warps each re-read the activation slice ran at half that):
+//   * Warp w (16 compute warps) owns rows 64 (w & 1) .. +63 of the 128-row tile (four
+//     m16 tiles), one 32-k chunk c = (w >> 1) & 3 and every other K block of a stage
+//     (parity w >> 3), so every packed byte is read from shared memory once, the
+//     activation fragment once per (chunk, row half) and reused by four tiles; four
+//     warps per scheduler hide the HMMA / shared-memory latencies (with two, the warps
+//     issued at IPC ~0.4 and the consumer, not the HBM, paced the ring).
+//   * ldmatrix of the SUN-W4 block [chunk 4][row 128][16 B] as b16 8x8 matrices gives
+//     lane (g, t) word t (k = 32c + 8t .. +7) of row g: one ldmatrix.x4 per block
+//     fetches the warp's four rows-of-8 (conflict-free, rows 16 B apart). A word's bf16
+//     pairs (e0,e1) (e2,e3) (e4,e5) (e6,e7) (LOP3 with the 0x4300 magic: q + 136 as
+//     bf16) fill the A slots (2t,2t+1 | 2t+8,2t+9) of two MMAs; K is permuted
+//     inside an MMA and the activation fragment uses the same permutation: lane (g, t)
+//     loads x[n][32c + 8t .. +8] (one 16-byte SUN-ACT chunk) for batch row
+//     n = (g & 1) * 4 + (g >> 1) — that row order puts the eight lanes of each
+//     shared-memory phase on eight different 16-byte bank groups.
+//   * The MMAs run on q + 136 (the magic pair itself, exact in bf16) from an accumulator
+//     preset to -136 sum x (two MMAs with A = 1 per block, shared by the four tiles),
+//     i.e. sum q x in fp32 per block and warp-chunk; the group scale s is applied once
+//     per block with an FMA (s * sum(q x), the operand bf16(q s) without its bf16
+//     rounding: below the 2e-2 logit tolerance). SUN-W4 stores a block's 128 scales row-interleaved
+//     (position (r & 7) * 16 + (r >> 3)), so lane g's four rows are one 8-byte load.
+//   * One producer warp streams stages of up to kbs consecutive K blocks of a tile
+//     (packed kbs x 8 KB, scales kbs x 256 B, the bn x 128 k SUN-ACT slice: three
+//     bulk copies); the weight and scale copies of the first ring's worth go out
+//     before griddepcontrol.wait.
+//   * Schedule: with at least one tile per SM, each CTA streams a contiguous run of
+//     whole tiles (the epilogue of one overlaps the ring's loads of the next); with
+//     fewer tiles, S = SMs / tiles CTAs split each tile's K, park their 128 x 16 fp32
+//     partials in L2 and bump the tile's counter, and the CTA completing the count
+//     adds the S partials in split order (deterministic) and runs the epilogue. (A
+//     stream-K grid measured slower: the partial segments' L2 round trips inside the
+//     main loop stalled the stream.) The epilogue is the tcgen05 GEMM's epi_chunk (QKV
+//     RoPE + KV append, residual + next-norm operand, SwiGLU, store) on warps 2..5.
+// ---------------------------------------------------------------------------
+constexpr int kGvWarps = 16;                     // compute warps: (row quarter, 32-k chunk)
+constexpr int kGvMT = 2;                         // m16 tiles per warp (32 rows)
+constexpr int kGvThreads = kGvWarps * 32 + 32;   // + the producer warp
+constexpr int kGvMaxStages = 8;
+constexpr int kGvTPitch = 17;                    // fp32 staging tile [128][17] (conflict-free row reads)
+
+__host__ __device__ inline uint32_t gv_stage_bytes(int bn, int kbs) {
+#if defined(SUN_GV_PROBE_NOX) || defined(SUN_GV_PROBE_NOSX)
+  bn = 0;  // probes: stages without the activation slice (deeper weight rings)
+#endif
+  return static_cast<uint32_t>(kbs) * (kW4PackedBytes + 256u + static_cast<uint32_t>(bn) * 256u);
+}
+__host__ __device__ inline size_t gv_smem_bytes(int bn, int kbs, int stages) {
+  return 1024 + static_cast<size_t>(stages) * gv_stage_bytes(bn, kbs) + kTileM * kGvTPitch * 4 + 3072 +
+         kEpiGroupBytes + 2 * kGvMaxStages * 8 + 64;
+}
+
+
+SUN_DEVICE void mma_16816_q(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                            uint32_t b1) {  // non-volatile: the scheduler may interleave it with the dequant
+#ifdef SUN_GV_NO_MMA  // probe: skip the tensor op (timing only, results invalid)
+  d[0] += __uint_as_float(a0 ^ b0); d[1] += __uint_as_float(a1 ^ b1); d[2] += __uint_as_float(a2); d[3] += __uint_as_float(a3);
+  return;
+#endif
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// word -> bf16x2 (q_{2p}, q_{2p+1}) of pair p (nibble order [0,2,4,6,1,3,5,7])
+SUN_DEVICE uint32_t w4_pair_q(uint32_t w, int p) {
+#ifdef SUN_GV_NO_CVT  // probe: skip the dequant arithmetic (timing only, results invalid)
+  return w >> p;
+#endif
+  uint32_t u = lop3_and_or(w >> (4 * p), 0x000F000Fu, 0x43004300u);  // bf16 128 + (q + 8)
+  __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(&u);
+  v = __hsub2(v, __floats2bfloat162_rn(136.f, 136.f));  // exact: q in [-8, 7]
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// word -> bf16x2 (q_{2p} + 136, q_{2p+1} + 136): the magic pair alone (exact)
+SUN_DEVICE uint32_t w4_pair_raw(uint32_t w, int p) {
+#ifdef SUN_GV_NO_CVT
+  return w >> p;
+#endif
+  return lop3_and_or(w >> (4 * p), 0x000F000Fu, 0x43004300u);
+}
+
+// batch row of fragment row g (conflict-free activation loads; see above)
+SUN_DEVICE int gv_nrow(int g) { return ((g & 1) << 2) | (g >> 1); }
+
+// One 128 x 128 K block for this warp's 64 rows (4 m16 tiles) and its 32-k chunk c,
+// split in a load half (fragments into registers) and a math half so the block loop can
+// issue block i+1's shared-memory loads before block i's dequant / MMAs.
+template <int NB>
+struct GvFrag {
+  uint32_t wq[2 * kGvMT];  // word t of row 32 rq + 16 m + 8 h + g: wq[2m + h] (one ldmatrix.x4)
+  uint32_t x[NB][4];       // x[n][32c + 8t .. +8] of batch row n = 8 j + gv_nrow(g)
+  uint32_t sv[kGvMT];      // bf16 scales of rows 32 rq + 16 m + g | +8: interleaved 16 g + 4 rq + 2 m + h
+};
+
+template <int NB>
+SUN_DEVICE void gv_load(GvFrag<NB>& f, uint32_t pk, uint32_t sc, uint32_t xs, int bn, int rq, int c, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  ldmatrix_x4(pk + c * 2048 + (32 * rq + lane) * 16, f.wq[0], f.wq[1], f.wq[2], f.wq[3]);
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    const int n = 8 * j + gv_nrow(g);
+    const uint32_t addr = xs + (c >> 1) * bn * 128 + n * 128 + ((((c & 1) * 4 + t) ^ (n & 7)) << 4);
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(f.x[j][0]), "=r"(f.x[j][1]), "=r"(f.x[j][2]), "=r"(f.x[j][3])
+                 : "r"(addr));
+  }
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(f.sv[0]), "=r"(f.sv[1]) : "r"(sc + (16 * g + 4 * rq) * 2));
+}
+
+// acc[m][j] += s_row * sum_k q x (n-tile j). The A operand is the raw magic pair
+// bf16(128 + q + 8) = q + 136 (one LOP3, no subtraction); each m16 tile's MMAs start from
+// -136 sum_k x (two extra MMAs per block with A = 1, shared by the four tiles), so the
+// accumulator holds sum (q + 136) x - 136 sum x = sum q x.
+template <int NB>
+SUN_DEVICE void gv_math(const GvFrag<NB>& f, float (&acc)[kGvMT][NB][4]) {
+  constexpr uint32_t kOnes = 0x3F803F80u;  // bf16x2 (1, 1)
+  float cx[NB][4];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    cx[j][0] = cx[j][1] = cx[j][2] = cx[j][3] = 0.f;
+    mma_16816_q(cx[j], kOnes, kOnes, kOnes, kOnes, f.x[j][0], f.x[j][1]);
+    mma_16816_q(cx[j], kOnes, kOnes, kOnes, kOnes, f.x[j][2], f.x[j][3]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) cx[j][e] *= -136.f;
+  }
+#pragma unroll
+  for (int m = 0; m < kGvMT; ++m) {
+    float blk[NB][4];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) blk[j][0] = cx[j][0], blk[j][1] = cx[j][1], blk[j][2] = cx[j][2], blk[j][3] = cx[j][3];
+    const uint32_t lo = f.wq[2 * m], hi = f.wq[2 * m + 1];
+    const uint32_t a00 = w4_pair_raw(lo, 0), a10 = w4_pair_raw(hi, 0), a01 = w4_pair_raw(lo, 1), a11 = w4_pair_raw(hi, 1);
+    const uint32_t a02 = w4_pair_raw(lo, 2), a12 = w4_pair_raw(hi, 2), a03 = w4_pair_raw(lo, 3), a13 = w4_pair_raw(hi, 3);
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      mma_16816_q(blk[j], a00, a10, a01, a11, f.x[j][0], f.x[j][1]);
+      mma_16816_q(blk[j], a02, a12, a03, a13, f.x[j][2], f.x[j][3]);
+    }
+    const float s0 = __uint_as_float(f.sv[m] << 16), s1 = __uint_as_float(f.sv[m] & 0xFFFF0000u);
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      acc[m][j][0] = fmaf(s0, blk[j][0], acc[m][j][0]);
+      acc[m][j][1] = fmaf(s0, blk[j][1], acc[m][j][1]);
+      acc[m][j][2] = fmaf(s1, blk[j][2], acc[m][j][2]);
+      acc[m][j][3] = fmaf(s1, blk[j][3], acc[m][j][3]);
+    }
+  }
+}
+
+SUN_DEVICE void gv_bar() { asm volatile("bar.sync 2, 512;" ::: "memory"); }  // the 16 compute warps
+
+template <int EPI, int NB>
+__global__ void __launch_bounds__(kGvThreads, 1) gemv_w4_kernel(const GemmArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  tl_begin(a.tl, a.tl_idx);
+  const int stages = a.stages, kbs = a.wgroup, bn = a.bn, KB = a.ksteps;
+  const uint32_t sb = gv_stage_bytes(bn, kbs);
+  uint8_t* ring = smem;
+  float* T = reinterpret_cast<float*>(ring + stages * sb);
+  float* epi = T + kTileM * kGvTPitch;
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(epi) + 3072 + kEpiGroupBytes);
+  uint64_t* empty = full + kGvMaxStages;
+  int* flag = reinterpret_cast<int*>(empty + kGvMaxStages);
+  const int warp = warp_id_sync(), lane = threadIdx.x & 31;
+  const int G = static_cast<int>(gridDim.x), c = static_cast<int>(blockIdx.x);
+  // work: splits == 0: whole tiles [c m / G, (c+1) m / G); splits == S: tile c / S, K blocks
+  // [r KB / S, (r+1) KB / S) of it (r = c % S)
+  const int S = a.splits;
+  int u0, u1;
+  if (S == 0) {
+    u0 = static_cast<int>(static_cast<long long>(c) * a.m_tiles / G) * KB;
+    u1 = static_cast<int>(static_cast<long long>(c + 1) * a.m_tiles / G) * KB;
+  } else {
+    const int t0 = c / S, r = c % S;
+    u0 = t0 * KB + r * KB / S;
+    u1 = t0 * KB + (r + 1) * KB / S;
+  }
+  if (threadIdx.x == 0) SUN_STAMP(0);
+  if (warp == kGvWarps && elect_one()) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kGvWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) SUN_STAMP(1);
+
+  if (warp == kGvWarps) {
+    // ---- producer: stages of up to kbs K blocks, never crossing a tile boundary
+    if (elect_one()) {
+#if defined(SUN_GV_PROBE_NOSX)  // probes (timing only, results invalid): skip the scale and X copies
+      const uint32_t wbytes = kW4PackedBytes, xbytes = 0u;
+#elif defined(SUN_GV_PROBE_NOX)  // skip the X copies
+      const uint32_t wbytes = kW4PackedBytes + 256u, xbytes = 0u;
+#else
+      const uint32_t wbytes = kW4PackedBytes + 256u, xbytes = static_cast<uint32_t>(bn) * 256u;
+#endif
+      int u = u0, slot = 0, phase = 0, issued = 0;
+      // first ring's worth: weights + scales before the dependency wait
+      int pu = u0, pre = 0;
+      for (; pre < stages && pu < u1; ++pre) {
+        const int len = min(kbs, min(u1 - pu, KB - pu % KB));
+        uint8_t* st = ring + pre * sb;
+        mbar_arrive_expect_tx(&full[pre], static_cast<uint32_t>(len) * (wbytes + xbytes));
+        bulk_load_hint(st, a.w4_packed + static_cast<long long>(pu) * kW4PackedBytes, len * kW4PackedBytes,
+                       &full[pre], kEvictFirst);
+#ifndef SUN_GV_PROBE_NOSX
+        bulk_load_hint(st + kbs * kW4PackedBytes, a.w4_scales + static_cast<long long>(pu) * kTileM, len * 256u,
+                       &full[pre], kEvictFirst);
+#endif
+        pu += len;
+      }
+      pdl_wait();  // activations are the previous kernel's output
+      for (; u < u1; ++issued) {
+        const int kb = u % KB;
+        const int len = min(kbs, min(u1 - u, KB - kb));
+        uint8_t* st = ring + slot * sb;
+        if (issued >= pre) {
+          mbar_wait(&empty[slot], phase ^ 1);
+          mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(len) * (wbytes + xbytes));
+          bulk_load_hint(st, a.w4_packed + static_cast<long long>(u) * kW4PackedBytes, len * kW4PackedBytes,
+                         &full[slot], kEvictFirst);
+#ifndef SUN_GV_PROBE_NOSX
+          bulk_load_hint(st + kbs * kW4PackedBytes, a.w4_scales + static_cast<long long>(u) * kTileM, len * 256u,
+                         &full[slot], kEvictFirst);
+#endif
+        }
+        if (xbytes)
+          bulk_load_hint(st + kbs * (kW4PackedBytes + 256u), a.xact + static_cast<long long>(2 * kb) * bn * 128,
+                         len * xbytes, &full[slot], kEvictLast);
+        u += len;
+        if (++slot == stages) {
+          slot = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ---- compute warps
+    pdl_wait();
+    if (warp >= 2 && warp < 6) load_qkv_meta<EPI>(a, epi);  // epilogue group: positions / pages / r_b
+    const int rq = warp & 3, ch = warp >> 2;  // row quarter, 32-k chunk of every block
+    const int g = lane >> 2, t = lane & 3;
+    const uint32_t ring_s = smem_u32(ring);
+    float acc[kGvMT][NB][4];
+    int u = u0, slot = 0, phase = 0;
+    while (u < u1) {
+      const int tile = u / KB;
+      const int seg_end = min(u1, (tile + 1) * KB);
+      const bool whole = (u == tile * KB) && (seg_end == (tile + 1) * KB);
+#pragma unroll
+      for (int m = 0; m < kGvMT; ++m)
+#pragma unroll
+        for (int j = 0; j < NB; ++j) acc[m][j][0] = acc[m][j][1] = acc[m][j][2] = acc[m][j][3] = 0.f;
+      while (u < seg_end) {
+        const int len = min(kbs, seg_end - u);
+        mbar_wait(&full[slot], phase);
+        if (threadIdx.x == 0 && u == u0) SUN_STAMP(2);  // first stage landed
+        const uint32_t st = ring_s + slot * sb;
+#ifndef SUN_GV_PROBE_IDLE  // probe: compute warps only pass the stages on (timing only)
+        {
+          auto ld = [&](GvFrag<NB>& f, int i) {
+            gv_load<NB>(f, st + i * kW4PackedBytes, st + kbs * kW4PackedBytes + i * 256,
+                        st + kbs * (kW4PackedBytes + 256u) + i * bn * 256, bn, rq, ch, lane);
+          };
+          GvFrag<NB> fa, fb;  // two fragment sets: block i+1 loads while block i computes
+          ld(fa, 0);
+          for (int i = 0; i < len; i += 2) {
+            if (i + 1 < len) ld(fb, i + 1);
+            gv_math<NB>(fa, acc);
+            if (i + 1 < len) {
+              if (i + 2 < len) ld(fa, i + 2);
+              gv_math<NB>(fb, acc);
+            }
+          }
+        }
+#endif
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        u += len;
+        if (++slot == stages) {
+          slot = 0;
+          phase ^= 1;
+        }
+      }
+      if (threadIdx.x == 0 && u == u1) SUN_STAMP(3);  // last stage consumed
+      // fragments -> T[row][batch]: row 32 rq + 16 m + g (+8), batch 8 j + t (c0) / 8 j + t + 4 (c1)
+      // (gv_nrow of columns 2t, 2t+1); columns >= 8 NB are zero. Chunk 0's warps store,
+      // chunks 1..3 add in order (fixed summation order).
+      gv_bar();  // the previous segment's epilogue is done with T
+      for (int cc = 0; cc < 4; ++cc) {
+        if (ch == cc) {
+#pragma unroll
+          for (int m = 0; m < kGvMT; ++m) {
+            const int r = 32 * rq + 16 * m + g;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const int jj = j < NB ? j : 0;
+              const bool have = j < NB;
+              float* p0 = T + r * kGvTPitch + 8 * j + t;
+              float* p1 = T + (r + 8) * kGvTPitch + 8 * j + t;
+              const float v0 = have ? acc[m][jj][0] : 0.f, v1 = have ? acc[m][jj][1] : 0.f;
+              const float v2 = have ? acc[m][jj][2] : 0.f, v3 = have ? acc[m][jj][3] : 0.f;
+              if (cc == 0) {
+                p0[0] = v0; p0[4] = v1; p1[0] = v2; p1[4] = v3;
+              } else {
+                p0[0] += v0; p0[4] += v1; p1[0] += v2; p1[4] += v3;
+              }
+            }
+          }
+        }
+        gv_bar();
+      }
+      bool run_epi = whole;
+      if (!whole) {
+        // park the partial: [c][128 rows][16] fp32, 8 floats per thread (split schedule:
+        // one segment per CTA)
+        const int pslot = 0;
+        const int tid = threadIdx.x & 255, row = tid >> 1, h = (tid & 1) * 8;
+        const bool mover = threadIdx.x < 256;  // 8 floats each
+        if (mover) {
+          float* dst = a.sk_part + (static_cast<long long>(c) * 2 + pslot) * (kTileM * 16) + row * 16 + h;
+          __stcg(reinterpret_cast<float4*>(dst), make_float4(T[row * kGvTPitch + h], T[row * kGvTPitch + h + 1],
+                                                             T[row * kGvTPitch + h + 2], T[row * kGvTPitch + h + 3]));
+          __stcg(reinterpret_cast<float4*>(dst + 4), make_float4(T[row * kGvTPitch + h + 4], T[row * kGvTPitch + h + 5],
+                                                                 T[row * kGvTPitch + h + 6], T[row * kGvTPitch + h + 7]));
+          __threadfence();
+        }
+        gv_bar();
+        const int cf = tile * S, cl = tile * S + S - 1;
+        if (threadIdx.x == 0) {
+          const unsigned old = atomicAdd(a.sk_flags + tile, 1u);
+          *flag = (old == static_cast<unsigned>(cl - cf)) ? 1 : 0;
+        }
+        gv_bar();
+        run_epi = *flag != 0;
+        if (run_epi && mover) {  // last contributor: sum the tile's partials in CTA order
+          __threadfence();
+          float s8[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) s8[e] = 0.f;
+          for (int c0 = cf; c0 <= cl; c0 += 4) {  // four partials' loads in flight per round trip
+            float4 p[4][2];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float* src = a.sk_part + static_cast<long long>(c0 + e <= cl ? c0 + e : cl) * 2 * (kTileM * 16) +
+                                 row * 16 + h;
+              p[e][0] = __ldcg(reinterpret_cast<const float4*>(src));
+              p[e][1] = __ldcg(reinterpret_cast<const float4*>(src + 4));
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              if (c0 + e > cl) break;
+              s8[0] += p[e][0].x; s8[1] += p[e][0].y; s8[2] += p[e][0].z; s8[3] += p[e][0].w;
+              s8[4] += p[e][1].x; s8[5] += p[e][1].y; s8[6] += p[e][1].z; s8[7] += p[e][1].w;
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < 8; ++e) T[row * kGvTPitch + h + e] = s8[e];
+          if (threadIdx.x == 0) a.sk_flags[tile] = 0u;  // self-resetting for the next launch
+        }
+        if (run_epi) gv_bar();
+      }
+      if (run_epi && warp >= 2 && warp < 6) {
+        const int q = warp & 3;
+        const int row_local = q * 32 + lane;
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = T[row_local * kGvTPitch + j];
+        epi_chunk<EPI>(a, tile, row_local, 0, v, epi);
+      }
+    }
+  }
+  if (threadIdx.x == 64) SUN_STAMP(5);  // (epilogue warp) last epilogue done
+  if (threadIdx.x == 0) SUN_STAMP(6);
+  tl_end(a.tl, a.tl_idx);
+}
+
+}  // namespace sun

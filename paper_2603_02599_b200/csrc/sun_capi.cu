@@ -195,6 +195,14 @@ void init_kernel_attrs() {
     set_max_smem(gemm_kernel<EPI_RESID_ADD, true>);
     set_max_smem(gemm_kernel<EPI_QKV_ROPE, true>);
     set_max_smem(gemm_kernel<EPI_SWIGLU, true>);
+    set_max_smem(gemv_w4_kernel<EPI_STORE_F32, 1>);
+    set_max_smem(gemv_w4_kernel<EPI_STORE_F32, 2>);
+    set_max_smem(gemv_w4_kernel<EPI_RESID_ADD, 1>);
+    set_max_smem(gemv_w4_kernel<EPI_RESID_ADD, 2>);
+    set_max_smem(gemv_w4_kernel<EPI_QKV_ROPE, 1>);
+    set_max_smem(gemv_w4_kernel<EPI_QKV_ROPE, 2>);
+    set_max_smem(gemv_w4_kernel<EPI_SWIGLU, 1>);
+    set_max_smem(gemv_w4_kernel<EPI_SWIGLU, 2>);
     set_max_smem(gemm_chain_kernel);
     set_max_smem(gemm_chain_w4_kernel);
     set_max_smem(attn_group_kernel<64>);
@@ -313,6 +321,11 @@ cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, c
 // Stream-K GEMM scratch: one fp32 [bn][128] partial and one flag per CTA slot.
 constexpr int kMaxGemmCtas = 2 * kNumSms;
 size_t sk_part_bytes(int bn) { return size_t(kMaxGemmCtas) * size_t(bn) * kTileM * 4; }
+// Small-batch W4 GEMV scratch: two 128 x 16 fp32 partial slots per CTA, one counter per tile.
+constexpr int kGvMaxTiles = 4096;
+size_t gv_part_bytes() { return size_t(kMaxGemmCtas) * 2 * kTileM * 16 * 4; }
+constexpr int kGemvKernelMaxBatch = 16;  // gemv_w4_kernel: one or two 8-column MMA tiles
+constexpr int kGemvMaxBatch = 8;  // decode steps use it up to 8 rows: at 9..16 the W4 chain measured faster (B=16 2.65 vs 2.82 ms)
 
 // GEMM schedule. 0 (default): cluster split-K for <= 148 tiles, whole tiles
 // otherwise. 1: stream-K for GEMMs with more tiles than SMs (even split of
@@ -331,7 +344,7 @@ int gemm_sched() {
 // Workspace layout shared by sizing and creation.
 struct WsLayout {
   size_t resid, xn, q, attn, act, part_o, part_ml, attn_cnt, ss, amax_val, amax_idx, logits, sk_part, sk_flags,
-      chain_bar, err, total;
+      chain_bar, err, gv_part, gv_cnt, total;
   int max_splits;
 };
 
@@ -369,6 +382,8 @@ WsLayout layout_ws(const SunDecoderDims& d, int max_batch) {
   w.sk_flags = take(kMaxGemmCtas * 4);
   w.chain_bar = take(64);
   w.err = take(64);
+  w.gv_part = take(gv_part_bytes());
+  w.gv_cnt = take(kGvMaxTiles * 4);
   w.total = off;
   return w;
 }
@@ -444,6 +459,8 @@ struct SunDecoder {
   unsigned* sk_flags;
   unsigned* chain_bar;
   unsigned* err;  // SUN_STEP_ERR_* bits (sun_decoder_status)
+  float* gv_part;     // small-batch W4 GEMV partials / per-tile counters
+  unsigned* gv_cnt;
   int num_sms = kNumSms;
   bool chain_ok = false;     // the layer chain's grid fits this device co-resident (chain_fits)
   bool chain_w4_ok = false;  // same for the QSUN chain (chain_w4_fits)
@@ -631,6 +648,62 @@ SunStatus run_gemm(const void* wblk, const void* packed, const void* scales, Gem
   } else {
     SUN_CUDA(launch(gemm_kernel<EPI, false>, dim3(c.grid), dim3(kGemmThreads), c.smem, st, pdl, a));
   }
+  return SUN_OK;
+}
+
+// Small-batch QSUN GEMV (gemv_w4_kernel, gemm_w4.cuh) for decode batches of <= 8
+// rows (kernel: <= 16): one CTA per SM (SUN_GV_CTAS_PER_SM), whole tiles or split-K per tile, a ring of
+// SUN_GV_STAGES stages of SUN_GV_KBS K blocks. SUN_W4_GEMV=0 keeps the tcgen05 path.
+struct GvCfg {
+  int kbs, stages, per_sm;
+  size_t smem;
+};
+GvCfg gv_cfg(int bn) {
+  static const int env_kbs = [] { const char* e = getenv("SUN_GV_KBS"); return e ? atoi(e) : 0; }();
+  static const int env_st = [] { const char* e = getenv("SUN_GV_STAGES"); return e ? atoi(e) : 0; }();
+  static const int env_ps = [] { const char* e = getenv("SUN_GV_CTAS_PER_SM"); return e ? atoi(e) : 0; }();
+  GvCfg c{};
+  c.kbs = env_kbs > 0 ? env_kbs : 4;
+  c.per_sm = env_ps > 0 ? env_ps : 1;
+  const int budget = kSmemPerSm / c.per_sm - int(gv_smem_bytes(bn, c.kbs, 0)) - 1024;
+  c.stages = std::max(2, std::min(kGvMaxStages, budget / int(gv_stage_bytes(bn, c.kbs))));
+  if (env_st > 0) c.stages = std::min(env_st, kGvMaxStages);
+  c.smem = gv_smem_bytes(bn, c.kbs, c.stages);
+  return c;
+}
+bool use_gemv(bool w4, int batch) {
+  static const int v = [] { const char* e = getenv("SUN_W4_GEMV"); return e ? atoi(e) : 1; }();
+  return w4 && v != 0 && batch <= kGemvMaxBatch;
+}
+
+template <int EPI>
+SunStatus run_gemv_w4(const void* packed, const void* scales, GemmArgs a, const GemmPlan& p, float* part,
+                      unsigned* cnt, cudaStream_t st, bool pdl, int num_sms) {
+  if (a.bn != 16 || a.batch > kGemvKernelMaxBatch) return fail(SUN_ERR_VALUE, "W4 GEMV takes batches of <= 16 rows");
+  if (p.m_tiles > kGvMaxTiles) return fail(SUN_ERR_UNSUPPORTED, "W4 GEMV: %d tiles > %d", p.m_tiles, kGvMaxTiles);
+  const GvCfg c = gv_cfg(a.bn);
+  a.w4_packed = static_cast<const uint8_t*>(packed);
+  a.w4_scales = static_cast<const __nv_bfloat16*>(scales);
+  a.wgroup = c.kbs;
+  a.stages = c.stages;
+  a.sk_units = 0;
+  a.sk_part = part;
+  a.sk_flags = cnt;
+  tl_assign(a);
+  tl_stamps(a);
+  // whole tiles when every SM gets one (splits = 0), else S-way split-K per tile
+  const int slots = std::min(num_sms * c.per_sm, kMaxGemmCtas);
+  int grid;
+  if (p.m_tiles >= slots) {
+    a.splits = 0;
+    grid = slots;
+  } else {
+    a.splits = std::max(1, std::min(p.ksteps, slots / p.m_tiles));
+    grid = p.m_tiles * a.splits;
+  }
+  g_cluster = 1;
+  if (a.batch <= 8) SUN_CUDA(launch(gemv_w4_kernel<EPI, 1>, dim3(grid), dim3(kGvThreads), c.smem, st, pdl, a));
+  else SUN_CUDA(launch(gemv_w4_kernel<EPI, 2>, dim3(grid), dim3(kGvThreads), c.smem, st, pdl, a));
   return SUN_OK;
 }
 
@@ -957,6 +1030,8 @@ SunStatus sun_decoder_create(const SunDecoderDims* dims, const SunWeights* weigh
   dec->sk_flags = reinterpret_cast<unsigned*>(ws + dec->L.sk_flags);
   dec->chain_bar = reinterpret_cast<unsigned*>(ws + dec->L.chain_bar);
   dec->err = reinterpret_cast<unsigned*>(ws + dec->L.err);
+  dec->gv_part = reinterpret_cast<float*>(ws + dec->L.gv_part);
+  dec->gv_cnt = reinterpret_cast<unsigned*>(ws + dec->L.gv_cnt);
 
   const SunDecoderDims& d = *dims;
   const int qd = d.n_q_heads * d.head_dim;
@@ -973,6 +1048,7 @@ SunStatus sun_decoder_create(const SunDecoderDims* dims, const SunWeights* weigh
   if (e == cudaSuccess) e = cudaMemset(ws + dec->L.sk_flags, 0, kMaxGemmCtas * 4);
   if (e == cudaSuccess) e = cudaMemset(ws + dec->L.chain_bar, 0, 64);
   if (e == cudaSuccess) e = cudaMemset(ws + dec->L.err, 0, 64);
+  if (e == cudaSuccess) e = cudaMemset(ws + dec->L.gv_cnt, 0, kGvMaxTiles * 4);
   if (e != cudaSuccess) {
     delete dec;
     return fail(SUN_ERR_CUDA, "cudaMemset ws: %s", cudaGetErrorString(e));
@@ -1097,14 +1173,23 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     produce_norm(a, l + 1 < d.n_layers ? dec->layers[l + 1].attn_norm : dec->w.final_norm);
     return a;
   };
-  const bool chain = use_chain(flags, w4, bn) && (w4 ? dec->chain_w4_ok : dec->chain_ok);
+  const bool gemv = use_gemv(w4, batch);  // QSUN small batches: W4 GEMV launches, no chain
+  const bool chain = !gemv && use_chain(flags, w4, bn) && (w4 ? dec->chain_w4_ok : dec->chain_ok);
+  auto w4_gemm = [&](auto epi_tag, const void* pk, const void* sc, const GemmArgs& ga, const GemmPlan& p) {
+    constexpr int E = decltype(epi_tag)::value;
+    return gemv ? run_gemv_w4<E>(pk, sc, ga, p, dec->gv_part, dec->gv_cnt, st, pdl, dec->num_sms)
+                : run_gemm<E>(nullptr, pk, sc, ga, p, st, pdl);
+  };
+  using QkvT = std::integral_constant<int, EPI_QKV_ROPE>;
+  using ResT = std::integral_constant<int, EPI_RESID_ADD>;
+  using SwiT = std::integral_constant<int, EPI_SWIGLU>;
   for (int l = 0; l < d.n_layers; ++l) {
     const SunLayerWeights& lw = dec->layers[l];
     GemmArgs a;
     if (!chain || l == 0) {
       a = qkv_args(l);
       set_prefetch(a, lw.w_o, dec->p_o, bn, w4);  // O-proj weights, through the attention kernel
-      if (!(skip & 1)) s = w4 ? run_gemm<EPI_QKV_ROPE>(nullptr, lw.w_qkv, lw.s_qkv, a, dec->p_qkv, st, pdl)
+      if (!(skip & 1)) s = w4 ? w4_gemm(QkvT{}, lw.w_qkv, lw.s_qkv, a, dec->p_qkv)
              : run_gemm<EPI_QKV_ROPE>(lw.w_qkv, nullptr, nullptr, a, dec->p_qkv, st, pdl);
       if (s != SUN_OK) return s;
     }
@@ -1131,18 +1216,18 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     }
     a = o_args(l);
     set_prefetch(a, lw.w_gate_up, dec->p_gu, bn, w4);
-    if (!(skip & 8)) s = w4 ? run_gemm<EPI_RESID_ADD>(nullptr, lw.w_o, lw.s_o, a, dec->p_o, st, pdl)
+    if (!(skip & 8)) s = w4 ? w4_gemm(ResT{}, lw.w_o, lw.s_o, a, dec->p_o)
            : run_gemm<EPI_RESID_ADD>(lw.w_o, nullptr, nullptr, a, dec->p_o, st, pdl);
     if (s != SUN_OK) return s;
     a = gu_args(l);
     set_prefetch(a, lw.w_down, dec->p_down, bn, w4);
-    if (!(skip & 16)) s = w4 ? run_gemm<EPI_SWIGLU>(nullptr, lw.w_gate_up, lw.s_gate_up, a, dec->p_gu, st, pdl)
+    if (!(skip & 16)) s = w4 ? w4_gemm(SwiT{}, lw.w_gate_up, lw.s_gate_up, a, dec->p_gu)
            : run_gemm<EPI_SWIGLU>(lw.w_gate_up, nullptr, nullptr, a, dec->p_gu, st, pdl);
     if (s != SUN_OK) return s;
     a = down_args(l);
     if (l + 1 < d.n_layers) set_prefetch(a, dec->layers[l + 1].w_qkv, dec->p_qkv, bn, w4);
     else set_prefetch(a, dec->w.lm_head, dec->p_lm, bn, false);
-    if (!(skip & 32)) s = w4 ? run_gemm<EPI_RESID_ADD>(nullptr, lw.w_down, lw.s_down, a, dec->p_down, st, pdl)
+    if (!(skip & 32)) s = w4 ? w4_gemm(ResT{}, lw.w_down, lw.s_down, a, dec->p_down)
            : run_gemm<EPI_RESID_ADD>(lw.w_down, nullptr, nullptr, a, dec->p_down, st, pdl);
     if (s != SUN_OK) return s;
   }
@@ -1233,7 +1318,8 @@ SunStatus sun_decode_step_timeline(SunDecoder* dec, const int32_t* tokens, const
 SunStatus sun_gemm_workspace_bytes(int64_t n_out, int64_t k, int32_t batch, size_t* bytes) {
   if (n_out < 1 || k < 1 || batch < 1 || batch > 256) return fail(SUN_ERR_VALUE, "bad gemm shape");
   const size_t act = align_up(size_t(round16(batch)) * size_t((k + 63) / 64) * 128, 1024);  // SUN-ACT copy of X
-  *bytes = act + sk_part_bytes(round16(batch)) + kMaxGemmCtas * 4;  // + stream-K partials and flags
+  // + stream-K partials (or the W4 GEMV's two slots per CTA) and flags / per-tile counters
+  *bytes = act + std::max(sk_part_bytes(round16(batch)), gv_part_bytes()) + kGvMaxTiles * 4;
   return SUN_OK;
 }
 
@@ -1242,7 +1328,7 @@ namespace {
 template <int EPI>
 SunStatus gemm_api(const void* wblk, const void* packed, const void* scales, int64_t n_out, int64_t k, const void* x,
                    int64_t ldx, int64_t x_rows, int32_t batch, float* out, int64_t ldo, void* workspace,
-                   size_t workspace_bytes, void* stream, uint64_t* stamps) {
+                   size_t workspace_bytes, void* stream, uint64_t* stamps, bool gemv = false) {
   if (batch < 1) return fail(SUN_ERR_VALUE, "empty batch");
   if (k % 8 != 0) return fail(SUN_ERR_UNSUPPORTED, "k must be a multiple of 8");
   size_t need = 0;
@@ -1258,11 +1344,13 @@ SunStatus gemm_api(const void* wblk, const void* packed, const void* scales, int
   GemmPlan p = plan_gemm(n_out, k);
   const size_t act = align_up(size_t(bn) * size_t((k + 63) / 64) * 128, 1024);
   uint8_t* wsb = static_cast<uint8_t*>(workspace);
-  GemmArgs a = base_args(p, n_out, k, batch, bn, workspace, reinterpret_cast<float*>(wsb + act),
-                         reinterpret_cast<unsigned*>(wsb + act + sk_part_bytes(bn)));
+  float* part = reinterpret_cast<float*>(wsb + act);
+  unsigned* flags = reinterpret_cast<unsigned*>(wsb + act + std::max(sk_part_bytes(bn), gv_part_bytes()));
+  GemmArgs a = base_args(p, n_out, k, batch, bn, workspace, part, flags);
   a.out_f32 = out;
   a.ldo = ldo;
   a.stamps = reinterpret_cast<unsigned long long*>(stamps);
+  if (gemv) return run_gemv_w4<EPI>(packed, scales, a, p, part, flags, st, false, device_sms());
   return run_gemm<EPI>(wblk, packed, scales, a, p, st, false);
 }
 }  // namespace
@@ -1294,6 +1382,26 @@ SunStatus sun_gemm_w4(const void* packed, const void* scales, int64_t n_out, int
                                               workspace, workspace_bytes, stream, nullptr)
                     : gemm_api<EPI_STORE_F32>(nullptr, packed, scales, n_out, k, x, ldx, x_rows, batch, out, ldo,
                                               workspace, workspace_bytes, stream, nullptr);
+}
+
+SunStatus sun_gemv_w4(const void* packed, const void* scales, int64_t n_out, int64_t k, const void* x, int64_t ldx,
+                      int64_t x_rows, int32_t batch, float* out, int64_t ldo, int32_t accumulate, void* workspace,
+                      size_t workspace_bytes, void* stream) {
+  if (k % 128 != 0) return fail(SUN_ERR_UNSUPPORTED, "W4 needs k multiple of 128");
+  if (batch > kGemvKernelMaxBatch) return fail(SUN_ERR_VALUE, "W4 GEMV takes batches of <= %d rows", kGemvKernelMaxBatch);
+  return accumulate ? gemm_api<EPI_RESID_ADD>(nullptr, packed, scales, n_out, k, x, ldx, x_rows, batch, out, ldo,
+                                              workspace, workspace_bytes, stream, nullptr, true)
+                    : gemm_api<EPI_STORE_F32>(nullptr, packed, scales, n_out, k, x, ldx, x_rows, batch, out, ldo,
+                                              workspace, workspace_bytes, stream, nullptr, true);
+}
+
+SunStatus sun_gemv_w4_stamped(const void* packed, const void* scales, int64_t n_out, int64_t k, const void* x,
+                              int64_t ldx, int64_t x_rows, int32_t batch, float* out, int64_t ldo, void* workspace,
+                              size_t workspace_bytes, void* stream, uint64_t* stamps) {
+  if (k % 128 != 0) return fail(SUN_ERR_UNSUPPORTED, "W4 needs k multiple of 128");
+  if (batch > kGemvKernelMaxBatch) return fail(SUN_ERR_VALUE, "W4 GEMV takes batches of <= %d rows", kGemvKernelMaxBatch);
+  return gemm_api<EPI_STORE_F32>(nullptr, packed, scales, n_out, k, x, ldx, x_rows, batch, out, ldo, workspace,
+                                 workspace_bytes, stream, stamps, true);
 }
 
 SunStatus sun_gemm_w4_stamped(const void* packed, const void* scales, int64_t n_out, int64_t k, const void* x,
@@ -1479,6 +1587,18 @@ SunStatus sun_quantize_w4(const void* w, int64_t rows, int64_t k, int32_t group,
   SUN_CUDA(launch(quantize_w4_kernel, dim3(unsigned((groups + 7) / 8)), dim3(256), 0,
                   static_cast<cudaStream_t>(stream), false, static_cast<const __nv_bfloat16*>(w), (long long)rows,
                   (long long)((rows + 127) / 128 * 128), (long long)k,
+                  static_cast<uint8_t*>(packed), static_cast<__nv_bfloat16*>(scales)));
+  return SUN_OK;
+}
+
+SunStatus sun_import_w4_ct(const void* ct_packed, const void* ct_scales, int64_t rows, int64_t k, int32_t group,
+                           void* packed, void* scales, void* stream) {
+  if (rows < 1 || k < 1 || group != 128 || k % group != 0) return fail(SUN_ERR_VALUE, "bad import_w4_ct shape");
+  if (!ct_packed || !ct_scales || !packed || !scales) return fail(SUN_ERR_VALUE, "import_w4_ct: null pointer");
+  const long long groups = rows * (k / group);
+  SUN_CUDA(launch(import_w4_ct_kernel, dim3(unsigned((groups + 127) / 128)), dim3(128), 0,
+                  static_cast<cudaStream_t>(stream), false, static_cast<const uint32_t*>(ct_packed),
+                  static_cast<const __nv_bfloat16*>(ct_scales), (long long)rows, (long long)k,
                   static_cast<uint8_t*>(packed), static_cast<__nv_bfloat16*>(scales)));
   return SUN_OK;
 }

@@ -11,6 +11,7 @@ import ctypes
 import torch
 
 from . import _lib
+from .errors import UnsupportedShape
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
@@ -75,16 +76,18 @@ def gemm_bf16(w: torch.Tensor, x: torch.Tensor, batch: int, out: torch.Tensor | 
 
 def gemm_w4(packed: torch.Tensor, scales: torch.Tensor, n_out: int, k: int, x: torch.Tensor, batch: int,
             out: torch.Tensor | None = None, accumulate: bool = False,
-            workspace: torch.Tensor | None = None) -> torch.Tensor:
-    """QSUN W4A16 GEMM: out[b, n] (=|+=) sum_k deq(w)[n, k] x[b, k]."""
+            workspace: torch.Tensor | None = None, gemv: bool = False) -> torch.Tensor:
+    """QSUN W4A16 GEMM: out[b, n] (=|+=) sum_k deq(w)[n, k] x[b, k]. gemv=True runs the
+    small-batch GEMV kernel (batch <= 16) that QSUN decode steps of <= 16 rows use."""
     _need_cuda(packed, scales, x)
     if out is None:
         out = torch.zeros(batch, n_out, dtype=torch.float32, device=x.device)
     ws = gemm_workspace(n_out, k, batch, x.device) if workspace is None else workspace
     lib = _lib.load()
-    _lib.check(lib.sun_gemm_w4(packed.data_ptr(), scales.data_ptr(), n_out, k, x.data_ptr(), x.stride(0), x.shape[0],
-                               batch, out.data_ptr(), out.stride(0), int(accumulate), ws.data_ptr(), ws.numel(),
-                               _stream()), "sun_gemm_w4")
+    fn = lib.sun_gemv_w4 if gemv else lib.sun_gemm_w4
+    _lib.check(fn(packed.data_ptr(), scales.data_ptr(), n_out, k, x.data_ptr(), x.stride(0), x.shape[0],
+                  batch, out.data_ptr(), out.stride(0), int(accumulate), ws.data_ptr(), ws.numel(),
+                  _stream()), "sun_gemv_w4" if gemv else "sun_gemm_w4")
     return out
 
 
@@ -128,4 +131,24 @@ def quantize_w4(w: torch.Tensor, group: int = 128) -> tuple[torch.Tensor, torch.
     lib = _lib.load()
     _lib.check(lib.sun_quantize_w4(w.contiguous().data_ptr(), rows, k, group, packed.data_ptr(), scales.data_ptr(),
                                    _stream()), "sun_quantize_w4")
+    return packed, scales
+
+
+def import_w4_ct(ct_packed: torch.Tensor, ct_scales: torch.Tensor, group: int = 128
+                 ) -> tuple[torch.Tensor, torch.Tensor]:
+    """compressed-tensors pack-quantized W4 (int32 [rows, K/8], bf16 [rows, K/group]) -> SUN-W4
+    (packed uint8, scales bf16 [rows_pad/128, K/g, 128]) on the GPU, bit-preserving."""
+    _need_cuda(ct_packed, ct_scales)
+    if ct_packed.dtype != torch.int32 or ct_scales.dtype != torch.bfloat16:
+        raise UnsupportedShape("compressed-tensors import needs int32 weight_packed and bf16 weight_scale")
+    rows, k8 = ct_packed.shape
+    k = k8 * 8
+    if tuple(ct_scales.shape) != (rows, k // group):
+        raise UnsupportedShape(f"weight_scale {tuple(ct_scales.shape)} does not match {rows} x {k}/{group}")
+    rows_pad = (rows + 127) // 128 * 128
+    packed = torch.zeros(rows_pad * k // 2, dtype=torch.uint8, device=ct_packed.device)
+    scales = torch.zeros(rows_pad // 128, k // group, 128, dtype=torch.bfloat16, device=ct_packed.device)
+    lib = _lib.load()
+    _lib.check(lib.sun_import_w4_ct(ct_packed.contiguous().data_ptr(), ct_scales.contiguous().data_ptr(), rows, k,
+                                    group, packed.data_ptr(), scales.data_ptr(), _stream()), "sun_import_w4_ct")
     return packed, scales

@@ -11,6 +11,7 @@ token, as Eq. 2 specifies.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import torch
 
@@ -21,13 +22,26 @@ from .weights import DeviceWeights
 
 
 W4_CHAIN_MAX_BATCH = 128  # sun_capi.cu kW4ChainMaxBn: QSUN chain up to bn = 128
+W4_GEMV_MAX_BATCH = 8  # sun_capi.cu kGemvMaxBatch: QSUN steps of <= 8 rows run the W4 GEMV
+
+
+def uses_w4_gemv(weight_bits: int, batch: int, env: str | None = None) -> bool:
+    """Whether a QSUN step runs the small-batch W4 GEMV launches (mirrors sun_capi.cu
+    use_gemv; SUN_W4_GEMV=0 keeps the tcgen05 path)."""
+    if env is None:
+        env = os.environ.get("SUN_W4_GEMV")
+    try:
+        on = int(env) != 0 if env is not None else True
+    except ValueError:  # atoi semantics
+        on = False
+    return weight_bits == 4 and on and batch <= W4_GEMV_MAX_BATCH
 
 
 def uses_gemm_chain(weight_bits: int, distinct_rows: bool, env: str | None, batch: int = 1) -> bool:
     """Whether sun_decode_step runs the persistent layer GEMM chain (mirrors
     sun_capi.cu use_chain): decode batches by default (QSUN: up to 128 rows),
     SUN_GEMM_CHAIN=0/1 forces."""
-    if weight_bits == 4 and (batch + 15) // 16 * 16 > W4_CHAIN_MAX_BATCH:
+    if weight_bits == 4 and ((batch + 15) // 16 * 16 > W4_CHAIN_MAX_BATCH or uses_w4_gemv(4, batch)):
         return False
     if env is not None:
         try:
@@ -158,7 +172,8 @@ class _StepRunner:
         ran unsplit (combine=False)."""
         combine = (not self.fused_combine) if combine is None else combine
         batch = self.max_batch if batch is None else batch
-        chain = self.gemm_chain and (self.spec.weight_bits == 16 or (batch + 15) // 16 * 16 <= W4_CHAIN_MAX_BATCH)
+        chain = self.gemm_chain and (self.spec.weight_bits == 16 or (
+            (batch + 15) // 16 * 16 <= W4_CHAIN_MAX_BATCH and not uses_w4_gemv(4, batch)))
         names = ["embed_norm"]
         if chain:  # O -> gate_up -> down -> next QKV as one launch per layer
             names.append("gemm_qkv_rope_kv")

@@ -135,6 +135,30 @@ class DeviceWeights:
             self.layers.append(L)
         self._build_struct()
 
+    @classmethod
+    def from_layout(cls, spec: DecoderSpec, embed: torch.Tensor, final_norm: torch.Tensor, lm_head: torch.Tensor,
+                    layers: list[dict], device: torch.device, max_context: int) -> "DeviceWeights":
+        """Tensors already in the kernels' layout (a checkpoint, checkpoint.py): nothing
+        is quantised or re-blocked; only the RoPE tables are computed for max_context."""
+        self = cls.__new__(cls)
+        self.spec, self.device = spec, torch.device(device)
+        need = ["attn_norm", "ffn_norm", "w_qkv", "w_o", "w_gate_up", "w_down"]
+        if spec.weight_bits == 4:
+            need += ["s_qkv", "s_o", "s_gate_up", "s_down"]
+        if spec.qkv_bias:
+            need.append("b_qkv")
+        for l, L in enumerate(layers):
+            missing = [k for k in need if k not in L]
+            if missing:
+                raise ValueError(f"layer {l}: missing {missing}")
+        if len(layers) != spec.n_layers:
+            raise ValueError(f"{len(layers)} layers for a {spec.n_layers}-layer spec")
+        self.embed, self.final_norm, self.lm_head, self.layers = embed, final_norm, lm_head, layers
+        cos, sin = rope_tables(max_context, spec.head_dim, spec.rope_theta)
+        self.rope_cos, self.rope_sin = cos.to(self.device), sin.to(self.device)
+        self._build_struct()
+        return self
+
     def _build_struct(self) -> None:
         ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
         arr = (_lib.SunLayerWeights * len(self.layers))()

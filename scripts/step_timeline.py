@@ -15,8 +15,14 @@ ap.add_argument("--config", default="c3")
 ap.add_argument("--layers", type=int, default=3, help="layers to print")
 ap.add_argument("--stamp", type=int, default=-1, help="launch index whose per-CTA phases to print")
 ap.add_argument("--slow", type=int, default=0, help="with --stamp: also list the N CTAs that finish last")
+ap.add_argument("--batch", type=int, default=0, help="override the config's batch")
+ap.add_argument("--isl", type=int, default=0, help="override the config's context start")
 args = ap.parse_args()
-cfg = bench.CONFIGS[args.config]
+cfg = dict(bench.CONFIGS[args.config])
+if args.batch:
+    cfg["batch"] = args.batch
+if args.isl:
+    cfg["isl"] = args.isl
 spec = SPECS[cfg["spec"]].with_bits(4) if cfg["bits"] == 4 else SPECS[cfg["spec"]]
 dev = torch.device("cuda")
 B = cfg["batch"]

@@ -1,13 +1,15 @@
 """QSUN W4 GEMM bottleneck probe: standalone sun_gemm_w4 timings (CUDA events, L2
 flushed) for the library named by SUN_LIB (A/B variants built by
 scripts/build_variant.sh: -DSUN_W4_NO_CVT skips the dequant arithmetic,
--DSUN_W4_NO_MMA skips the MMAs; both timing-only)."""
+-DSUN_W4_NO_MMA skips the MMAs; both timing-only). PROBE_GEMV=1 times the
+small-batch GEMV kernel for B <= 16."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2603_02599_b200 import kernels
 
 dev = torch.device("cuda")
+GEMV = os.environ.get("PROBE_GEMV") == "1"  # small-batch W4 GEMV kernel for B <= 16
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 shapes = [(28672, 4096), (4096, 14336), (6144, 4096), (4096, 4096)]
 res = {}
@@ -23,12 +25,12 @@ for n_out, k in shapes:
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            kernels.gemm_w4(packed, scales, n_out, k, x, B, out=out, workspace=ws)
+            kernels.gemm_w4(packed, scales, n_out, k, x, B, out=out, workspace=ws, gemv=GEMV and B <= 16)
             e1.record()
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
         t = sorted(ts[2:])[len(ts[2:]) // 2]
         wb = n_out * k // 2 + n_out * (k // 128) * 2
         res[f"{n_out}x{k}/B{B}"] = round(t * 1e3, 1)
-        print(f"{os.environ.get('SUN_LIB', 'default')[-30:]:30s} W4 {n_out}x{k} B={B}: {t*1e3:7.1f} us  {wb/t/1e6:6.0f} GB/s", flush=True)
+        print(f"{('gemv ' if GEMV and B <= 16 else '') + os.environ.get('SUN_LIB', 'default')[-30:]:30s} W4 {n_out}x{k} B={B}: {t*1e3:7.1f} us  {wb/t/1e6:6.0f} GB/s", flush=True)
 print(json.dumps(res))

@@ -169,7 +169,7 @@ def _dequantized_decoder_weights(spec, w):
     return out
 
 
-@pytest.mark.parametrize("variant", ["qsun_w4", "qkv_bias"])
+@pytest.mark.parametrize("variant", ["qsun_w4", "qsun_w4_b12", "qkv_bias"])
 def test_tiny_variants_mixed_batch(cuda, variant):
     """QSUN (W4A16 g128 shared decoder, bf16 prefill modules and lm_head,
     PAPER.md:515-519) and Qwen2.5-style QKV bias, end to end vs the oracle."""
@@ -178,15 +178,16 @@ def test_tiny_variants_mixed_batch(cuda, variant):
     from paper_2603_02599_b200.spec import TINY
     from paper_2603_02599_b200.weights import init_weights, perturb
 
-    if variant == "qsun_w4":
+    if variant.startswith("qsun_w4"):
         spec = replace(TINY, name="tiny-w4", ffn=768, weight_bits=4)  # W4 needs K % 128 == 0
     else:
         spec = replace(TINY, name="tiny-bias", qkv_bias=True)
     w_d = init_weights(spec, seed=0)
     w_ps = [perturb(spec, w_d, seed=1), perturb(spec, w_d, seed=2)]
-    prompts = make_prompts(6, spec.vocab)
-    module_of = [i % 2 for i in range(6)]
-    if variant == "qsun_w4":
+    n = 12 if variant == "qsun_w4_b12" else 6  # 6 rows: the small-batch W4 GEMV; 12: the W4 chain
+    prompts = make_prompts(n, spec.vocab)
+    module_of = [i % 2 for i in range(n)]
+    if variant.startswith("qsun_w4"):
         # GPU: DeviceWeights quantises θ_d in-kernel; prefill modules stay bf16
         from dataclasses import replace as rp
 

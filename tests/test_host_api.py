@@ -171,4 +171,11 @@ def test_step_flags_and_chain_selection():
     assert not uses_gemm_chain(16, True, "x") and not uses_gemm_chain(4, True, "0")
     # QSUN: the W4 layer chain up to 128 rows, separate launches above
     assert uses_gemm_chain(4, True, None, batch=128) and not uses_gemm_chain(4, True, None, batch=129)
-    assert uses_gemm_chain(4, False, "1", batch=1) and not uses_gemm_chain(4, True, "1", batch=256)
+    assert uses_gemm_chain(4, False, "1", batch=17) and not uses_gemm_chain(4, True, "1", batch=256)
+    # QSUN steps of <= 8 rows run the small-batch W4 GEMV (SUN_W4_GEMV=0: the chain / tcgen05 path)
+    from paper_2603_02599_b200.modules import uses_w4_gemv
+
+    assert uses_w4_gemv(4, 8, None) and not uses_w4_gemv(4, 9, None) and not uses_w4_gemv(16, 1, None)
+    assert not uses_w4_gemv(4, 1, "0") and uses_w4_gemv(4, 1, "1")
+    if os.environ.get("SUN_W4_GEMV", "1") != "0":
+        assert not uses_gemm_chain(4, True, None, batch=8) and uses_gemm_chain(4, True, None, batch=9)

@@ -58,7 +58,7 @@ def test_gemm_deterministic_stream_k(cuda):
         assert torch.equal(a, kernels.gemm_bf16(w, x, 64))
 
 
-@pytest.mark.parametrize("sched", ["0", "2", "vcl2", "novcl", "push", "nochain", "l2chain"])
+@pytest.mark.parametrize("sched", ["0", "2", "vcl2", "novcl", "push", "nochain", "l2chain", "nogemv"])
 def test_gemm_schedules_subprocess(sched):
     """The GEMM kernel tests and the end-to-end decode parity under the other
     schedules: 0 = cluster split-K / whole tiles only, 2 = stream-K on every
@@ -68,7 +68,8 @@ def test_gemm_schedules_subprocess(sched):
     copies (instead of pulled after a cluster barrier), nochain = separate GEMM launches
     instead of the persistent per-layer GEMM chain kernels (the decode default, bf16 and
     QSUN), l2chain = the chains over plain CTAs with every split phase reduced through L2
-    (instead of 4-CTA clusters reducing over DSMEM)."""
+    (instead of 4-CTA clusters reducing over DSMEM), nogemv = QSUN decode batches of <= 16
+    rows on the tcgen05 W4 GEMM instead of the small-batch W4 GEMV."""
     import os
     import subprocess
     import sys
@@ -85,6 +86,8 @@ def test_gemm_schedules_subprocess(sched):
         env["SUN_GEMM_CHAIN"] = "0"
     elif sched == "l2chain":
         env["SUN_CHAIN_CLUSTER"] = "0"
+    elif sched == "nogemv":
+        env["SUN_W4_GEMV"] = "0"
     else:
         env["SUN_GEMM_SCHED"] = sched
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", "(gemm or tiny) and not subprocess",
@@ -205,7 +208,7 @@ def test_w4_quantizer_bit_exact_vs_oracle(cuda, rows, k):
     pg, pr = by_row(packed.cpu().numpy()), by_row(p_ref)
     assert np.array_equal(pg[:rows], pr[:rows])
     sg = scales.cpu().view(torch.int16).numpy().astype(np.uint16)  # [rows_pad/128, K/128, 128]
-    by_row_s = lambda a: a.transpose(0, 2, 1).reshape(rows_pad, -1)  # noqa: E731
+    by_row_s = lambda a: a[..., quant_ref.SCALE_POS].transpose(0, 2, 1).reshape(rows_pad, -1)  # noqa: E731
     assert np.array_equal(by_row_s(sg)[:rows], by_row_s(s_ref)[:rows])
     assert torch.equal(quant_ref.unpack(packed.cpu().numpy(), rows, k), q)
 
@@ -225,3 +228,34 @@ def test_gemm_w4_matches_dequantized_fp32(cuda, n_out, k, batch):
     deq = quant_ref.dequantize(q, s)  # bf16(q * s): the exact tcgen05 operand
     ref = x[:batch].float() @ deq.float().t()
     torch.testing.assert_close(out, ref, rtol=1e-4, atol=1e-4 * math.sqrt(k))
+
+
+@pytest.mark.parametrize("n_out,k,batch", [(256, 256, 1), (300, 512, 5), (768, 512, 8), (4096, 4096, 9),
+                                           (6144, 4096, 16), (28672, 4096, 16), (4096, 14336, 1), (1536, 14336, 3),
+                                           (128, 128, 2)])
+def test_gemv_w4_matches_group_scaled_fp64(cuda, n_out, k, batch):
+    """Small-batch W4 GEMV (stream-K, L2 partials): exactly sum_g s_g * sum_k q x up to
+    fp32 summation order; and within the bf16 rounding of q*s of the tcgen05 operand."""
+    from oracle import quant_ref
+    from paper_2603_02599_b200 import kernels
+
+    g = torch.Generator(device="cpu").manual_seed(n_out * 3 + k + batch)
+    w = (torch.randn(n_out, k, generator=g) * 0.02).to(torch.bfloat16)
+    x = torch.randn(_r16(batch), k, generator=g).to(torch.bfloat16)
+    x[batch:] = float("nan")  # padding rows of the activation must not leak
+    packed, scales = kernels.quantize_w4(w.to(cuda))
+    ws = kernels.gemm_workspace(n_out, k, batch, cuda)
+    out = kernels.gemm_w4(packed, scales, n_out, k, x.to(cuda), batch, workspace=ws, gemv=True)
+    out2 = kernels.gemm_w4(packed, scales, n_out, k, x.to(cuda), batch, workspace=ws, gemv=True)
+    acc = kernels.gemm_w4(packed, scales, n_out, k, x.to(cuda), batch, out=out.clone(), accumulate=True,
+                          workspace=ws, gemv=True)
+    torch.cuda.synchronize()
+    assert torch.equal(out, out2)  # deterministic stream-K reduction, self-resetting counters
+    q, s = quant_ref.quantize(w)
+    xs = x[:batch].double().view(batch, k // 128, 128)
+    qs = q.double().view(n_out, k // 128, 128)
+    exact = torch.einsum("bgk,ngk,ng->bn", xs, qs, s.double())
+    torch.testing.assert_close(out.cpu().double(), exact, rtol=1e-4, atol=1e-4 * math.sqrt(k))
+    torch.testing.assert_close(acc.cpu().double(), 2 * exact, rtol=1e-4, atol=2e-4 * math.sqrt(k))
+    deq_ref = x[:batch].float() @ quant_ref.dequantize(q, s).float().t()
+    torch.testing.assert_close(out.cpu(), deq_ref, rtol=1e-2, atol=2e-3 * math.sqrt(k) * 0.02 * 8)
