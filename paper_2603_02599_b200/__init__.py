@@ -9,6 +9,7 @@ from .pricing import (AnalyticBackend, CalibrationTarget, CostParams, DecodeBack
                       calibrate_decode, decode_step_time, decode_step_time_from_totals, kv_step_bytes,
                       load_targets_csv, prefill_time, single_request_tpot, single_request_ttft, step_bytes,
                       transfer_time)
+from .harness import ROW_FIELDS, SUMMARY_FIELDS, summary_row
 from .scheduler import SimResult, SimulationDiverged, run
 from .router import DecodeDispatcher, PoolSnapshot, outstanding_tokens, route_prefill
 from .spec import LLAMA31_8B, LLAMA32_1B, QWEN25_14B, SPECS, TINY, DecoderSpec
@@ -36,4 +37,5 @@ __all__ = [
     "DecoderSpec", "SPECS", "TINY", "LLAMA32_1B", "LLAMA31_8B", "QWEN25_14B", "calibrate_decode",
     "decode_step_time_from_totals", "kv_step_bytes", "load_targets_csv", "nearest_rank", "outstanding_tokens",
     "single_request_tpot", "single_request_ttft", "step_bytes", "read_trace", "write_trace",
+    "ROW_FIELDS", "SUMMARY_FIELDS", "summary_row",
 ]

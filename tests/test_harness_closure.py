@@ -89,3 +89,64 @@ def test_serving_loop_on_measured_b200_steps():
     # the analytic reference price differs (it has no batch term)
     ana = scheduler.run(cfg, trace, COST)
     assert [s[2] for s in ana.log.steps] != [s[2] for s in res.log.steps]
+
+
+# poolsim harness.py:33-45 ROW_FIELDS (the reference's row schema, as its module builds it)
+REFERENCE_ROW_FIELDS = [
+    "config_hash", "decode_pool_mode", "decode_pool_size", "alpha", "isl", "osl", "offered_rps",
+    "completed_requests", "ttft_mean_s", "ttft_p50_s", "ttft_p99_s", "tpot_mean_s", "tpot_p50_s", "tpot_p99_s",
+    "itl_mean_s", "interactivity_tok_s", "output_throughput_tok_s", "throughput_per_decode_gpu_tok_s",
+    "throughput_per_gpu_all_tok_s", "achieved_rps", "achieved_offered_ratio", "seed", "cell_index", "replicate",
+    "error"]
+ROWS_CSV = os.path.join(GOLDEN, "b200_consolidation_rows.csv")
+
+
+def test_row_schema_is_the_reference_one():
+    import csv
+    import subprocess
+    import sys
+
+    from paper_2603_02599_b200 import harness
+
+    assert harness.ROW_FIELDS == REFERENCE_ROW_FIELDS
+    with open(ROWS_CSV) as fh:
+        assert next(csv.reader(fh)) == REFERENCE_ROW_FIELDS
+    src = "/root/reference/pkg/src"
+    if os.path.isdir(src):  # the build container: check against the reference module itself
+        out = subprocess.run([sys.executable, "-c", "import sys; sys.path.insert(0, %r); "
+                              "from poolsim.harness import ROW_FIELDS; print(','.join(ROW_FIELDS))" % src],
+                             capture_output=True, text=True, cwd="/tmp", env={**os.environ,
+                                                                               "PYTHONDONTWRITEBYTECODE": "1"})
+        assert out.returncode == 0, out.stderr
+        assert out.stdout.strip().split(",") == REFERENCE_ROW_FIELDS
+
+
+def test_consolidation_rows_reproduce_and_shared_tpot_within_5pct():
+    """The committed rows (scripts/harness_rows.py: sweep_consolidation.toml's axes plus the
+    4 x 1P/1D partition, decode priced by the B200 step table) are reproduced exactly, and
+    the shared pool's TPOT p50 is within 5% of (here: at or below) the per-model partition's
+    at equal GPU count (north star: TPOT within 5% of a partitioned decode)."""
+    import csv
+    import io
+
+    from paper_2603_02599_b200 import harness
+    from scripts.harness_rows import COST
+
+    hdr, pts = _load("b200_steps_8b_bf16.json")
+    backend = pricing.MeasuredBackend(pts, hdr["kv_bytes_per_token"])
+    cells = harness.consolidation_cells(B200)[:5]  # alpha 0, osl 128: the partition + pools 4..1
+    rows = [harness.run_cell(c, COST, backend, "b200-measured:b200_steps_8b_bf16.json") for c in cells]
+    buf = io.StringIO()
+    harness.write_rows(rows, buf)
+    committed = open(ROWS_CSV).read().splitlines()
+    assert buf.getvalue().splitlines() == committed[:6]
+    table = list(csv.DictReader(open(ROWS_CSV)))
+    assert len(table) == 20 and not any(r["error"] for r in table)
+    for (alpha, osl) in [("0.0", "128"), ("0.0", "256"), ("1.5", "128"), ("1.5", "256")]:
+        sel = [r for r in table if r["alpha"] == alpha and r["osl"] == osl]
+        iso = [r for r in sel if r["decode_pool_mode"] == "isolated"][0]
+        sh4 = [r for r in sel if r["decode_pool_mode"] == "shared" and r["decode_pool_size"] == "4"][0]
+        assert float(sh4["tpot_p50_s"]) <= 1.05 * float(iso["tpot_p50_s"])
+        # consolidation: per-decode-GPU throughput grows as the shared pool shrinks
+        thr = [float(r["throughput_per_decode_gpu_tok_s"]) for r in sel if r["decode_pool_mode"] == "shared"]
+        assert thr == sorted(thr)
