@@ -69,7 +69,7 @@ def test_measured_backend_predicts_the_c3_bench():
     contexts 1024..1279 growing while timed) within 3%."""
     hdr, pts = _load("b200_steps_8b_bf16.json")
     mb = pricing.MeasuredBackend(pts, hdr["kv_bytes_per_token"])
-    line = json.load(open(os.path.join(ROOT, "profiles", "r01", "bench_c3_n1.json")))
+    line = json.load(open(os.path.join(ROOT, "profiles", "r02", "bench_c3_n1.json")))
     ctx_mean = (line["config"]["ctx_min"] + line["config"]["ctx_max"]) / 2 + line["warmup"] + line["steps"] / 2
     pred = mb.predict(line["config"]["batch_per_gpu"], ctx_mean)
     assert pred == pytest.approx(line["ms_per_step"] / 1e3, rel=0.03)
