@@ -8,6 +8,12 @@ fill the prompt KV into those pages (Eq. 2); every scheduled step runs
 the frozen shared decode module over the batch's block tables (Eq. 3); at
 retirement the pages go back to the allocator (the reference's ``_free_kv``,
 engine.py:360-365).
+
+Members only need the reference's ``_Member`` fields (engine.py:135-145): ``request``
+(``id``, ``model_id``, ``isl``, ``target_osl``) and ``steps_done``. The physical pages of a
+request are kept here, keyed by request id, and mirrored onto ``member.kv.pages`` when the
+handle has that field (this package's ``KvHandle``) — so poolsim's own ``_Member`` /
+``KvHandle`` objects drive it unchanged (tests/test_executor.py).
 """
 from __future__ import annotations
 
@@ -38,6 +44,7 @@ class B200Executor:
         self.graph = graph
         self.last_token: dict[int, int] = {}
         self.first_token: dict[int, int] = {}
+        self.pages: dict[int, list[int]] = {}  # request id -> its pages in the shared pool
         self.steps_run = 0
         self.keep_logits = keep_logits
         self.logits: dict[int, list] = {}  # request id -> [first-token logits, step logits...] (testing)
@@ -55,9 +62,12 @@ class B200Executor:
 
     def admit(self, m: Member) -> None:
         r = m.request
-        m.kv.pages = self.alloc.alloc(pages_for(r.isl + r.target_osl - 1))
+        pages = self.alloc.alloc(pages_for(r.isl + r.target_osl - 1))
+        self.pages[r.id] = pages
+        if hasattr(m.kv, "pages"):
+            m.kv.pages = pages
         pre = self.prefills[r.model_id]
-        first, lg = pre.prefill([self.prompt_of(r.id, r.isl)], [m.kv.pages])
+        first, lg = pre.prefill([self.prompt_of(r.id, r.isl)], [pages])
         if self.keep_logits:
             self.logits[r.id] = [lg[0].cpu()]
         self.first_token[r.id] = first[0]
@@ -67,11 +77,14 @@ class B200Executor:
         b = len(members)
         tokens = torch.tensor([self.last_token[m.request.id] for m in members], dtype=torch.int32)
         positions = torch.tensor([m.request.isl + m.steps_done for m in members], dtype=torch.int32)
-        width = max(len(m.kv.pages) for m in members)
+        rows = [self.pages[m.request.id] for m in members]
+        width = max(len(p) for p in rows)
         bt = torch.zeros(b, width, dtype=torch.int32)
-        for i, m in enumerate(members):
-            bt[i, :len(m.kv.pages)] = torch.tensor(m.kv.pages, dtype=torch.int32)
-        nxt = self.dec.decode(tokens.pin_memory(), positions.pin_memory(), bt.pin_memory(), graph=self.graph).cpu()
+        for i, p in enumerate(rows):
+            bt[i, :len(p)] = torch.tensor(p, dtype=torch.int32)
+        if torch.cuda.is_available():
+            tokens, positions, bt = tokens.pin_memory(), positions.pin_memory(), bt.pin_memory()
+        nxt = self.dec.decode(tokens, positions, bt, graph=self.graph).cpu()
         out = [int(x) for x in nxt]
         lg = self.dec.logits[:b].cpu() if self.keep_logits else None
         for i, (m, t) in enumerate(zip(members, out)):
@@ -82,5 +95,6 @@ class B200Executor:
         return out
 
     def retire(self, m: Member) -> None:
-        self.alloc.free(m.kv.pages)
-        m.kv.pages = []
+        self.alloc.free(self.pages.pop(m.request.id))
+        if hasattr(m.kv, "pages"):
+            m.kv.pages = []
