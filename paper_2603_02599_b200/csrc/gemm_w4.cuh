@@ -255,234 +255,384 @@ SUN_DEVICE void gv_math(const GvFrag<NB>& f, float (&acc)[kGvMT][NB][4]) {
 
 SUN_DEVICE void gv_bar() { asm volatile("bar.sync 2, 512;" ::: "memory"); }  // the 16 compute warps
 
+// Shared-memory map of a GEMV CTA: the stage ring, the fp32 staging tile T, the epilogue
+// area of epi_chunk (meta + one group's staging), the ring barriers and a flag word.
+struct GvSmem {
+  uint8_t* ring;
+  float* T;
+  float* epi;
+  uint64_t* full;
+  uint64_t* empty;
+  int* flag;
+};
+SUN_DEVICE GvSmem gv_smem(uint8_t* smem, int stages, uint32_t sb) {
+  GvSmem m;
+  m.ring = smem;
+  m.T = reinterpret_cast<float*>(smem + stages * sb);
+  m.epi = m.T + kTileM * kGvTPitch;
+  m.full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(m.epi) + 3072 + kEpiGroupBytes);
+  m.empty = m.full + kGvMaxStages;
+  m.flag = reinterpret_cast<int*>(m.empty + kGvMaxStages);
+  return m;
+}
+
+// This CTA's units [u0, u1) (unit = tile * KB + K block) of one GEMV: splits == 0: whole
+// tiles [c m / G, (c+1) m / G); splits == S: tile c / S, K blocks [r KB / S, (r+1) KB / S)
+// (r = c % S; CTAs c >= m S have none).
+SUN_DEVICE void gv_range(const GemmArgs& a, int c, int G, int& u0, int& u1) {
+  const int KB = a.ksteps, S = a.splits;
+  if (S == 0) {
+    u0 = static_cast<int>(static_cast<long long>(c) * a.m_tiles / G) * KB;
+    u1 = static_cast<int>(static_cast<long long>(c + 1) * a.m_tiles / G) * KB;
+  } else if (c < a.m_tiles * S) {
+    const int t0 = c / S, r = c % S;
+    u0 = t0 * KB + r * KB / S;
+    u1 = t0 * KB + (r + 1) * KB / S;
+  } else {
+    u0 = u1 = 0;
+  }
+}
+
+// Producer (one elected thread): the stages of [u0, u1) — up to kbs consecutive K blocks
+// of one tile each — into the ring, continuing at (slot, phase). The weight + scale copies
+// of the first ring's worth go out before `gate()` (they never depend on earlier work:
+// under PDL, or during the previous chain phase's tail), the activation copies after it.
+template <typename Gate>
+SUN_DEVICE void gv_produce(const GemmArgs& a, int u0, int u1, const GvSmem& m, int stages, int& slot, int& phase,
+                           Gate gate, int max_pre = kGvMaxStages) {
+  const int kbs = a.wgroup, bn = a.bn, KB = a.ksteps;
+  const uint32_t sb = gv_stage_bytes(bn, kbs);
+#if defined(SUN_GV_PROBE_NOSX)  // probes (timing only, results invalid): skip the scale and X copies
+  const uint32_t wbytes = kW4PackedBytes, xbytes = 0u;
+#elif defined(SUN_GV_PROBE_NOX)  // skip the X copies
+  const uint32_t wbytes = kW4PackedBytes + 256u, xbytes = 0u;
+#else
+  const uint32_t wbytes = kW4PackedBytes + 256u, xbytes = static_cast<uint32_t>(bn) * 256u;
+#endif
+  auto issue_w = [&](int u, int len) {
+    uint8_t* st = m.ring + slot * sb;
+    mbar_wait(&m.empty[slot], phase ^ 1);
+    mbar_arrive_expect_tx(&m.full[slot], static_cast<uint32_t>(len) * (wbytes + xbytes));
+    bulk_load_hint(st, a.w4_packed + static_cast<long long>(u) * kW4PackedBytes, len * kW4PackedBytes, &m.full[slot],
+                   kEvictFirst);
+#ifndef SUN_GV_PROBE_NOSX
+    bulk_load_hint(st + kbs * kW4PackedBytes, a.w4_scales + static_cast<long long>(u) * kTileM, len * 256u,
+                   &m.full[slot], kEvictFirst);
+#endif
+  };
+  auto issue_x = [&](int sl, int u, int len) {
+    if (xbytes)
+      bulk_load_hint(m.ring + sl * sb + kbs * (kW4PackedBytes + 256u),
+                     a.xact + static_cast<long long>(2 * (u % KB)) * bn * 128, len * xbytes, &m.full[sl], kEvictLast);
+  };
+  auto advance = [&]() {
+    if (++slot == stages) {
+      slot = 0;
+      phase ^= 1;
+    }
+  };
+  int pre_slot[kGvMaxStages], pre_u[kGvMaxStages], pre_len[kGvMaxStages];
+  int u = u0, npre = 0;
+  for (; npre < min(stages, max_pre) && u < u1; ++npre) {
+    const int len = min(kbs, min(u1 - u, KB - u % KB));
+    issue_w(u, len);
+    pre_slot[npre] = slot;
+    pre_u[npre] = u;
+    pre_len[npre] = len;
+    u += len;
+    advance();
+  }
+  gate();
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // activations written by other CTAs' stores
+  for (int i = 0; i < npre; ++i) issue_x(pre_slot[i], pre_u[i], pre_len[i]);
+  while (u < u1) {
+    const int len = min(kbs, min(u1 - u, KB - u % KB));
+    const int sl = slot;
+    issue_w(u, len);
+    issue_x(sl, u, len);
+    u += len;
+    advance();
+  }
+}
+
+// Compute warps: the segments of [u0, u1) continuing at the ring position (slot, phase),
+// each reduced over the chunk warps into T and finished by the fused epilogue (whole
+// tile) or parked in L2 for the tile's last-arriving split (which reduces and finishes it).
+// `gate()` runs first (all 512 compute threads): the epilogue metadata reads the previous
+// work's outputs.
+template <int EPI, int NB, typename Gate>
+SUN_DEVICE void gv_consume(const GemmArgs& a, int u0, int u1, const GvSmem& m, int stages, int& slot, int& phase,
+                           Gate gate, unsigned long long* pst = nullptr) {
+  const int kbs = a.wgroup, bn = a.bn, KB = a.ksteps, S = a.splits;
+  const uint32_t sb = gv_stage_bytes(bn, kbs);
+  const int warp = static_cast<int>(threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int c = static_cast<int>(blockIdx.x);
+  float* T = m.T;
+  gate();
+  if (pst && threadIdx.x == 0) pst[0] = gtimer();
+  if (warp >= 2 && warp < 6) load_qkv_meta<EPI>(a, m.epi);  // epilogue group: positions / pages / r_b
+  const int rq = warp & 3, ch = warp >> 2;  // row quarter, 32-k chunk of every block
+  const int g = lane >> 2, t = lane & 3;
+  const uint32_t ring_s = smem_u32(m.ring);
+  float acc[kGvMT][NB][4];
+  int u = u0;
+  while (u < u1) {
+    const int tile = u / KB;
+    const int seg_end = min(u1, (tile + 1) * KB);
+    const bool whole = (u == tile * KB) && (seg_end == (tile + 1) * KB);
+#pragma unroll
+    for (int mt = 0; mt < kGvMT; ++mt)
+#pragma unroll
+      for (int j = 0; j < NB; ++j) acc[mt][j][0] = acc[mt][j][1] = acc[mt][j][2] = acc[mt][j][3] = 0.f;
+    while (u < seg_end) {
+      const int len = min(kbs, seg_end - u);
+      mbar_wait(&m.full[slot], phase);
+      if (threadIdx.x == 0 && u == u0) {
+        SUN_STAMP(2);  // first stage landed
+        if (pst) pst[1] = gtimer();
+      }
+      const uint32_t st = ring_s + slot * sb;
+#ifndef SUN_GV_PROBE_IDLE  // probe: compute warps only pass the stages on (timing only)
+      {
+        auto ld = [&](GvFrag<NB>& f, int i) {
+          gv_load<NB>(f, st + i * kW4PackedBytes, st + kbs * kW4PackedBytes + i * 256,
+                      st + kbs * (kW4PackedBytes + 256u) + i * bn * 256, bn, rq, ch, lane);
+        };
+        GvFrag<NB> fa, fb;  // two fragment sets: block i+1 loads while block i computes
+        ld(fa, 0);
+        for (int i = 0; i < len; i += 2) {
+          if (i + 1 < len) ld(fb, i + 1);
+          gv_math<NB>(fa, acc);
+          if (i + 1 < len) {
+            if (i + 2 < len) ld(fa, i + 2);
+            gv_math<NB>(fb, acc);
+          }
+        }
+      }
+#endif
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&m.empty[slot]);
+      u += len;
+      if (++slot == stages) {
+        slot = 0;
+        phase ^= 1;
+      }
+    }
+    if (threadIdx.x == 0 && u == u1) {
+      SUN_STAMP(3);  // last stage consumed
+      if (pst) pst[2] = gtimer();
+    }
+    // fragments -> T[row][batch]: row 32 rq + 16 m + g (+8), batch 8 j + t (c0) / 8 j + t + 4 (c1)
+    // (gv_nrow of columns 2t, 2t+1); columns >= 8 NB are zero. Chunk 0's warps store,
+    // chunks 1..3 add in order (fixed summation order).
+    gv_bar();  // the previous segment's epilogue is done with T
+    for (int cc = 0; cc < 4; ++cc) {
+      if (ch == cc) {
+#pragma unroll
+        for (int mt = 0; mt < kGvMT; ++mt) {
+          const int r = 32 * rq + 16 * mt + g;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int jj = j < NB ? j : 0;
+            const bool have = j < NB;
+            float* p0 = T + r * kGvTPitch + 8 * j + t;
+            float* p1 = T + (r + 8) * kGvTPitch + 8 * j + t;
+            const float v0 = have ? acc[mt][jj][0] : 0.f, v1 = have ? acc[mt][jj][1] : 0.f;
+            const float v2 = have ? acc[mt][jj][2] : 0.f, v3 = have ? acc[mt][jj][3] : 0.f;
+            if (cc == 0) {
+              p0[0] = v0; p0[4] = v1; p1[0] = v2; p1[4] = v3;
+            } else {
+              p0[0] += v0; p0[4] += v1; p1[0] += v2; p1[4] += v3;
+            }
+          }
+        }
+      }
+      gv_bar();
+    }
+    bool run_epi = whole;
+    if (!whole) {
+      // park the partial: [c][128 rows][16] fp32, 8 floats per thread (split schedule:
+      // one segment per CTA)
+      const int tid = threadIdx.x & 255, row = tid >> 1, h = (tid & 1) * 8;
+      const bool mover = threadIdx.x < 256;  // 8 floats each
+      if (mover) {
+        float* dst = a.sk_part + static_cast<long long>(c) * 2 * (kTileM * 16) + row * 16 + h;
+        __stcg(reinterpret_cast<float4*>(dst), make_float4(T[row * kGvTPitch + h], T[row * kGvTPitch + h + 1],
+                                                           T[row * kGvTPitch + h + 2], T[row * kGvTPitch + h + 3]));
+        __stcg(reinterpret_cast<float4*>(dst + 4), make_float4(T[row * kGvTPitch + h + 4], T[row * kGvTPitch + h + 5],
+                                                               T[row * kGvTPitch + h + 6], T[row * kGvTPitch + h + 7]));
+        __threadfence();
+      }
+      gv_bar();
+      const int cf = tile * S, cl = tile * S + S - 1;
+      if (threadIdx.x == 0) {
+        const unsigned old = atomicAdd(a.sk_flags + tile, 1u);
+        *m.flag = (old == static_cast<unsigned>(cl - cf)) ? 1 : 0;
+      }
+      gv_bar();
+      run_epi = *m.flag != 0;
+      if (run_epi && mover) {  // last contributor: sum the tile's partials in split order
+        __threadfence();
+        float s8[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s8[e] = 0.f;
+        for (int c0 = cf; c0 <= cl; c0 += 4) {  // four partials' loads in flight per round trip
+          float4 pp[4][2];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float* src = a.sk_part + static_cast<long long>(c0 + e <= cl ? c0 + e : cl) * 2 * (kTileM * 16) +
+                               row * 16 + h;
+            pp[e][0] = __ldcg(reinterpret_cast<const float4*>(src));
+            pp[e][1] = __ldcg(reinterpret_cast<const float4*>(src + 4));
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (c0 + e > cl) break;
+            s8[0] += pp[e][0].x; s8[1] += pp[e][0].y; s8[2] += pp[e][0].z; s8[3] += pp[e][0].w;
+            s8[4] += pp[e][1].x; s8[5] += pp[e][1].y; s8[6] += pp[e][1].z; s8[7] += pp[e][1].w;
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) T[row * kGvTPitch + h + e] = s8[e];
+        if (threadIdx.x == 0) a.sk_flags[tile] = 0u;  // self-resetting for the next use
+      }
+      if (run_epi) gv_bar();
+    }
+    if (run_epi && warp >= 2 && warp < 6) {
+      const int q = warp & 3;
+      const int row_local = q * 32 + lane;
+      float v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = T[row_local * kGvTPitch + j];
+      epi_chunk<EPI>(a, tile, row_local, 0, v, m.epi);
+    }
+  }
+}
+
+SUN_DEVICE void gv_init_ring(const GvSmem& m, int stages) {
+  if (static_cast<int>(threadIdx.x >> 5) == kGvWarps && elect_one()) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&m.full[s], 1);
+      mbar_init(&m.empty[s], kGvWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+}
+
 template <int EPI, int NB>
 __global__ void __launch_bounds__(kGvThreads, 1) gemv_w4_kernel(const GemmArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   tl_begin(a.tl, a.tl_idx);
-  const int stages = a.stages, kbs = a.wgroup, bn = a.bn, KB = a.ksteps;
-  const uint32_t sb = gv_stage_bytes(bn, kbs);
-  uint8_t* ring = smem;
-  float* T = reinterpret_cast<float*>(ring + stages * sb);
-  float* epi = T + kTileM * kGvTPitch;
-  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(epi) + 3072 + kEpiGroupBytes);
-  uint64_t* empty = full + kGvMaxStages;
-  int* flag = reinterpret_cast<int*>(empty + kGvMaxStages);
-  const int warp = warp_id_sync(), lane = threadIdx.x & 31;
-  const int G = static_cast<int>(gridDim.x), c = static_cast<int>(blockIdx.x);
-  // work: splits == 0: whole tiles [c m / G, (c+1) m / G); splits == S: tile c / S, K blocks
-  // [r KB / S, (r+1) KB / S) of it (r = c % S)
-  const int S = a.splits;
+  const int stages = a.stages;
+  const GvSmem m = gv_smem(smem, stages, gv_stage_bytes(a.bn, a.wgroup));
+  const int warp = warp_id_sync();
   int u0, u1;
-  if (S == 0) {
-    u0 = static_cast<int>(static_cast<long long>(c) * a.m_tiles / G) * KB;
-    u1 = static_cast<int>(static_cast<long long>(c + 1) * a.m_tiles / G) * KB;
-  } else {
-    const int t0 = c / S, r = c % S;
-    u0 = t0 * KB + r * KB / S;
-    u1 = t0 * KB + (r + 1) * KB / S;
-  }
+  gv_range(a, static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), u0, u1);
   if (threadIdx.x == 0) SUN_STAMP(0);
-  if (warp == kGvWarps && elect_one()) {
-    for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kGvWarps);
-    }
-    fence_barrier_init();
-  }
-  __syncthreads();
+  gv_init_ring(m, stages);
   pdl_launch_dependents();
   if (threadIdx.x == 0) SUN_STAMP(1);
-
+  int slot = 0, phase = 0;
   if (warp == kGvWarps) {
-    // ---- producer: stages of up to kbs K blocks, never crossing a tile boundary
-    if (elect_one()) {
-#if defined(SUN_GV_PROBE_NOSX)  // probes (timing only, results invalid): skip the scale and X copies
-      const uint32_t wbytes = kW4PackedBytes, xbytes = 0u;
-#elif defined(SUN_GV_PROBE_NOX)  // skip the X copies
-      const uint32_t wbytes = kW4PackedBytes + 256u, xbytes = 0u;
-#else
-      const uint32_t wbytes = kW4PackedBytes + 256u, xbytes = static_cast<uint32_t>(bn) * 256u;
-#endif
-      int u = u0, slot = 0, phase = 0, issued = 0;
-      // first ring's worth: weights + scales before the dependency wait
-      int pu = u0, pre = 0;
-      for (; pre < stages && pu < u1; ++pre) {
-        const int len = min(kbs, min(u1 - pu, KB - pu % KB));
-        uint8_t* st = ring + pre * sb;
-        mbar_arrive_expect_tx(&full[pre], static_cast<uint32_t>(len) * (wbytes + xbytes));
-        bulk_load_hint(st, a.w4_packed + static_cast<long long>(pu) * kW4PackedBytes, len * kW4PackedBytes,
-                       &full[pre], kEvictFirst);
-#ifndef SUN_GV_PROBE_NOSX
-        bulk_load_hint(st + kbs * kW4PackedBytes, a.w4_scales + static_cast<long long>(pu) * kTileM, len * 256u,
-                       &full[pre], kEvictFirst);
-#endif
-        pu += len;
-      }
-      pdl_wait();  // activations are the previous kernel's output
-      for (; u < u1; ++issued) {
-        const int kb = u % KB;
-        const int len = min(kbs, min(u1 - u, KB - kb));
-        uint8_t* st = ring + slot * sb;
-        if (issued >= pre) {
-          mbar_wait(&empty[slot], phase ^ 1);
-          mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(len) * (wbytes + xbytes));
-          bulk_load_hint(st, a.w4_packed + static_cast<long long>(u) * kW4PackedBytes, len * kW4PackedBytes,
-                         &full[slot], kEvictFirst);
-#ifndef SUN_GV_PROBE_NOSX
-          bulk_load_hint(st + kbs * kW4PackedBytes, a.w4_scales + static_cast<long long>(u) * kTileM, len * 256u,
-                         &full[slot], kEvictFirst);
-#endif
-        }
-        if (xbytes)
-          bulk_load_hint(st + kbs * (kW4PackedBytes + 256u), a.xact + static_cast<long long>(2 * kb) * bn * 128,
-                         len * xbytes, &full[slot], kEvictLast);
-        u += len;
-        if (++slot == stages) {
-          slot = 0;
-          phase ^= 1;
-        }
-      }
-    }
+    if (elect_one()) gv_produce(a, u0, u1, m, stages, slot, phase, [] { pdl_wait(); });
   } else {
-    // ---- compute warps
-    pdl_wait();
-    if (warp >= 2 && warp < 6) load_qkv_meta<EPI>(a, epi);  // epilogue group: positions / pages / r_b
-    const int rq = warp & 3, ch = warp >> 2;  // row quarter, 32-k chunk of every block
-    const int g = lane >> 2, t = lane & 3;
-    const uint32_t ring_s = smem_u32(ring);
-    float acc[kGvMT][NB][4];
-    int u = u0, slot = 0, phase = 0;
-    while (u < u1) {
-      const int tile = u / KB;
-      const int seg_end = min(u1, (tile + 1) * KB);
-      const bool whole = (u == tile * KB) && (seg_end == (tile + 1) * KB);
-#pragma unroll
-      for (int m = 0; m < kGvMT; ++m)
-#pragma unroll
-        for (int j = 0; j < NB; ++j) acc[m][j][0] = acc[m][j][1] = acc[m][j][2] = acc[m][j][3] = 0.f;
-      while (u < seg_end) {
-        const int len = min(kbs, seg_end - u);
-        mbar_wait(&full[slot], phase);
-        if (threadIdx.x == 0 && u == u0) SUN_STAMP(2);  // first stage landed
-        const uint32_t st = ring_s + slot * sb;
-#ifndef SUN_GV_PROBE_IDLE  // probe: compute warps only pass the stages on (timing only)
-        {
-          auto ld = [&](GvFrag<NB>& f, int i) {
-            gv_load<NB>(f, st + i * kW4PackedBytes, st + kbs * kW4PackedBytes + i * 256,
-                        st + kbs * (kW4PackedBytes + 256u) + i * bn * 256, bn, rq, ch, lane);
-          };
-          GvFrag<NB> fa, fb;  // two fragment sets: block i+1 loads while block i computes
-          ld(fa, 0);
-          for (int i = 0; i < len; i += 2) {
-            if (i + 1 < len) ld(fb, i + 1);
-            gv_math<NB>(fa, acc);
-            if (i + 1 < len) {
-              if (i + 2 < len) ld(fa, i + 2);
-              gv_math<NB>(fb, acc);
-            }
-          }
-        }
-#endif
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
-        u += len;
-        if (++slot == stages) {
-          slot = 0;
-          phase ^= 1;
-        }
-      }
-      if (threadIdx.x == 0 && u == u1) SUN_STAMP(3);  // last stage consumed
-      // fragments -> T[row][batch]: row 32 rq + 16 m + g (+8), batch 8 j + t (c0) / 8 j + t + 4 (c1)
-      // (gv_nrow of columns 2t, 2t+1); columns >= 8 NB are zero. Chunk 0's warps store,
-      // chunks 1..3 add in order (fixed summation order).
-      gv_bar();  // the previous segment's epilogue is done with T
-      for (int cc = 0; cc < 4; ++cc) {
-        if (ch == cc) {
-#pragma unroll
-          for (int m = 0; m < kGvMT; ++m) {
-            const int r = 32 * rq + 16 * m + g;
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              const int jj = j < NB ? j : 0;
-              const bool have = j < NB;
-              float* p0 = T + r * kGvTPitch + 8 * j + t;
-              float* p1 = T + (r + 8) * kGvTPitch + 8 * j + t;
-              const float v0 = have ? acc[m][jj][0] : 0.f, v1 = have ? acc[m][jj][1] : 0.f;
-              const float v2 = have ? acc[m][jj][2] : 0.f, v3 = have ? acc[m][jj][3] : 0.f;
-              if (cc == 0) {
-                p0[0] = v0; p0[4] = v1; p1[0] = v2; p1[4] = v3;
-              } else {
-                p0[0] += v0; p0[4] += v1; p1[0] += v2; p1[4] += v3;
-              }
-            }
-          }
-        }
-        gv_bar();
-      }
-      bool run_epi = whole;
-      if (!whole) {
-        // park the partial: [c][128 rows][16] fp32, 8 floats per thread (split schedule:
-        // one segment per CTA)
-        const int pslot = 0;
-        const int tid = threadIdx.x & 255, row = tid >> 1, h = (tid & 1) * 8;
-        const bool mover = threadIdx.x < 256;  // 8 floats each
-        if (mover) {
-          float* dst = a.sk_part + (static_cast<long long>(c) * 2 + pslot) * (kTileM * 16) + row * 16 + h;
-          __stcg(reinterpret_cast<float4*>(dst), make_float4(T[row * kGvTPitch + h], T[row * kGvTPitch + h + 1],
-                                                             T[row * kGvTPitch + h + 2], T[row * kGvTPitch + h + 3]));
-          __stcg(reinterpret_cast<float4*>(dst + 4), make_float4(T[row * kGvTPitch + h + 4], T[row * kGvTPitch + h + 5],
-                                                                 T[row * kGvTPitch + h + 6], T[row * kGvTPitch + h + 7]));
-          __threadfence();
-        }
-        gv_bar();
-        const int cf = tile * S, cl = tile * S + S - 1;
-        if (threadIdx.x == 0) {
-          const unsigned old = atomicAdd(a.sk_flags + tile, 1u);
-          *flag = (old == static_cast<unsigned>(cl - cf)) ? 1 : 0;
-        }
-        gv_bar();
-        run_epi = *flag != 0;
-        if (run_epi && mover) {  // last contributor: sum the tile's partials in CTA order
-          __threadfence();
-          float s8[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) s8[e] = 0.f;
-          for (int c0 = cf; c0 <= cl; c0 += 4) {  // four partials' loads in flight per round trip
-            float4 p[4][2];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float* src = a.sk_part + static_cast<long long>(c0 + e <= cl ? c0 + e : cl) * 2 * (kTileM * 16) +
-                                 row * 16 + h;
-              p[e][0] = __ldcg(reinterpret_cast<const float4*>(src));
-              p[e][1] = __ldcg(reinterpret_cast<const float4*>(src + 4));
-            }
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              if (c0 + e > cl) break;
-              s8[0] += p[e][0].x; s8[1] += p[e][0].y; s8[2] += p[e][0].z; s8[3] += p[e][0].w;
-              s8[4] += p[e][1].x; s8[5] += p[e][1].y; s8[6] += p[e][1].z; s8[7] += p[e][1].w;
-            }
-          }
-#pragma unroll
-          for (int e = 0; e < 8; ++e) T[row * kGvTPitch + h + e] = s8[e];
-          if (threadIdx.x == 0) a.sk_flags[tile] = 0u;  // self-resetting for the next launch
-        }
-        if (run_epi) gv_bar();
-      }
-      if (run_epi && warp >= 2 && warp < 6) {
-        const int q = warp & 3;
-        const int row_local = q * 32 + lane;
-        float v[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = T[row_local * kGvTPitch + j];
-        epi_chunk<EPI>(a, tile, row_local, 0, v, epi);
-      }
-    }
+    gv_consume<EPI, NB>(a, u0, u1, m, stages, slot, phase, [] { pdl_wait(); });
   }
   if (threadIdx.x == 64) SUN_STAMP(5);  // (epilogue warp) last epilogue done
   if (threadIdx.x == 0) SUN_STAMP(6);
   tl_end(a.tl, a.tl_idx);
+}
+
+// ---------------------------------------------------------------------------
+// Small-batch QSUN layer chain: O -> gate_up -> down -> next layer's QKV as GEMV phases of
+// one persistent launch (one CTA per SM, all resident). The ring and its producer run across
+// the phase boundaries: the next phase's weight and scale stages stream in while the compute
+// warps finish the current phase's tail, so a boundary costs the tail and a grid-wide count
+// (every CTA adds 1 after its last epilogue of a phase; the next phase's activation copies
+// and epilogue metadata wait for count >= G x phase), not a launch, a ring ramp and a cold
+// first stage per GEMM. Same split-K partials / tile counters as the separate launches.
+// ---------------------------------------------------------------------------
+constexpr int kGvChainMaxPhases = 4;
+struct GvChainArgs {
+  GemmArgs ph[kGvChainMaxPhases];  // O (RESID_ADD), gate_up (SWIGLU), down (RESID_ADD), next QKV (QKV_ROPE)
+  int nph;
+  unsigned* bar;  // [2]: phases completed x CTAs, CTAs exited (zeroed once, self-resetting)
+  int pre;        // stages of a phase p >= 1 whose weights are issued before its grid count: deeper
+                  // prefetch saturates the HBM under the previous phase's tail round trips
+  unsigned long long* stamps;  // profiling: per CTA [16] = per phase p: [4p] gate passed, [4p+1] first
+                               // stage landed, [4p+2] last stage consumed, [4p+3] phase done
+  unsigned long long* tl;
+  int tl_idx;
+};
+
+SUN_DEVICE void gv_wait_count(const unsigned* bar, unsigned target) {
+  if (target == 0) return;
+  const unsigned long long t0 = gtimer();
+  while (ld_acquire_u32(bar) < target) {
+    __nanosleep(64);
+    if (gtimer() - t0 > 2000000000ull) __trap();  // a grid that cannot become resident fails, not hangs
+  }
+}
+
+template <int NB>
+__global__ void __launch_bounds__(kGvThreads, 1) gemv_chain_w4_kernel(const __grid_constant__ GvChainArgs c) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  tl_begin(c.tl, c.tl_idx);
+  const GemmArgs& a0 = c.ph[0];
+  const int stages = a0.stages;
+  const GvSmem m = gv_smem(smem, stages, gv_stage_bytes(a0.bn, a0.wgroup));
+  const int warp = warp_id_sync();
+  const int G = static_cast<int>(gridDim.x), cta = static_cast<int>(blockIdx.x);
+  gv_init_ring(m, stages);
+  pdl_launch_dependents();
+  int slot = 0, phase = 0;
+  if (warp == kGvWarps) {
+    if (elect_one()) {
+      for (int p = 0; p < c.nph; ++p) {
+        int u0, u1;
+        gv_range(c.ph[p], cta, G, u0, u1);
+        const unsigned target = static_cast<unsigned>(G * p);
+        gv_produce(c.ph[p], u0, u1, m, stages, slot, phase, [&] {
+          if (p == 0) pdl_wait();
+          else gv_wait_count(c.bar, target);
+        }, p == 0 ? kGvMaxStages : c.pre);
+      }
+    }
+  } else {
+    for (int p = 0; p < c.nph; ++p) {
+      const GemmArgs& a = c.ph[p];
+      int u0, u1;
+      gv_range(a, cta, G, u0, u1);
+      const unsigned target = static_cast<unsigned>(G * p);
+      auto gate = [&] {
+        if (p == 0) {
+          pdl_wait();
+        } else {
+          if (threadIdx.x == 0) gv_wait_count(c.bar, target);
+          gv_bar();
+        }
+      };
+      unsigned long long* pst = c.stamps ? c.stamps + cta * 16 + 4 * p : nullptr;
+      if (p == 1) gv_consume<EPI_SWIGLU, NB>(a, u0, u1, m, stages, slot, phase, gate, pst);
+      else if (p == 3) gv_consume<EPI_QKV_ROPE, NB>(a, u0, u1, m, stages, slot, phase, gate, pst);
+      else gv_consume<EPI_RESID_ADD, NB>(a, u0, u1, m, stages, slot, phase, gate, pst);
+      gv_bar();  // every epilogue store of this CTA's phase-p work is issued
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(c.bar, 1u);
+        if (pst) pst[3] = gtimer();
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(c.bar + 1, 1u) == static_cast<unsigned>(G - 1)) {  // last CTA out rearms
+    c.bar[0] = 0u;
+    c.bar[1] = 0u;
+  }
+  tl_end(c.tl, c.tl_idx);
 }
 
 }  // namespace sun

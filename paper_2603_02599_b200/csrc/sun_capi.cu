@@ -203,6 +203,8 @@ void init_kernel_attrs() {
     set_max_smem(gemv_w4_kernel<EPI_QKV_ROPE, 2>);
     set_max_smem(gemv_w4_kernel<EPI_SWIGLU, 1>);
     set_max_smem(gemv_w4_kernel<EPI_SWIGLU, 2>);
+    set_max_smem(gemv_chain_w4_kernel<1>);
+    set_max_smem(gemv_chain_w4_kernel<2>);
     set_max_smem(gemm_chain_kernel);
     set_max_smem(gemm_chain_w4_kernel);
     set_max_smem(attn_group_kernel<64>);
@@ -707,6 +709,42 @@ SunStatus run_gemv_w4(const void* packed, const void* scales, GemmArgs a, const 
   return SUN_OK;
 }
 
+// Small-batch QSUN layer chain (gemv_chain_w4_kernel): the W4 GEMV phases O -> gate_up ->
+// down -> next QKV in one persistent launch of one CTA per SM (all resident: 1 x ~222 KB).
+SunStatus run_gemv_chain_w4(GemmArgs* ph, const GemmPlan* plans, const void* const* packed,
+                            const void* const* scales, int nph, float* part, unsigned* cnt, unsigned* bar,
+                            cudaStream_t st, bool pdl, int num_sms) {
+  GvChainArgs c;
+  memset(&c, 0, sizeof(c));
+  const int bn = ph[0].bn;
+  if (bn != 16 || ph[0].batch > kGemvKernelMaxBatch) return fail(SUN_ERR_VALUE, "W4 GEMV chain takes <= 16 rows");
+  const GvCfg g = gv_cfg(bn);
+  const int G = std::min(num_sms, kMaxGemmCtas);
+  for (int i = 0; i < nph; ++i) {
+    GemmArgs a = ph[i];
+    if (plans[i].m_tiles > kGvMaxTiles) return fail(SUN_ERR_UNSUPPORTED, "W4 GEMV chain: too many tiles");
+    a.w4_packed = static_cast<const uint8_t*>(packed[i]);
+    a.w4_scales = static_cast<const __nv_bfloat16*>(scales[i]);
+    a.wgroup = g.kbs;
+    a.stages = g.stages;
+    a.sk_units = 0;
+    a.sk_part = part;
+    a.sk_flags = cnt;
+    a.splits = plans[i].m_tiles >= G ? 0 : std::max(1, std::min(plans[i].ksteps, G / plans[i].m_tiles));
+    c.ph[i] = a;
+  }
+  c.nph = nph;
+  c.bar = bar;
+  static const int pre_env = [] { const char* e = getenv("SUN_GVC_PRE"); return e ? atoi(e) : 2; }();
+  c.pre = pre_env;
+  tl_assign(c);
+  if (g_tl.stamps != nullptr && c.tl != nullptr && c.tl_idx == g_tl.stamp_idx) c.stamps = g_tl.stamps;
+  g_cluster = 1;
+  if (ph[0].batch <= 8) SUN_CUDA(launch(gemv_chain_w4_kernel<1>, dim3(G), dim3(kGvThreads), g.smem, st, pdl, c));
+  else SUN_CUDA(launch(gemv_chain_w4_kernel<2>, dim3(G), dim3(kGvThreads), g.smem, st, pdl, c));
+  return SUN_OK;
+}
+
 // Layer GEMM chain (bf16): the phases' GemmArgs are filled as for run_gemm; every
 // split phase reduces through L2 over 148 persistent CTAs. Used by default for
 // decode batches (SUN_STEP_DISTINCT_ROWS; measured C2 1.65 -> 1.59 ms, C3 5.03 ->
@@ -1173,8 +1211,12 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     produce_norm(a, l + 1 < d.n_layers ? dec->layers[l + 1].attn_norm : dec->w.final_norm);
     return a;
   };
-  const bool gemv = use_gemv(w4, batch);  // QSUN small batches: W4 GEMV launches, no chain
-  const bool chain = !gemv && use_chain(flags, w4, bn) && (w4 ? dec->chain_w4_ok : dec->chain_ok);
+  // QSUN small batches: the W4 GEMV, as separate launches (default) or as the GEMV layer
+  // chain (SUN_W4_GEMV_CHAIN=1: measured slower, 2.56 vs 2.36 ms at B=1 — the split phases'
+  // L2 reduction tails, 7-10 us, bound each phase either way and the chain adds the grid count)
+  static const int gvchain_env = [] { const char* e = getenv("SUN_W4_GEMV_CHAIN"); return e ? atoi(e) : 0; }();
+  const bool gemv = use_gemv(w4, batch);
+  const bool chain = use_chain(flags, w4, bn) && (gemv ? gvchain_env != 0 : (w4 ? dec->chain_w4_ok : dec->chain_ok));
   auto w4_gemm = [&](auto epi_tag, const void* pk, const void* sc, const GemmArgs& ga, const GemmPlan& p) {
     constexpr int E = decltype(epi_tag)::value;
     return gemv ? run_gemv_w4<E>(pk, sc, ga, p, dec->gv_part, dec->gv_cnt, st, pdl, dec->num_sms)
@@ -1209,8 +1251,10 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
         sc[3] = dec->layers[l + 1].s_qkv;
         nph = 4;
       }
-      s = w4 ? run_chain_w4(ph, epi, plans, wb, sc, nph, dec->chain_bar, st, pdl, dec->num_sms)
-             : run_chain(ph, epi, plans, wb, nph, dec->chain_bar, st, pdl, dec->num_sms);
+      s = gemv ? run_gemv_chain_w4(ph, plans, wb, sc, nph, dec->gv_part, dec->gv_cnt, dec->chain_bar, st, pdl,
+                                   dec->num_sms)
+          : w4 ? run_chain_w4(ph, epi, plans, wb, sc, nph, dec->chain_bar, st, pdl, dec->num_sms)
+               : run_chain(ph, epi, plans, wb, nph, dec->chain_bar, st, pdl, dec->num_sms);
       if (s != SUN_OK) return s;
       continue;
     }

@@ -39,10 +39,12 @@ def uses_w4_gemv(weight_bits: int, batch: int, env: str | None = None) -> bool:
 
 def uses_gemm_chain(weight_bits: int, distinct_rows: bool, env: str | None, batch: int = 1) -> bool:
     """Whether sun_decode_step runs the persistent layer GEMM chain (mirrors
-    sun_capi.cu use_chain): decode batches by default (QSUN: up to 128 rows),
-    SUN_GEMM_CHAIN=0/1 forces."""
-    if weight_bits == 4 and ((batch + 15) // 16 * 16 > W4_CHAIN_MAX_BATCH or uses_w4_gemv(4, batch)):
+    sun_capi.cu use_chain): decode batches by default (QSUN: 9..128 rows; at <= 8 rows the
+    W4 GEMV's separate launches unless SUN_W4_GEMV_CHAIN=1), SUN_GEMM_CHAIN=0/1 forces."""
+    if weight_bits == 4 and (batch + 15) // 16 * 16 > W4_CHAIN_MAX_BATCH:
         return False
+    if uses_w4_gemv(weight_bits, batch) and os.environ.get("SUN_W4_GEMV_CHAIN", "0") in ("", "0"):
+        return False  # the W4 GEMV's separate launches (its chain is opt-in)
     if env is not None:
         try:
             return int(env) == 1
@@ -172,8 +174,8 @@ class _StepRunner:
         ran unsplit (combine=False)."""
         combine = (not self.fused_combine) if combine is None else combine
         batch = self.max_batch if batch is None else batch
-        chain = self.gemm_chain and (self.spec.weight_bits == 16 or (
-            (batch + 15) // 16 * 16 <= W4_CHAIN_MAX_BATCH and not uses_w4_gemv(4, batch)))
+        # (the decoder's flag, then this batch width's W4 rules)
+        chain = self.gemm_chain and uses_gemm_chain(self.spec.weight_bits, True, "1", batch)
         names = ["embed_norm"]
         if chain:  # O -> gate_up -> down -> next QKV as one launch per layer
             names.append("gemm_qkv_rope_kv")

@@ -177,5 +177,5 @@ def test_step_flags_and_chain_selection():
 
     assert uses_w4_gemv(4, 8, None) and not uses_w4_gemv(4, 9, None) and not uses_w4_gemv(16, 1, None)
     assert not uses_w4_gemv(4, 1, "0") and uses_w4_gemv(4, 1, "1")
-    if os.environ.get("SUN_W4_GEMV", "1") != "0":
+    if os.environ.get("SUN_W4_GEMV", "1") != "0" and os.environ.get("SUN_W4_GEMV_CHAIN", "0") == "0":
         assert not uses_gemm_chain(4, True, None, batch=8) and uses_gemm_chain(4, True, None, batch=9)
