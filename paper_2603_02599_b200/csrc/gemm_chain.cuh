@@ -120,6 +120,36 @@ SUN_DEVICE void chain_epilogue_phase(const GemmArgs& a, const PhaseSched& ps, fl
   const int KS = a.ksteps;
   if (warp < 6) load_qkv_meta<EPI>(a, epi);
   epi_pair_bar();
+  // Residual-phase inputs that do not depend on this phase's result — the previous
+  // residual of the columns this group will finish and the next norm's gain — are copied
+  // into the group's staging area with cp.async now, while the phase's MMAs run (no
+  // registers held: the register preload measured slower through spills); the tail then
+  // reads shared memory instead of paying a global round trip under a saturated HBM.
+  // Hardware-cluster split phases with one 8-column chunk per group (O / down at bn <= 64).
+  const float* pre_res = nullptr;
+  float pre_gain = 0.f;
+  if constexpr (EPI == EPI_RESID_ADD) {
+#ifndef SUN_NO_RESPRE  // (A/B build switch)
+    if (ps.nseg == 1 && ps.S > 1 && !a.vcluster && a.norm_w != nullptr &&
+        (a.bn / 16 - ps.rank + ps.S - 1) / ps.S == 1) {
+      float* dst = epi_stage(epi);  // [8 columns][128 rows]; the ss scratch sits above 8 KB
+      const int row = ps.t_first * kTileM + row_local;
+      const int c0 = ps.rank * 16 + 8 * epi_grp();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (row < a.n_out && c0 + j < a.batch)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst + j * kTileM + row_local)),
+                       "l"(a.out_f32 + static_cast<long long>(c0 + j) * a.ldo + row)
+                       : "memory");
+        else
+          dst[j * kTileM + row_local] = 0.f;
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      pre_gain = row < a.n_out ? __bfloat162float(a.norm_w[row]) : 0.f;
+      pre_res = dst + row_local;
+    }
+#endif
+  }
   for (int seg = 0; seg < ps.nseg; ++seg) {
     const int tile = ps.t_first + seg;
     mbar_wait(&tfull[buf], tphase);
@@ -185,7 +215,12 @@ SUN_DEVICE void chain_epilogue_phase(const GemmArgs& a, const PhaseSched& ps, fl
         tc_fence_before();
         epi_pair_bar();
         if (epi_lead_thread()) mbar_arrive(&tempty[buf]);  // accumulator read: the MMA may reuse it
-        epi_chunk<EPI, 8>(a, tile, row_local, rank * 16 + 8 * epi_grp(), v, epi);
+        if (pre_res != nullptr) {
+          asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's own prefetched values
+          epi_chunk<EPI, 8>(a, tile, row_local, rank * 16 + 8 * epi_grp(), v, epi, pre_res, &pre_gain, kTileM);
+        } else {
+          epi_chunk<EPI, 8>(a, tile, row_local, rank * 16 + 8 * epi_grp(), v, epi);
+        }
       } else {
         for (int c = rank + S * epi_grp(); c < nch; c += 2 * S) {
           float v[16];
@@ -500,7 +535,8 @@ SUN_DEVICE void chain_wait_mbar_cluster(uint64_t* bar, uint32_t parity) {  // ac
 template <int EPI>
 SUN_DEVICE void w4_chain_segment(const GemmArgs& a, const PhaseSched& ps, int tile, uint32_t taddr, float* epi,
                                  uint64_t* tempty_buf, float* park, uint64_t* pbar,
-                                 unsigned long long* seg_stamps = nullptr) {
+                                 unsigned long long* seg_stamps = nullptr, const float* pre_res = nullptr,
+                                 const float* pre_gain = nullptr) {
   SUN_SEGSTAMP(12);
   const int q = static_cast<int>(threadIdx.x >> 5) & 3;
   const int row_local = q * 32 + (threadIdx.x & 31);
@@ -563,10 +599,17 @@ SUN_DEVICE void w4_chain_segment(const GemmArgs& a, const PhaseSched& ps, int ti
           v[4 * j + 3] += x[u][j].w;
         }
     };
-    for (int c0 = rank * 16; c0 < a.bn; c0 += S * 16) {
+    int k = 0;
+    for (int c0 = rank * 16; c0 < a.bn; c0 += S * 16, ++k) {
       float v[16];
       reduce_cols(c0, 0, v);
-      epi_chunk<EPI>(a, tile, row_local, c0, v, epi);
+      if (pre_res != nullptr) {
+        asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's own prefetched values
+        // chunk k's residual columns: group A's staging area (k = 0) or group B's (k = 1)
+        epi_chunk<EPI>(a, tile, row_local, c0, v, epi, pre_res + k * (kEpiGroupBytes / 4), pre_gain, kTileM);
+      } else {
+        epi_chunk<EPI>(a, tile, row_local, c0, v, epi);
+      }
     }
     bar();
     SUN_SEGSTAMP(15);
@@ -631,9 +674,12 @@ SUN_DEVICE void w4_chain_segment(const GemmArgs& a, const PhaseSched& ps, int ti
 }
 
 SUN_DEVICE void w4_segment(int epi_kind, const GemmArgs& a, const PhaseSched& ps, int tile, uint32_t taddr, float* epi,
-                           uint64_t* tempty_buf, float* park, uint64_t* pbar, unsigned long long* seg_stamps) {
+                           uint64_t* tempty_buf, float* park, uint64_t* pbar, unsigned long long* seg_stamps,
+                           const float* pre_res = nullptr, const float* pre_gain = nullptr) {
   switch (epi_kind) {
-    case EPI_RESID_ADD: w4_chain_segment<EPI_RESID_ADD>(a, ps, tile, taddr, epi, tempty_buf, park, pbar, seg_stamps); break;
+    case EPI_RESID_ADD:
+      w4_chain_segment<EPI_RESID_ADD>(a, ps, tile, taddr, epi, tempty_buf, park, pbar, seg_stamps, pre_res, pre_gain);
+      break;
     case EPI_SWIGLU: w4_chain_segment<EPI_SWIGLU>(a, ps, tile, taddr, epi, tempty_buf, park, pbar); break;
     case EPI_QKV_ROPE: w4_chain_segment<EPI_QKV_ROPE>(a, ps, tile, taddr, epi, tempty_buf, park, pbar); break;
     default: __trap();
@@ -853,12 +899,43 @@ __global__ void __launch_bounds__(kW4Threads, 1) gemm_chain_w4_kernel(const __gr
         case EPI_QKV_ROPE: load_qkv_meta<EPI_QKV_ROPE>(a, epi); break;
         default: __trap();
       }
+      // Residual-phase inputs that do not depend on this phase's result (the previous
+      // residual of this rank's columns, the next norm's gain) into both epilogue staging
+      // areas with cp.async while the phase's MMAs run (hardware-cluster split phases with
+      // up to two 16-column chunks per rank, one segment): the tail reads shared memory
+      // instead of paying a global round trip under a saturated HBM.
+      const float* pre_res = nullptr;
+      float pre_gain = 0.f;
+#ifndef SUN_NO_RESPRE  // (A/B build switch)
+      if (c.epi[p] == EPI_RESID_ADD && ps.nseg == 1 && ps.S > 1 && !a.vcluster && a.norm_w != nullptr &&
+          (a.bn / 16 - ps.rank + ps.S - 1) / ps.S <= 2) {
+        const int row_local = (warp & 3) * 32 + (threadIdx.x & 31);
+        const int row = ps.t_first * kTileM + row_local;
+        float* base = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(epi) + 3072);  // group A | group B staging
+        int k = 0;
+        for (int c0 = ps.rank * 16; c0 < a.bn; c0 += ps.S * 16, ++k) {
+          float* dst = base + k * (kEpiGroupBytes / 4);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (row < a.n_out && c0 + j < a.batch)
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst + j * kTileM + row_local)),
+                           "l"(a.out_f32 + static_cast<long long>(c0 + j) * a.ldo + row)
+                           : "memory");
+            else
+              dst[j * kTileM + row_local] = 0.f;
+          }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        pre_gain = row < a.n_out ? __bfloat162float(a.norm_w[row]) : 0.f;
+        pre_res = base + row_local;
+      }
+#endif
       for (int seg = 0; seg < ps.nseg; ++seg) {
         mbar_wait(&tfull[buf], tphase);
         tc_fence_after();
         const uint32_t taddr = tmem_base + static_cast<uint32_t>(buf * bn) + (static_cast<uint32_t>((warp & 3) * 32) << 16);
         w4_segment(c.epi[p], a, ps, ps.t_first + seg, taddr, epi, &tempty[buf], park, &pbar[p],
-                   p == 0 ? c.stamps : nullptr);
+                   p == 0 ? c.stamps : nullptr, pre_res, &pre_gain);
         if (++buf == 2) {
           buf = 0;
           tphase ^= 1;

@@ -209,7 +209,7 @@ SUN_DEVICE float* epi_stage(float* epi) {
 
 template <int EPI, int NC = 16>  // NC: columns in this chunk (16, or 8 for a half chunk)
 SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, float (&v)[NC], float* epi,
-                          const float* pre0 = nullptr, const float* pre1 = nullptr) {
+                          const float* pre0 = nullptr, const float* pre1 = nullptr, int pstride = 1) {
   const int row = m_tile * kTileM + row_local;
   const int B = a.batch;
   float* stage_f32 = epi_stage(epi);
@@ -228,7 +228,7 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
         float* base = a.out_f32 + static_cast<long long>(c0) * a.ldo + row;
         float old[NC];
 #pragma unroll
-        for (int j = 0; j < NC; ++j) old[j] = pre0 ? pre0[j] : ((in && c0 + j < B) ? base[j * a.ldo] : 0.f);
+        for (int j = 0; j < NC; ++j) old[j] = pre0 ? pre0[j * pstride] : ((in && c0 + j < B) ? base[j * a.ldo] : 0.f);
         const float g = pre1 ? pre1[0] : (in ? __bfloat162float(a.norm_w[row]) : 0.f);
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
@@ -267,7 +267,7 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
         // issue all 16 residual loads before any store (one memory round trip)
         float old[NC];
 #pragma unroll
-        for (int j = 0; j < NC; ++j) old[j] = pre0 ? pre0[j] : ((c0 + j < B) ? base[j * a.ldo] : 0.f);
+        for (int j = 0; j < NC; ++j) old[j] = pre0 ? pre0[j * pstride] : ((c0 + j < B) ? base[j * a.ldo] : 0.f);
 #pragma unroll
         for (int j = 0; j < NC; ++j)
           if (c0 + j < B) base[j * a.ldo] = old[j] + v[j];
