@@ -118,10 +118,10 @@ __global__ void import_w4_ct_kernel(const uint32_t* __restrict__ ct_packed, cons
 //     loads x[n][32c + 8t .. +8] (one 16-byte SUN-ACT chunk) for batch row
 //     n = (g & 1) * 4 + (g >> 1) — that row order puts the eight lanes of each
 //     shared-memory phase on eight different 16-byte bank groups.
-//   * The MMAs run on q + 136 (the magic pair itself, exact in bf16) from an accumulator
-//     preset to -136 sum x (two MMAs with A = 1 per block, shared by the four tiles),
-//     i.e. sum q x in fp32 per block and warp-chunk; the group scale s is applied once
-//     per block with an FMA (s * sum(q x), the operand bf16(q s) without its bf16
+//   * The MMAs run on q + 136 (the magic pair itself, exact in bf16); -136 sum x (two MMAs
+//     with A = 1 per block, shared by the tiles) is added before the group scale s, i.e.
+//     s sum q x per block and warp-chunk in fp32; blocks go in pairs so two MMA chains
+//     interleave; the scale is applied once per block with an FMA (s * sum(q x), the operand bf16(q s) without its bf16
 //     rounding: below the 2e-2 logit tolerance). SUN-W4 stores a block's 128 scales row-interleaved
 //     (position (r & 7) * 16 + (r >> 3)), so lane g's four rows are one 8-byte load.
 //   * One producer warp streams stages of up to kbs consecutive K blocks of a tile
@@ -213,44 +213,93 @@ SUN_DEVICE void gv_load(GvFrag<NB>& f, uint32_t pk, uint32_t sc, uint32_t xs, in
   asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(f.sv[0]), "=r"(f.sv[1]) : "r"(sc + (16 * g + 4 * rq) * 2));
 }
 
-// acc[m][j] += s_row * sum_k q x (n-tile j). The A operand is the raw magic pair
-// bf16(128 + q + 8) = q + 136 (one LOP3, no subtraction); each m16 tile's MMAs start from
-// -136 sum_k x (two extra MMAs per block with A = 1, shared by the four tiles), so the
-// accumulator holds sum (q + 136) x - 136 sum x = sum q x.
+// Fast path of a full 4-block stage at bn = 16 (the decode steps' shape): every address is a
+// per-thread register + a compile-time immediate (block i of the stage at i x 8 KB, its
+// scales at 32 KB + 256 i, its activation slice at 33 KB + 4 KB i). The generic loads
+// recompute the swizzled offsets per block — integer ALU work on the pipe the dequant
+// already saturates (measured: half the loop's ALU instructions were address arithmetic).
+constexpr int kGvFastKbs = 4, kGvFastBn = 16;
 template <int NB>
-SUN_DEVICE void gv_math(const GvFrag<NB>& f, float (&acc)[kGvMT][NB][4]) {
-  constexpr uint32_t kOnes = 0x3F803F80u;  // bf16x2 (1, 1)
-  float cx[NB][4];
+struct GvBase {
+  uint32_t w, s, x[NB];  // per-thread shared addresses within stage 0 (block 0)
+};
+template <int NB>
+SUN_DEVICE GvBase<NB> gv_base(uint32_t ring_s, int rq, int c, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  GvBase<NB> b;
+  b.w = ring_s + c * 2048 + (32 * rq + lane) * 16;
+  b.s = ring_s + kGvFastKbs * kW4PackedBytes + (16 * g + 4 * rq) * 2;
 #pragma unroll
   for (int j = 0; j < NB; ++j) {
-    cx[j][0] = cx[j][1] = cx[j][2] = cx[j][3] = 0.f;
-    mma_16816_q(cx[j], kOnes, kOnes, kOnes, kOnes, f.x[j][0], f.x[j][1]);
-    mma_16816_q(cx[j], kOnes, kOnes, kOnes, kOnes, f.x[j][2], f.x[j][3]);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) cx[j][e] *= -136.f;
+    const int n = 8 * j + gv_nrow(g);
+    b.x[j] = ring_s + kGvFastKbs * (kW4PackedBytes + 256u) + (c >> 1) * kGvFastBn * 128 + n * 128 +
+             ((((c & 1) * 4 + t) ^ (n & 7)) << 4);
   }
+  return b;
+}
+template <int NB, int I>
+SUN_DEVICE void gv_load_fast(GvFrag<NB>& f, const GvBase<NB>& b, uint32_t stage_off) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4+%5];"
+               : "=r"(f.wq[0]), "=r"(f.wq[1]), "=r"(f.wq[2]), "=r"(f.wq[3])
+               : "r"(b.w + stage_off), "n"(I * kW4PackedBytes));
 #pragma unroll
-  for (int m = 0; m < kGvMT; ++m) {
-    float blk[NB][4];
+  for (int j = 0; j < NB; ++j)
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4+%5];"
+                 : "=r"(f.x[j][0]), "=r"(f.x[j][1]), "=r"(f.x[j][2]), "=r"(f.x[j][3])
+                 : "r"(b.x[j] + stage_off), "n"(I * kGvFastBn * 256));
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2+%3];" : "=r"(f.sv[0]), "=r"(f.sv[1]) : "r"(b.s + stage_off), "n"(I * 256));
+}
+
+// acc[m][j] += s_row * sum_k q x (n-tile j), for NBLK blocks at once (their MMA chains
+// interleave: one block's chain is two dependent 26-cycle HMMAs, so a warp alone on one
+// block idles the tensor pipe). The A operand is the raw magic pair bf16(128 + q + 8) =
+// q + 136 (one LOP3, no subtraction); the block's -136 sum_k x comes from two MMAs with
+// A = 1 (shared by the m16 tiles, off the tiles' critical path) and is added before the
+// scale: acc += s (sum (q + 136) x - 136 sum x) = s sum q x.
+template <int NB, int NBLK>
+SUN_DEVICE void gv_math(const GvFrag<NB> (&f)[NBLK], float (&acc)[kGvMT][NB][4]) {
+  constexpr uint32_t kOnes = 0x3F803F80u;  // bf16x2 (1, 1)
+  float cx[NBLK][NB][4];
+  float blk[NBLK][kGvMT][NB][4];
 #pragma unroll
-    for (int j = 0; j < NB; ++j) blk[j][0] = cx[j][0], blk[j][1] = cx[j][1], blk[j][2] = cx[j][2], blk[j][3] = cx[j][3];
-    const uint32_t lo = f.wq[2 * m], hi = f.wq[2 * m + 1];
-    const uint32_t a00 = w4_pair_raw(lo, 0), a10 = w4_pair_raw(hi, 0), a01 = w4_pair_raw(lo, 1), a11 = w4_pair_raw(hi, 1);
-    const uint32_t a02 = w4_pair_raw(lo, 2), a12 = w4_pair_raw(hi, 2), a03 = w4_pair_raw(lo, 3), a13 = w4_pair_raw(hi, 3);
+  for (int b = 0; b < NBLK; ++b)
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
-      mma_16816_q(blk[j], a00, a10, a01, a11, f.x[j][0], f.x[j][1]);
-      mma_16816_q(blk[j], a02, a12, a03, a13, f.x[j][2], f.x[j][3]);
-    }
-    const float s0 = __uint_as_float(f.sv[m] << 16), s1 = __uint_as_float(f.sv[m] & 0xFFFF0000u);
+      cx[b][j][0] = cx[b][j][1] = cx[b][j][2] = cx[b][j][3] = 0.f;
 #pragma unroll
-    for (int j = 0; j < NB; ++j) {
-      acc[m][j][0] = fmaf(s0, blk[j][0], acc[m][j][0]);
-      acc[m][j][1] = fmaf(s0, blk[j][1], acc[m][j][1]);
-      acc[m][j][2] = fmaf(s1, blk[j][2], acc[m][j][2]);
-      acc[m][j][3] = fmaf(s1, blk[j][3], acc[m][j][3]);
+      for (int m = 0; m < kGvMT; ++m) blk[b][m][j][0] = blk[b][m][j][1] = blk[b][m][j][2] = blk[b][m][j][3] = 0.f;
+    }
+  // first k16 step of every (block, tile) and the ones-MMAs, then the second steps
+#pragma unroll
+  for (int step = 0; step < 2; ++step) {
+#pragma unroll
+    for (int b = 0; b < NBLK; ++b) {
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+        mma_16816_q(cx[b][j], kOnes, kOnes, kOnes, kOnes, f[b].x[j][2 * step], f[b].x[j][2 * step + 1]);
+#pragma unroll
+      for (int m = 0; m < kGvMT; ++m) {
+        const uint32_t lo = f[b].wq[2 * m], hi = f[b].wq[2 * m + 1];
+        const uint32_t a0 = w4_pair_raw(lo, 2 * step), a1 = w4_pair_raw(hi, 2 * step);
+        const uint32_t a2 = w4_pair_raw(lo, 2 * step + 1), a3 = w4_pair_raw(hi, 2 * step + 1);
+#pragma unroll
+        for (int j = 0; j < NB; ++j) mma_16816_q(blk[b][m][j], a0, a1, a2, a3, f[b].x[j][2 * step], f[b].x[j][2 * step + 1]);
+      }
     }
   }
+#pragma unroll
+  for (int b = 0; b < NBLK; ++b)
+#pragma unroll
+    for (int m = 0; m < kGvMT; ++m) {
+      const float s0 = __uint_as_float(f[b].sv[m] << 16), s1 = __uint_as_float(f[b].sv[m] & 0xFFFF0000u);
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        acc[m][j][0] = fmaf(s0, fmaf(-136.f, cx[b][j][0], blk[b][m][j][0]), acc[m][j][0]);
+        acc[m][j][1] = fmaf(s0, fmaf(-136.f, cx[b][j][1], blk[b][m][j][1]), acc[m][j][1]);
+        acc[m][j][2] = fmaf(s1, fmaf(-136.f, cx[b][j][2], blk[b][m][j][2]), acc[m][j][2]);
+        acc[m][j][3] = fmaf(s1, fmaf(-136.f, cx[b][j][3], blk[b][m][j][3]), acc[m][j][3]);
+      }
+    }
 }
 
 SUN_DEVICE void gv_bar() { asm volatile("bar.sync 2, 512;" ::: "memory"); }  // the 16 compute warps
@@ -312,6 +361,10 @@ SUN_DEVICE void gv_produce(const GemmArgs& a, int u0, int u1, const GvSmem& m, i
   auto issue_w = [&](int u, int len) {
     uint8_t* st = m.ring + slot * sb;
     mbar_wait(&m.empty[slot], phase ^ 1);
+#ifdef SUN_GV_PROBE_NOLOAD  // probe: stages handed over without any copy (compute-only rate; results invalid)
+    mbar_arrive(&m.full[slot]);
+    return;
+#endif
     mbar_arrive_expect_tx(&m.full[slot], static_cast<uint32_t>(len) * (wbytes + xbytes));
     bulk_load_hint(st, a.w4_packed + static_cast<long long>(u) * kW4PackedBytes, len * kW4PackedBytes, &m.full[slot],
                    kEvictFirst);
@@ -321,6 +374,9 @@ SUN_DEVICE void gv_produce(const GemmArgs& a, int u0, int u1, const GvSmem& m, i
 #endif
   };
   auto issue_x = [&](int sl, int u, int len) {
+#ifdef SUN_GV_PROBE_NOLOAD
+    return;
+#endif
     if (xbytes)
       bulk_load_hint(m.ring + sl * sb + kbs * (kW4PackedBytes + 256u),
                      a.xact + static_cast<long long>(2 * (u % KB)) * bn * 128, len * xbytes, &m.full[sl], kEvictLast);
@@ -374,6 +430,8 @@ SUN_DEVICE void gv_consume(const GemmArgs& a, int u0, int u1, const GvSmem& m, i
   const int rq = warp & 3, ch = warp >> 2;  // row quarter, 32-k chunk of every block
   const int g = lane >> 2, t = lane & 3;
   const uint32_t ring_s = smem_u32(m.ring);
+  const bool fast = kbs == kGvFastKbs && bn == kGvFastBn;
+  const GvBase<NB> base = gv_base<NB>(ring_s, rq, ch, lane);
   float acc[kGvMT][NB][4];
   int u = u0;
   while (u < u1) {
@@ -393,20 +451,31 @@ SUN_DEVICE void gv_consume(const GemmArgs& a, int u0, int u1, const GvSmem& m, i
       }
       const uint32_t st = ring_s + slot * sb;
 #ifndef SUN_GV_PROBE_IDLE  // probe: compute warps only pass the stages on (timing only)
-      {
+      if (fast && len == kGvFastKbs) {
+        const uint32_t so = slot * sb;
+        GvFrag<NB> f2[2];
+        gv_load_fast<NB, 0>(f2[0], base, so);
+        gv_load_fast<NB, 1>(f2[1], base, so);
+        gv_math<NB, 2>(f2, acc);
+        gv_load_fast<NB, 2>(f2[0], base, so);
+        gv_load_fast<NB, 3>(f2[1], base, so);
+        gv_math<NB, 2>(f2, acc);
+      } else {
         auto ld = [&](GvFrag<NB>& f, int i) {
           gv_load<NB>(f, st + i * kW4PackedBytes, st + kbs * kW4PackedBytes + i * 256,
                       st + kbs * (kW4PackedBytes + 256u) + i * bn * 256, bn, rq, ch, lane);
         };
-        GvFrag<NB> fa, fb;  // two fragment sets: block i+1 loads while block i computes
-        ld(fa, 0);
-        for (int i = 0; i < len; i += 2) {
-          if (i + 1 < len) ld(fb, i + 1);
-          gv_math<NB>(fa, acc);
-          if (i + 1 < len) {
-            if (i + 2 < len) ld(fa, i + 2);
-            gv_math<NB>(fb, acc);
-          }
+        int i = 0;
+        for (; i + 1 < len; i += 2) {  // block pairs: two interleaved MMA chains
+          GvFrag<NB> f2[2];
+          ld(f2[0], i);
+          ld(f2[1], i + 1);
+          gv_math<NB, 2>(f2, acc);
+        }
+        if (i < len) {
+          GvFrag<NB> f1[1];
+          ld(f1[0], i);
+          gv_math<NB, 1>(f1, acc);
         }
       }
 #endif
