@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-2 evidence: GPU tests, smoke, every bench config (N=1) + pinned + reference arm,
 # step-time grids (harness closure fixtures), step timelines, ncu launch lists + full
-# captures (C3, C4) -> gpurun_out/ (copied to profiles/r02 by hand).
+# captures (C3, C4) -> gpurun_out/ (copied to profiles/<round> by hand).
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/gpu.txt
@@ -9,7 +9,7 @@ timeout 1500 python -m pytest -q -m gpu tests/ > gpurun_out/pytest_gpu.log 2>&1;
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -2 gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
 timeout 600 python bench.py --routing pinned > gpurun_out/bench_c3_pinned.json 2> gpurun_out/bench_c3_pinned.err
-for c in c1 c2 c4 c5; do timeout 900 python bench.py --config $c --steps 30 --warmup 5 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; done
+for c in c1 c2 c4 c5; do timeout 1500 python bench.py --config $c --steps 30 --warmup 5 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; done
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 900 python scripts/measure_step_grid.py --spec llama3.1-8b --bits 16 --out gpurun_out/b200_steps_8b_bf16.json > gpurun_out/grid16.log 2>&1
 timeout 900 python scripts/measure_step_grid.py --spec llama3.1-8b --bits 4 --out gpurun_out/b200_steps_8b_w4.json > gpurun_out/grid4.log 2>&1
