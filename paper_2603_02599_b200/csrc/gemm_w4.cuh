@@ -94,48 +94,47 @@ __global__ void import_w4_ct_kernel(const uint32_t* __restrict__ ct_packed, cons
 }
 
 // ---------------------------------------------------------------------------
-// Small-batch QSUN GEMV (decode batches of <= 16 rows): D^T = W4 . X^T on the
-// legacy tensor path (mma.sync m16n8k16), dequantised in registers.
+// Small-batch QSUN GEMV (decode steps of <= 8 rows; the kernel takes <= 16): D^T =
+// W4 . X^T on the legacy tensor path (mma.sync m16n8k16), dequantised in registers.
 //
 // At B <= 16 the tcgen05 W4 kernel runs at a batch-independent 0.45-1.5 TB/s
-// (scripts/w4_probe.py: 28672x4096 in 39.9 us at B = 1, 4 and 16): its converter
-// warps' TMEM round trip paces it. Here the packed words go straight into
-// m16n8k16 A fragments. The kernel is shaped by shared-memory bandwidth (measured:
-// with the compute warps idle the ring streams the 8B gate_up at 7.5 TB/s; a first
-// version whose eight row-warps each re-read the activation slice ran at half that):
-//   * Warp w (16 compute warps) owns rows 64 (w & 1) .. +63 of the 128-row tile (four
-//     m16 tiles), one 32-k chunk c = (w >> 1) & 3 and every other K block of a stage
-//     (parity w >> 3), so every packed byte is read from shared memory once, the
-//     activation fragment once per (chunk, row half) and reused by four tiles; four
-//     warps per scheduler hide the HMMA / shared-memory latencies (with two, the warps
-//     issued at IPC ~0.4 and the consumer, not the HBM, paced the ring).
-//   * ldmatrix of the SUN-W4 block [chunk 4][row 128][16 B] as b16 8x8 matrices gives
-//     lane (g, t) word t (k = 32c + 8t .. +7) of row g: one ldmatrix.x4 per block
-//     fetches the warp's four rows-of-8 (conflict-free, rows 16 B apart). A word's bf16
-//     pairs (e0,e1) (e2,e3) (e4,e5) (e6,e7) (LOP3 with the 0x4300 magic: q + 136 as
-//     bf16) fill the A slots (2t,2t+1 | 2t+8,2t+9) of two MMAs; K is permuted
-//     inside an MMA and the activation fragment uses the same permutation: lane (g, t)
-//     loads x[n][32c + 8t .. +8] (one 16-byte SUN-ACT chunk) for batch row
-//     n = (g & 1) * 4 + (g >> 1) — that row order puts the eight lanes of each
+// (scripts/w4_probe.py: 28672x4096 in 39.9 us at B = 1, 4 and 16): its converter warps'
+// TMEM round trip paces it. Here the packed words go straight into MMA A fragments.
+//   * Warp w of 16 compute warps (four per scheduler) owns rows 32 (w & 3) .. +31 of the
+//     128-row tile (two m16 tiles) and the 32-k chunk c = w >> 2 of every 128 x 128 K
+//     block: every packed byte is read from shared memory once, the activation fragment
+//     once per (chunk, row quarter) and reused by both tiles.
+//   * ldmatrix of the SUN-W4 block [chunk 4][row 128][16 B] as b16 8x8 matrices gives lane
+//     (g, t) word t (k = 32c + 8t .. +7) of row g (one x4 per block, conflict-free). A
+//     word's bf16 pairs (e0,e1) (e2,e3) (e4,e5) (e6,e7) — one LOP3 with the 0x4300 magic
+//     each: q + 136, exact in bf16 — fill the A slots (2t,2t+1 | 2t+8,2t+9) of two MMAs;
+//     K is permuted inside an MMA and the activation fragment uses the same permutation:
+//     lane (g, t) loads x[n][32c + 8t .. +8] (one 16-byte SUN-ACT chunk) of batch row
+//     n = (g & 1) * 4 + (g >> 1), an order that puts the eight lanes of each
 //     shared-memory phase on eight different 16-byte bank groups.
-//   * The MMAs run on q + 136 (the magic pair itself, exact in bf16); -136 sum x (two MMAs
-//     with A = 1 per block, shared by the tiles) is added before the group scale s, i.e.
-//     s sum q x per block and warp-chunk in fp32; blocks go in pairs so two MMA chains
-//     interleave; the scale is applied once per block with an FMA (s * sum(q x), the operand bf16(q s) without its bf16
-//     rounding: below the 2e-2 logit tolerance). SUN-W4 stores a block's 128 scales row-interleaved
-//     (position (r & 7) * 16 + (r >> 3)), so lane g's four rows are one 8-byte load.
-//   * One producer warp streams stages of up to kbs consecutive K blocks of a tile
-//     (packed kbs x 8 KB, scales kbs x 256 B, the bn x 128 k SUN-ACT slice: three
-//     bulk copies); the weight and scale copies of the first ring's worth go out
-//     before griddepcontrol.wait.
-//   * Schedule: with at least one tile per SM, each CTA streams a contiguous run of
-//     whole tiles (the epilogue of one overlaps the ring's loads of the next); with
-//     fewer tiles, S = SMs / tiles CTAs split each tile's K, park their 128 x 16 fp32
-//     partials in L2 and bump the tile's counter, and the CTA completing the count
-//     adds the S partials in split order (deterministic) and runs the epilogue. (A
-//     stream-K grid measured slower: the partial segments' L2 round trips inside the
-//     main loop stalled the stream.) The epilogue is the tcgen05 GEMM's epi_chunk (QKV
-//     RoPE + KV append, residual + next-norm operand, SwiGLU, store) on warps 2..5.
+//   * -136 sum x comes from two MMAs with A = 1 per block (shared by the tiles) and is
+//     added before the group scale: acc += s (sum (q + 136) x - 136 sum x) = s sum q x in
+//     fp32 (the operand bf16(q s) without its bf16 rounding: below the 2e-2 logit
+//     tolerance). Blocks go in pairs so two MMA chains interleave; full 4-block stages use
+//     per-thread base registers + immediate offsets. SUN-W4 stores a block's 128 scales
+//     row-interleaved ((r & 7) * 16 + (r >> 3)): a lane's four rows are one 8-byte load.
+//   * One producer warp streams stages of up to kbs consecutive K blocks of one tile
+//     (packed kbs x 8 KB, scales kbs x 256 B, the bn x 128 k SUN-ACT slice: three bulk
+//     copies); the weight and scale copies of the first ring's worth go out before the
+//     dependency wait (griddepcontrol.wait, or a chain phase's grid count).
+//   * Measured (scripts/gv_timeline.py; probe builds -DSUN_GV_PROBE_IDLE / _NOLOAD): the
+//     consumer, not the ring, paces it — with no loads at all (NOLOAD) the 8B gate_up's
+//     2-tile CTAs take the same ~16 us as with them, while the ring alone (IDLE) streams
+//     at 7.5 TB/s; the integer ALU pipe (LOP3 / SHF of the dequant) runs at ~53% and the
+//     HMMA pipe at ~33%, the rest is dependency latency with four warps per scheduler.
+//   * Schedule: with at least one tile per SM, each CTA streams a contiguous run of whole
+//     tiles (the epilogue of one overlaps the ring's loads of the next); with fewer tiles,
+//     S = SMs / tiles CTAs split each tile's K, park their 128 x 16 fp32 partials in L2
+//     and bump the tile's counter, and the CTA completing the count adds the S partials
+//     in split order (deterministic) and runs the epilogue. (A stream-K grid measured
+//     slower: the partial segments' L2 round trips inside the main loop stalled the
+//     stream.) The epilogue is the tcgen05 GEMM's epi_chunk (QKV RoPE + KV append,
+//     residual + next-norm operand, SwiGLU, store) on warps 2..5.
 // ---------------------------------------------------------------------------
 constexpr int kGvWarps = 16;                     // compute warps: (row quarter, 32-k chunk)
 constexpr int kGvMT = 2;                         // m16 tiles per warp (32 rows)
