@@ -35,6 +35,9 @@ struct ChainArgs {
   unsigned long long* stamps;  // profiling: per CTA [16] = per phase p: [4p] activations ready,
                                // [4p+1] first MMA, [4p+2] last MMA issued, [4p+3] epilogue done
   unsigned* bar;  // [2]: phases completed x CTAs, CTAs exited (zeroed once, self-resetting)
+  unsigned* ready;  // bf16 chain, non-null: [kChainMaxPhases][kChainReadyTiles] per-tile counts of the
+                    // CTAs that finished writing a phase's output tile; the next phase's activation
+                    // stages wait only for the tiles they read (zeroed by the last CTA out)
   unsigned long long* tl;
   int tl_idx;
 };
@@ -74,6 +77,38 @@ SUN_DEVICE PhaseSched phase_sched(const GemmArgs& a) {
 // (e.g. another persistent kernel holding SMs) traps after 2 s — the launch fails with
 // an error instead of hanging the GPU.
 constexpr unsigned long long kChainWatchdogNs = 2000000000ull;
+constexpr int kChainReadyTiles = 1024;
+
+// Per-tile readiness (bf16 chain): the activation producer of phase p waits for the
+// producer tiles of phase p - 1 that its K steps read, instead of the whole phase. `rp`
+// is the ready prefix of the producer's tiles (tiles < rp all complete); a poll round
+// reads 16 counters at once (relaxed loads, then an acquire fence: one round trip) and
+// the grid count (every tile of the phase done).
+SUN_DEVICE void chain_wait_tiles(const unsigned* rd, unsigned writers, int need_hi, int tiles, int& rp,
+                                 const unsigned* bar, unsigned phase_target) {
+  if (need_hi < rp) return;
+  const unsigned long long t0 = gtimer();
+  for (;;) {
+    unsigned v[16];
+    const int base = rp;
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      v[i] = base + i < tiles ? *reinterpret_cast<const volatile unsigned*>(rd + base + i) : writers;
+    const unsigned b = *reinterpret_cast<const volatile unsigned*>(bar);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    if (b >= phase_target) {
+      rp = tiles;
+      return;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (rp == base + i && v[i] >= writers) ++rp;
+    }
+    if (need_hi < rp) return;
+    __nanosleep(32);
+    if (gtimer() - t0 > kChainWatchdogNs) __trap();
+  }
+}
 
 SUN_DEVICE void chain_wait_phase(const unsigned* bar, unsigned target) {
   if (target == 0) return;
@@ -113,7 +148,16 @@ SUN_DEVICE void st_async_f4(uint32_t addr, const float* v, uint32_t mbar) {
 template <int EPI>
 SUN_DEVICE void chain_epilogue_phase(const GemmArgs& a, const PhaseSched& ps, float* epi, uint32_t tmem_base,
                                      uint64_t* tfull, uint64_t* tempty, int& buf, int& tphase, float* recv,
-                                     uint64_t* rbar) {
+                                     uint64_t* rbar, unsigned* ready_p) {
+  // this CTA's share of `tile` is written: publish it to the next phase's activation loads
+  auto publish = [&](int tile, bool need_bar) {
+    if (ready_p == nullptr) return;
+    if (need_bar) epi_pair_bar();
+    if (threadIdx.x == 64) {
+      __threadfence();
+      atomicAdd(ready_p + tile, 1u);
+    }
+  };
   const int warp = static_cast<int>(threadIdx.x >> 5);
   const int q = warp & 3;
   const int row_local = q * 32 + (threadIdx.x & 31);
@@ -160,6 +204,7 @@ SUN_DEVICE void chain_epilogue_phase(const GemmArgs& a, const PhaseSched& ps, fl
       tc_fence_before();
       epi_bar();
       if (epi_lead_thread()) mbar_arrive(&tempty[buf]);
+      publish(tile, true);
     } else if (!a.vcluster) {
       // hardware cluster (S = 2 or 4 ranks of one tile, 4 / S tiles per 4-CTA cluster):
       // send every chunk another rank owns (chunk c -> rank c % S, slot = our rank among
@@ -221,6 +266,7 @@ SUN_DEVICE void chain_epilogue_phase(const GemmArgs& a, const PhaseSched& ps, fl
         } else {
           epi_chunk<EPI, 8>(a, tile, row_local, rank * 16 + 8 * epi_grp(), v, epi);
         }
+        publish(tile, true);
       } else {
         for (int c = rank + S * epi_grp(); c < nch; c += 2 * S) {
           float v[16];
@@ -230,6 +276,7 @@ SUN_DEVICE void chain_epilogue_phase(const GemmArgs& a, const PhaseSched& ps, fl
         tc_fence_before();
         epi_pair_bar();
         if (epi_lead_thread()) mbar_arrive(&tempty[buf]);
+        publish(tile, false);
       }
     } else {
       // split phase: park this rank's partial in L2, meet the tile's S CTAs, reduce
@@ -301,6 +348,7 @@ SUN_DEVICE void chain_epilogue_phase(const GemmArgs& a, const PhaseSched& ps, fl
       }
       epi_pair_bar();  // the last of the tile's 2S arrivals rearms its counter
       if (threadIdx.x == 64 && atomicAdd(tile_cnt, 1u) == 2u * S - 1u) *tile_cnt = 0u;
+      publish(tile, false);
     }
     if (++buf == 2) {
       buf = 0;
@@ -382,9 +430,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_chain_kernel(const __gri
       for (int p = 0; p < c.nph; ++p) {
         const GemmArgs& a = c.ph[p];
         const PhaseSched ps = phase_sched(a);
+        // per-tile readiness of the producing phase (bf16 chain, p >= 1): K step ks reads
+        // rows 128 ks .. 128 ks + 127 of its output = tiles of `rows_per` rows
+        const bool tiles_wait = !wprod && p > 0 && c.ready != nullptr;
+        const int rows_per = (p > 0 && c.epi[p - 1] == EPI_SWIGLU) ? 64 : kTileM;
+        const unsigned writers = p > 0 && c.ph[p - 1].splits > 1 ? static_cast<unsigned>(c.ph[p - 1].splits) : 1u;
+        const int ptiles = p > 0 ? c.ph[p - 1].m_tiles : 0;
+        int rp = 0;
         if (!wprod) {
           if (p == 0) pdl_wait();
-          else chain_wait_phase(c.bar, G * p);
+          else if (!tiles_wait) chain_wait_phase(c.bar, G * p);
           SUN_CSTAMP(4 * p);
         }
         const int KS = a.ksteps;
@@ -392,6 +447,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_chain_kernel(const __gri
         for (int j = 0; j < ps.n; ++j) {
           const int nb = min(2, a.kb64 - 2 * ks);
           if (issued >= depth) mbar_wait(&eb[slot], phase ^ 1);
+          if (tiles_wait) {
+            chain_wait_tiles(c.ready + (p - 1) * kChainReadyTiles, writers,
+                             min(ptiles - 1, (kTileM * ks + kTileM - 1) / rows_per), ptiles, rp, c.bar, G * p);
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy stores -> bulk copy
+          }
           if (wprod) {
             mbar_arrive_expect_tx(&fb[slot], nb * kTileWBytes);
             bulk_load_hint(stg + slot * sb, a.wblk + (static_cast<long long>(tile) * a.kb64 + 2 * ks) * kTileWBytes,
@@ -477,10 +537,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_chain_kernel(const __gri
         if (threadIdx.x == 64) chain_wait_phase(c.bar, G * p);
         epi_pair_bar();
       }
+      unsigned* ready_p = (c.ready != nullptr && p + 1 < c.nph) ? c.ready + p * kChainReadyTiles : nullptr;
       switch (c.epi[p]) {
-        case EPI_RESID_ADD: chain_epilogue_phase<EPI_RESID_ADD>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase, recv, &rbar[p]); break;
-        case EPI_SWIGLU: chain_epilogue_phase<EPI_SWIGLU>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase, recv, &rbar[p]); break;
-        case EPI_QKV_ROPE: chain_epilogue_phase<EPI_QKV_ROPE>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase, recv, &rbar[p]); break;
+        case EPI_RESID_ADD: chain_epilogue_phase<EPI_RESID_ADD>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase, recv, &rbar[p], ready_p); break;
+        case EPI_SWIGLU: chain_epilogue_phase<EPI_SWIGLU>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase, recv, &rbar[p], ready_p); break;
+        case EPI_QKV_ROPE: chain_epilogue_phase<EPI_QKV_ROPE>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase, recv, &rbar[p], ready_p); break;
         default: __trap();  // the layer chain's phases are O / gate_up / down / QKV
       }
       epi_pair_bar();
@@ -498,9 +559,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_chain_kernel(const __gri
     tc_fence_after();
     tmem_dealloc(tmem_base, ncols);
   }
-  if (threadIdx.x == 0 && atomicAdd(c.bar + 1, 1u) == G - 1) {  // last CTA out rearms the counters
-    c.bar[0] = 0u;
-    c.bar[1] = 0u;
+  if (c.ready == nullptr) {
+    if (threadIdx.x == 0 && atomicAdd(c.bar + 1, 1u) == G - 1) {  // last CTA out rearms the counters
+      c.bar[0] = 0u;
+      c.bar[1] = 0u;
+    }
+  } else {
+    __shared__ int last_out;
+    if (threadIdx.x == 0) last_out = atomicAdd(c.bar + 1, 1u) == G - 1;
+    __syncthreads();
+    if (last_out) {  // every CTA is past its last read of the tile counters: rearm them too
+      for (int p = 0; p + 1 < c.nph; ++p)
+        for (int t = threadIdx.x; t < c.ph[p].m_tiles; t += blockDim.x) c.ready[p * kChainReadyTiles + t] = 0u;
+      if (threadIdx.x == 0) {
+        c.bar[0] = 0u;
+        c.bar[1] = 0u;
+      }
+    }
   }
   tl_end(c.tl, c.tl_idx);
 }

@@ -58,7 +58,8 @@ def test_gemm_deterministic_stream_k(cuda):
         assert torch.equal(a, kernels.gemm_bf16(w, x, 64))
 
 
-@pytest.mark.parametrize("sched", ["0", "2", "vcl2", "novcl", "push", "nochain", "l2chain", "nogemv", "gvchain"])
+@pytest.mark.parametrize("sched", ["0", "2", "vcl2", "novcl", "push", "nochain", "l2chain", "nogemv", "gvchain",
+                                   "tileready"])
 def test_gemm_schedules_subprocess(sched):
     """The GEMM kernel tests and the end-to-end decode parity under the other
     schedules: 0 = cluster split-K / whole tiles only, 2 = stream-K on every
@@ -70,7 +71,8 @@ def test_gemm_schedules_subprocess(sched):
     QSUN), l2chain = the chains over plain CTAs with every split phase reduced through L2
     (instead of 4-CTA clusters reducing over DSMEM), nogemv = QSUN decode batches of <= 16
     rows on the tcgen05 W4 GEMM instead of the small-batch W4 GEMV, gvchain = the small-batch
-    W4 GEMV as a persistent layer chain (opt-in)."""
+    W4 GEMV as a persistent layer chain (opt-in), tileready = the bf16 chain's activation
+    loads waiting for the producing tiles instead of the whole previous phase (opt-in)."""
     import os
     import subprocess
     import sys
@@ -91,6 +93,8 @@ def test_gemm_schedules_subprocess(sched):
         env["SUN_W4_GEMV"] = "0"
     elif sched == "gvchain":
         env["SUN_W4_GEMV_CHAIN"] = "1"
+    elif sched == "tileready":
+        env["SUN_CHAIN_TILE_READY"] = "1"
     else:
         env["SUN_GEMM_SCHED"] = sched
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", "(gemm or tiny) and not subprocess",
