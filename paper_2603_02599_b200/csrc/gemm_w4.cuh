@@ -131,9 +131,10 @@ __global__ void import_w4_ct_kernel(const uint32_t* __restrict__ ct_packed, cons
 //     tiles (the epilogue of one overlaps the ring's loads of the next); with fewer tiles,
 //     S = SMs / tiles CTAs split each tile's K, park their 128 x 16 fp32 partials in L2
 //     and bump the tile's counter, and the CTA completing the count adds the S partials
-//     in split order (deterministic) and runs the epilogue. (A stream-K grid measured
-//     slower: the partial segments' L2 round trips inside the main loop stalled the
-//     stream.) The epilogue is the tcgen05 GEMM's epi_chunk (QKV RoPE + KV append,
+//     in split order (deterministic) and runs the epilogue. (Measured slower: a stream-K
+//     grid — the partial segments' L2 round trips inside the main loop stalled the stream —
+//     and, behind SUN_GV_CLUSTER=1, one hardware cluster per tile whose rank 0 adds the
+//     peers' staged tiles over DSMEM between two cluster barriers: 7.4 vs 2.6 us tails.) The epilogue is the tcgen05 GEMM's epi_chunk (QKV RoPE + KV append,
 //     residual + next-norm operand, SwiGLU, store) on warps 2..5.
 // ---------------------------------------------------------------------------
 constexpr int kGvWarps = 16;                     // compute warps: (row quarter, 32-k chunk)
@@ -518,6 +519,32 @@ SUN_DEVICE void gv_consume(const GemmArgs& a, int u0, int u1, const GvSmem& m, i
       gv_bar();
     }
     bool run_epi = whole;
+    if (!whole && a.vcluster == 0) {
+      // hardware cluster of the tile's S ranks (split schedule: one segment per CTA): every
+      // rank's T is complete after the first cluster barrier; rank 0's epilogue warps add the
+      // peers' rows over DSMEM in rank order (deterministic: ((T0 + T1) + T2) + ...) and run
+      // the epilogue; the second barrier keeps the peers' T alive until it is read (the
+      // producer warp mirrors both barriers). No L2 partials, atomics or reducer loads.
+      cluster_sync_all();
+      if (cluster_ctarank() == 0 && warp >= 2 && warp < 6) {
+        const int q = warp & 3;
+        const int row_local = q * 32 + lane;
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = T[row_local * kGvTPitch + j];
+        for (int r = 1; r < S; ++r) {
+          const uint32_t src = dsmem_addr(T + row_local * kGvTPitch, static_cast<uint32_t>(r));
+          float pv[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(pv[j]) : "r"(src + 4 * j));
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] += pv[j];
+        }
+        epi_chunk<EPI>(a, tile, row_local, 0, v, m.epi);
+      }
+      cluster_sync_all();
+      continue;
+    }
     if (!whole) {
       // park the partial: [c][128 rows][16] fp32, 8 floats per thread (split schedule:
       // one segment per CTA)
@@ -605,6 +632,11 @@ __global__ void __launch_bounds__(kGvThreads, 1) gemv_w4_kernel(const GemmArgs a
   int slot = 0, phase = 0;
   if (warp == kGvWarps) {
     if (elect_one()) gv_produce(a, u0, u1, m, stages, slot, phase, [] { pdl_wait(); });
+    __syncwarp();
+    if (a.splits > 0 && a.vcluster == 0 && u0 < u1) {  // the consumers' two cluster barriers
+      cluster_sync_all();
+      cluster_sync_all();
+    }
   } else {
     gv_consume<EPI, NB>(a, u0, u1, m, stages, slot, phase, [] { pdl_wait(); });
   }

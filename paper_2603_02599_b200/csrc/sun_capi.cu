@@ -673,6 +673,33 @@ GvCfg gv_cfg(int bn) {
   c.smem = gv_smem_bytes(bn, c.kbs, c.stages);
   return c;
 }
+int max_active_clusters_gv(unsigned size, size_t smem) {
+  static std::map<std::pair<unsigned, size_t>, int> cache;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(size, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(size * 16);
+  cfg.blockDim = dim3(kGvThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = size;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, gemv_w4_kernel<EPI_STORE_F32, 1>, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  cache[key] = n;
+  return n;
+}
+
 bool use_gemv(bool w4, int batch) {
   static const int v = [] { const char* e = getenv("SUN_W4_GEMV"); return e ? atoi(e) : 1; }();
   return w4 && v != 0 && batch <= kGemvMaxBatch;
@@ -693,17 +720,26 @@ SunStatus run_gemv_w4(const void* packed, const void* scales, GemmArgs a, const 
   a.sk_flags = cnt;
   tl_assign(a);
   tl_stamps(a);
-  // whole tiles when every SM gets one (splits = 0), else S-way split-K per tile
+  // whole tiles when every SM gets one (splits = 0), else S-way split-K per tile with the
+  // partials reduced through L2 by the tile's last arrival — or (SUN_GV_CLUSTER=1, off: measured
+  // slower, the 8B O / down GEMV tails 2.6 -> 7.4 us, W4 B=1 step 2.35 -> 2.52 ms) one hardware
+  // cluster of S CTAs per tile reducing over DSMEM between two cluster barriers
+  static const int cl_env = [] { const char* e = getenv("SUN_GV_CLUSTER"); return e ? atoi(e) : 0; }();
   const int slots = std::min(num_sms * c.per_sm, kMaxGemmCtas);
   int grid;
+  a.vcluster = 1;
+  g_cluster = 1;
   if (p.m_tiles >= slots) {
     a.splits = 0;
     grid = slots;
   } else {
     a.splits = std::max(1, std::min(p.ksteps, slots / p.m_tiles));
     grid = p.m_tiles * a.splits;
+    if (cl_env && a.splits > 1 && a.splits <= 8 && max_active_clusters_gv(unsigned(a.splits), c.smem) >= p.m_tiles) {
+      a.vcluster = 0;
+      g_cluster = unsigned(a.splits);
+    }
   }
-  g_cluster = 1;
   if (a.batch <= 8) SUN_CUDA(launch(gemv_w4_kernel<EPI, 1>, dim3(grid), dim3(kGvThreads), c.smem, st, pdl, a));
   else SUN_CUDA(launch(gemv_w4_kernel<EPI, 2>, dim3(grid), dim3(kGvThreads), c.smem, st, pdl, a));
   return SUN_OK;
@@ -731,6 +767,7 @@ SunStatus run_gemv_chain_w4(GemmArgs* ph, const GemmPlan* plans, const void* con
     a.sk_part = part;
     a.sk_flags = cnt;
     a.splits = plans[i].m_tiles >= G ? 0 : std::max(1, std::min(plans[i].ksteps, G / plans[i].m_tiles));
+    a.vcluster = 1;  // (split tiles reduce through L2: the chain is not a cluster launch)
     c.ph[i] = a;
   }
   c.nph = nph;

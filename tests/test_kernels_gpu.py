@@ -59,7 +59,7 @@ def test_gemm_deterministic_stream_k(cuda):
 
 
 @pytest.mark.parametrize("sched", ["0", "2", "vcl2", "novcl", "push", "nochain", "l2chain", "nogemv", "gvchain",
-                                   "tileready"])
+                                   "tileready", "gvcluster"])
 def test_gemm_schedules_subprocess(sched):
     """The GEMM kernel tests and the end-to-end decode parity under the other
     schedules: 0 = cluster split-K / whole tiles only, 2 = stream-K on every
@@ -72,7 +72,8 @@ def test_gemm_schedules_subprocess(sched):
     (instead of 4-CTA clusters reducing over DSMEM), nogemv = QSUN decode batches of <= 16
     rows on the tcgen05 W4 GEMM instead of the small-batch W4 GEMV, gvchain = the small-batch
     W4 GEMV as a persistent layer chain (opt-in), tileready = the bf16 chain's activation
-    loads waiting for the producing tiles instead of the whole previous phase (opt-in)."""
+    loads waiting for the producing tiles instead of the whole previous phase (opt-in), gvcluster =
+    the W4 GEMV's split tiles reduced over DSMEM in hardware clusters instead of through L2."""
     import os
     import subprocess
     import sys
@@ -95,6 +96,8 @@ def test_gemm_schedules_subprocess(sched):
         env["SUN_W4_GEMV_CHAIN"] = "1"
     elif sched == "tileready":
         env["SUN_CHAIN_TILE_READY"] = "1"
+    elif sched == "gvcluster":
+        env["SUN_GV_CLUSTER"] = "1"
     else:
         env["SUN_GEMM_SCHED"] = sched
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", "(gemm or tiny) and not subprocess",
