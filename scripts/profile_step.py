@@ -12,8 +12,14 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c3")
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--no-pdl", action="store_true")
+ap.add_argument("--batch", type=int, default=0, help="override the config's batch")
+ap.add_argument("--isl", type=int, default=0, help="override the config's context start")
 args = ap.parse_args()
-cfg = bench.CONFIGS[args.config]
+cfg = dict(bench.CONFIGS[args.config])
+if args.batch:
+    cfg["batch"] = args.batch
+if args.isl:
+    cfg["isl"] = args.isl
 spec = SPECS[cfg["spec"]].with_bits(4) if cfg["bits"] == 4 else SPECS[cfg["spec"]]
 dev = torch.device("cuda")
 B = cfg["batch"]
@@ -32,4 +38,4 @@ dec.positions[:B] = torch.tensor(ctx, dtype=torch.int32, device=dev)
 for _ in range(args.steps):
     dec.step_static(B, 0, graph=False, feedback=True)
 torch.cuda.synchronize()
-print("done", len(dec.kernel_names()), "kernels/step")
+print("done", len(dec.kernel_names(batch=B)), "kernels/step")
