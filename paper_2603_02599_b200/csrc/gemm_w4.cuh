@@ -631,7 +631,13 @@ __global__ void __launch_bounds__(kGvThreads, 1) gemv_w4_kernel(const GemmArgs a
   if (threadIdx.x == 0) SUN_STAMP(1);
   int slot = 0, phase = 0;
   if (warp == kGvWarps) {
-    if (elect_one()) gv_produce(a, u0, u1, m, stages, slot, phase, [] { pdl_wait(); });
+    if (elect_one()) {
+      gv_produce(a, u0, u1, m, stages, slot, phase, [] { pdl_wait(); });
+      // every stage of this CTA is in flight: pull the next GEMV's first weight bytes into L2
+      // while this kernel's ring drains and its tail runs (the next kernel's CTAs cannot be
+      // resident before this one exits, so their own first loads would start cold)
+      prefetch_next_weights(a);
+    }
     __syncwarp();
     if (a.splits > 0 && a.vcluster == 0 && u0 < u1) {  // the consumers' two cluster barriers
       cluster_sync_all();

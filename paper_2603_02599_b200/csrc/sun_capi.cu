@@ -705,6 +705,34 @@ bool use_gemv(bool w4, int batch) {
   return w4 && v != 0 && batch <= kGemvMaxBatch;
 }
 
+// L2 prefetch budget per next-GEMV CTA (SUN_GV_PREFETCH_KB, default 0: 32-128 KB measured
+// neutral on the 8B W4 B=1 / B=8 steps) and its target: the next W4 GEMV of the step (its
+// schedule as run_gemv_w4 will launch it).
+int gv_prefetch_bytes() {
+  static const int v = [] { const char* e = getenv("SUN_GV_PREFETCH_KB"); return (e ? atoi(e) : 0) * 1024; }();
+  return v;
+}
+void gv_set_prefetch(GemmArgs& a, const void* next_packed, const GemmPlan& np, int num_sms) {
+  const int bytes = gv_prefetch_bytes();
+  if (!next_packed || bytes <= 0) return;
+  const GvCfg c = gv_cfg(a.bn);
+  const int slots = std::min(num_sms * c.per_sm, kMaxGemmCtas);
+  a.pf_w = static_cast<const uint8_t*>(next_packed);
+  a.pf_w4 = 1;
+  a.pf_m_tiles = np.m_tiles;
+  a.pf_ksteps = np.ksteps;
+  a.pf_kb64 = np.kb64;
+  a.pf_sk_units = 0;
+  if (np.m_tiles >= slots) {
+    a.pf_splits = 0;
+    a.pf_grid = slots;
+  } else {
+    a.pf_splits = std::max(1, std::min(np.ksteps, slots / np.m_tiles));
+    a.pf_grid = np.m_tiles * a.pf_splits;
+  }
+  a.pf_bytes = bytes;
+}
+
 template <int EPI>
 SunStatus run_gemv_w4(const void* packed, const void* scales, GemmArgs a, const GemmPlan& p, float* part,
                       unsigned* cnt, cudaStream_t st, bool pdl, int num_sms) {
@@ -1262,10 +1290,14 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
   static const int gvchain_env = [] { const char* e = getenv("SUN_W4_GEMV_CHAIN"); return e ? atoi(e) : 0; }();
   const bool gemv = use_gemv(w4, batch);
   const bool chain = use_chain(flags, w4, bn) && (gemv ? gvchain_env != 0 : (w4 ? dec->chain_w4_ok : dec->chain_ok));
-  auto w4_gemm = [&](auto epi_tag, const void* pk, const void* sc, const GemmArgs& ga, const GemmPlan& p) {
+  auto w4_gemm = [&](auto epi_tag, const void* pk, const void* sc, const GemmArgs& ga, const GemmPlan& p,
+                     const void* next_pk = nullptr, const GemmPlan* next_p = nullptr) {
     constexpr int E = decltype(epi_tag)::value;
-    return gemv ? run_gemv_w4<E>(pk, sc, ga, p, dec->gv_part, dec->gv_cnt, st, pdl, dec->num_sms)
-                : run_gemm<E>(nullptr, pk, sc, ga, p, st, pdl);
+    if (!gemv) return run_gemm<E>(nullptr, pk, sc, ga, p, st, pdl);
+    GemmArgs g = ga;
+    g.pf_w = nullptr;  // (the tcgen05 path's prefetch target: not this kernel's)
+    if (next_p) gv_set_prefetch(g, next_pk, *next_p, dec->num_sms);
+    return run_gemv_w4<E>(pk, sc, g, p, dec->gv_part, dec->gv_cnt, st, pdl, dec->num_sms);
   };
   using QkvT = std::integral_constant<int, EPI_QKV_ROPE>;
   using ResT = std::integral_constant<int, EPI_RESID_ADD>;
@@ -1276,7 +1308,7 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     if (!chain || l == 0) {
       a = qkv_args(l);
       set_prefetch(a, lw.w_o, dec->p_o, bn, w4);  // O-proj weights, through the attention kernel
-      if (!(skip & 1)) s = w4 ? w4_gemm(QkvT{}, lw.w_qkv, lw.s_qkv, a, dec->p_qkv)
+      if (!(skip & 1)) s = w4 ? w4_gemm(QkvT{}, lw.w_qkv, lw.s_qkv, a, dec->p_qkv, lw.w_o, &dec->p_o)
              : run_gemm<EPI_QKV_ROPE>(lw.w_qkv, nullptr, nullptr, a, dec->p_qkv, st, pdl);
       if (s != SUN_OK) return s;
     }
@@ -1305,18 +1337,19 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     }
     a = o_args(l);
     set_prefetch(a, lw.w_gate_up, dec->p_gu, bn, w4);
-    if (!(skip & 8)) s = w4 ? w4_gemm(ResT{}, lw.w_o, lw.s_o, a, dec->p_o)
+    if (!(skip & 8)) s = w4 ? w4_gemm(ResT{}, lw.w_o, lw.s_o, a, dec->p_o, lw.w_gate_up, &dec->p_gu)
            : run_gemm<EPI_RESID_ADD>(lw.w_o, nullptr, nullptr, a, dec->p_o, st, pdl);
     if (s != SUN_OK) return s;
     a = gu_args(l);
     set_prefetch(a, lw.w_down, dec->p_down, bn, w4);
-    if (!(skip & 16)) s = w4 ? w4_gemm(SwiT{}, lw.w_gate_up, lw.s_gate_up, a, dec->p_gu)
+    if (!(skip & 16)) s = w4 ? w4_gemm(SwiT{}, lw.w_gate_up, lw.s_gate_up, a, dec->p_gu, lw.w_down, &dec->p_down)
            : run_gemm<EPI_SWIGLU>(lw.w_gate_up, nullptr, nullptr, a, dec->p_gu, st, pdl);
     if (s != SUN_OK) return s;
     a = down_args(l);
     if (l + 1 < d.n_layers) set_prefetch(a, dec->layers[l + 1].w_qkv, dec->p_qkv, bn, w4);
     else set_prefetch(a, dec->w.lm_head, dec->p_lm, bn, false);
-    if (!(skip & 32)) s = w4 ? w4_gemm(ResT{}, lw.w_down, lw.s_down, a, dec->p_down)
+    if (!(skip & 32)) s = w4 ? w4_gemm(ResT{}, lw.w_down, lw.s_down, a, dec->p_down,
+                                       l + 1 < d.n_layers ? dec->layers[l + 1].w_qkv : nullptr, &dec->p_qkv)
            : run_gemm<EPI_RESID_ADD>(lw.w_down, nullptr, nullptr, a, dec->p_down, st, pdl);
     if (s != SUN_OK) return s;
   }
