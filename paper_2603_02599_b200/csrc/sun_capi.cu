@@ -837,10 +837,14 @@ struct W4ChainCfg {
   size_t smem;
 };
 W4ChainCfg w4_chain_cfg(int bn) {
+  // (SUN_W4_WGROUP / SUN_W4_XK / SUN_W4_XSTAGES override, as for the separate W4 GEMMs)
+  static const int env_wg = [] { const char* e = getenv("SUN_W4_WGROUP"); return e ? atoi(e) : 0; }();
+  static const int env_xk = [] { const char* e = getenv("SUN_W4_XK"); return e ? atoi(e) : 0; }();
+  static const int env_xs = [] { const char* e = getenv("SUN_W4_XSTAGES"); return e ? atoi(e) : 0; }();
   W4ChainCfg c{};
-  c.wgroup = 4;
-  c.xk = bn <= 32 ? 4 : 2;
-  c.xstages = bn > 64 ? 2 : 3;
+  c.wgroup = env_wg > 0 ? env_wg : 4;
+  c.xk = env_xk > 0 ? env_xk : (bn <= 32 ? 4 : 2);
+  c.xstages = env_xs > 0 ? env_xs : (bn > 64 ? 2 : 3);
   const int budget = kSmemPerSm - 2048 - 2048 - int(kEpiSmemBytes) - 1024 - c.xstages * int(w4_xstage_bytes(bn, c.xk));
   c.stages = std::max(2, std::min(kMaxWStages, budget / int(w4_wstage_bytes(c.wgroup))));
   c.smem = gemm_smem_bytes_w4(bn, c.wgroup, c.stages, c.xk, c.xstages);
