@@ -25,6 +25,7 @@ ap.add_argument("--bits", type=int, default=16)
 ap.add_argument("--batches", default="1,8,16,32,64,128")
 ap.add_argument("--contexts", default="256,1024,2048,4096")
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--pps", type=int, default=0, help="attention pages per split (0 = automatic)")
 ap.add_argument("--out", required=True)
 args = ap.parse_args()
 
@@ -45,12 +46,12 @@ for ctx in contexts:
     for B in batches:
         dec.positions[:B] = ctx
         for _ in range(3):
-            dec.step_static(B, 0, graph=True, feedback=False)
+            dec.step_static(B, args.pps, graph=True, feedback=False)
         ts = []
         for _ in range(args.reps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            dec.step_static(B, 0, graph=True, feedback=False)
+            dec.step_static(B, args.pps, graph=True, feedback=False)
             e1.record()
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1) / 1e3)
