@@ -66,3 +66,26 @@ def test_compressed_tensors_packing_rule():
     for r in range(5):
         for k in range(64):
             assert ((int(u[r, k // 8]) >> (4 * (k % 8))) & 0xF) - 8 == int(q[r, k])
+
+
+def test_compressed_tensors_import_rejects_non_w4_layers():
+    """A linear layer that is not pack-quantized int4 (missing weight_scale, or a
+    weight_shape that disagrees with the packing) is refused before any device work."""
+    import pytest
+
+    from paper_2603_02599_b200.errors import UnsupportedShape
+
+    spec = replace(TINY, name="tiny", ffn=768, n_layers=1)
+    w = init_weights(spec, 0)
+    q, s = quant_ref.quantize(w["l0.wq"])
+    base = {"model.embed_tokens.weight": w["embed"], "model.norm.weight": w["final_norm"],
+            "lm_head.weight": w["lm_head"], "model.layers.0.input_layernorm.weight": w["l0.attn_norm"],
+            "model.layers.0.post_attention_layernorm.weight": w["l0.ffn_norm"],
+            "model.layers.0.self_attn.q_proj.weight_packed": checkpoint.pack_compressed_tensors(q)}
+    with pytest.raises(UnsupportedShape):  # no weight_scale
+        checkpoint.from_compressed_tensors(spec, base, "cpu", 64)
+    bad = dict(base)
+    bad["model.layers.0.self_attn.q_proj.weight_scale"] = s
+    bad["model.layers.0.self_attn.q_proj.weight_shape"] = torch.tensor([q.shape[0], q.shape[1] * 2])
+    with pytest.raises(UnsupportedShape):  # weight_shape disagrees with the packed K
+        checkpoint.from_compressed_tensors(spec, bad, "cpu", 64)
