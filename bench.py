@@ -264,6 +264,34 @@ def reference_arm(args, cfg):
 HANDOFF_PAGES = 64  # one C3 request: ISL 1024 = 64 pages of 16 tokens (128 MiB at 8B geometry)
 
 
+def handoff_local(kv, dev, reps=5):
+    """N = 1: the product hand-off path (handoff.copy_pages -> sun_kv_handoff_copy, one
+    copy-engine transfer per consecutive page run) between two page runs of this GPU's own
+    pool — the same C-ABI call the N > 1 leg makes into a peer's pool over NVLink, here a
+    device-to-device copy (reads and writes the same HBM): the per-request overhead and a
+    lower bound of the path, not an NVLink figure."""
+    import torch
+
+    from paper_2603_02599_b200.handoff import copy_pages
+
+    src = list(range(kv.num_pages - HANDOFF_PAGES, kv.num_pages))
+    dst = list(range(kv.num_pages - 2 * HANDOFF_PAGES, kv.num_pages - HANDOFF_PAGES))
+    nbytes = HANDOFF_PAGES * kv.page_bytes
+    s = torch.cuda.Stream(device=dev)
+    dst_struct = kv.struct()
+    best = float("inf")
+    for i in range(reps + 1):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        copy_pages(kv, src, dst_struct, dst, s)
+        e1.record(s)
+        e1.synchronize()
+        if i > 0:
+            best = min(best, e0.elapsed_time(e1))
+    return {"bytes_per_request": nbytes, "pages": HANDOFF_PAGES, "transport": "same-device copy engine (D2D)",
+            "ms_per_request": best, "GB_s": nbytes / (best / 1e3) / 1e9}
+
+
 def handoff_leg(kv, rank, world, dev, spec, reps=5):
     """Every rank hands one ISL-1024 request's KV (the last HANDOFF_PAGES pages of its
     pool, reserved for this) to rank + 1 at the same time, two ways: (1) the
@@ -385,7 +413,7 @@ def gpu_arm(args, cfg):
     w = init_weights(spec, seed=0, device=dev)
     dw = DeviceWeights(spec, w, dev, max_ctx, free_source=True)
     del w
-    kv = KvPool(spec, sum(pages_for(c + total_steps + args.steps + 2) for c in ctx) + 4 + HANDOFF_PAGES, dev)
+    kv = KvPool(spec, sum(pages_for(c + total_steps + args.steps + 2) for c in ctx) + 4 + 2 * HANDOFF_PAGES, dev)
     kv.fill_random_(seed=1000 + rank)
     dec = SharedDecodeModule(spec, dw, kv, max_batch=B, max_context=max_ctx, use_pdl=not args.no_pdl)
     # block tables: contiguous page runs per member
@@ -509,6 +537,8 @@ def gpu_arm(args, cfg):
     handoff = None
     if world > 1 and not args.no_handoff:
         handoff = handoff_leg(kv, rank, world, dev, spec)
+    elif not args.no_handoff:
+        handoff = handoff_local(kv, dev)
 
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu:
