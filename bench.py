@@ -511,18 +511,35 @@ def gpu_arm(args, cfg):
                 dec.decode(h_tok, h_pos, h_bt, pages_per_split=args.pps, graph=False)
                 out.copy_(dec.next_tokens[:B])
             h_pos += 1
+        # serving-loop pipelining (graph path): one pinned token buffer is both a step's D2H
+        # destination and the next step's H2D source (stream-ordered), positions alternate
+        # between two pinned buffers whose rewrite waits for the step two back, so the GPU
+        # runs a step ahead of the host instead of idling through a sync + relaunch per step
+        h_pos2 = [h_pos, pin(h_pos.clone())]
+        evs = [torch.cuda.Event(), torch.cuda.Event()]
+        if graph:
+            h_tok.copy_(out)
+            for k in range(2):  # capture both (tokens == out) graphs
+                h_pos2[k].copy_(h_pos)
+                dec.decode_host(h_tok, h_pos2[k], h_bt, h_tok, pages_per_split=args.pps)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        pos_base = h_pos.clone()
         te = time.perf_counter()
         for i in range(args.steps):
-            if graph:  # H2D inputs + step + D2H next tokens as one graph launch, then synchronise
-                dec.decode_host(h_tok, h_pos, h_bt, out, pages_per_split=args.pps)
+            if graph:  # H2D inputs + step + D2H next tokens as one graph launch per step
+                k = i & 1
+                if i >= 2:
+                    evs[k].synchronize()  # the step that last read h_pos2[k] is done
+                torch.add(pos_base, i, out=h_pos2[k])
+                dec.decode_host(h_tok, h_pos2[k], h_bt, h_tok, pages_per_split=args.pps, sync=False)
+                evs[k].record()
             else:
                 nt = dec.decode(h_tok, h_pos, h_bt, pages_per_split=args.pps, graph=False)
                 out.copy_(nt)  # D2H read of the step's result (synchronises)
-            h_tok.copy_(out)
-            h_pos += 1
+                h_tok.copy_(out)
+                h_pos += 1
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - te
         t_e = torch.tensor([e2e_s], device=dev)
@@ -531,7 +548,9 @@ def gpu_arm(args, cfg):
         e2e = {"value": float(tok_all.item()) / float(t_e.item()), "unit": "tokens/s",
                "h2d_bytes_per_step": int(h_tok.numel() * 4 + h_pos.numel() * 4 + h_bt.numel() * 4),
                "d2h_bytes_per_step": int(out.numel() * 4),
-               "api": ("SharedDecodeModule.decode_host(pinned tokens/positions/block_tables) -> pinned next tokens"
+               "api": ("SharedDecodeModule.decode_host(pinned tokens/positions/block_tables) -> pinned next tokens, "
+                       "one graph per step (H2D inputs, step, D2H next tokens); the next step's tokens are "
+                       "H2D'd from the pinned buffer the previous D2H filled, the host keeps one step ahead"
                        if graph else "SharedDecodeModule.decode(host pinned tokens/positions/block_tables) -> next tokens")}
 
     handoff = None

@@ -246,12 +246,18 @@ class SharedDecodeModule(_StepRunner):
         g.replay()
 
     def decode_host(self, tokens: torch.Tensor, positions: torch.Tensor, block_tables: torch.Tensor,
-                    out: torch.Tensor, pages_per_split: int = 0) -> torch.Tensor:
+                    out: torch.Tensor, pages_per_split: int = 0, sync: bool = True) -> torch.Tensor:
         """Eq. 3 from pinned host buffers as ONE graph launch: the inputs' host->device
         copies, the step and the next tokens' device->host copy into pinned ``out``;
         returns ``out`` once the stream has synchronised. The host buffers are baked
         into the captured graph (keyed by their addresses): reuse the same buffers
-        from step to step, as a serving loop does."""
+        from step to step, as a serving loop does.
+
+        ``sync=False`` returns right after the launch (the caller orders its host reads
+        and rewrites of the buffers with events): a serving loop can then pass the same
+        pinned buffer as ``out`` and as the next step's ``tokens`` — the device-to-host
+        copy of step i and the host-to-device copy of step i + 1 are stream-ordered — and
+        keep the GPU one step ahead of its host bookkeeping."""
         b = int(tokens.shape[0])
         if b < 1:
             raise ValueError("decode batch must be non-empty")
@@ -280,7 +286,8 @@ class SharedDecodeModule(_StepRunner):
             self._graphs[key] = g
             return out
         g.replay()
-        torch.cuda.current_stream().synchronize()
+        if sync:
+            torch.cuda.current_stream().synchronize()
         return out
 
     def decode(self, tokens: torch.Tensor, positions: torch.Tensor, block_tables: torch.Tensor,

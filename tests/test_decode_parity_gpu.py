@@ -288,3 +288,50 @@ def test_grouped_prefill_matches_row_prefill(cuda, variant):
         if f0[i] != f1[i]:  # only a near-tie may flip
             top2 = l1[i].topk(2).values
             assert (top2[0] - top2[1]).item() < 2e-2
+
+
+def test_decode_host_pipelined_equals_synchronous(cuda):
+    """decode_host(sync=False) as bench.py's e2e serving loop drives it — one pinned token
+    buffer that is each step's D2H destination and the next step's H2D source, positions
+    alternating between two pinned buffers rewritten only after the step two back — ends in
+    exactly the state the synchronous host loop reaches: same KV cache, same tokens."""
+    from paper_2603_02599_b200.kvpool import KvPool, pages_for
+    from paper_2603_02599_b200.modules import SharedDecodeModule
+    from paper_2603_02599_b200.spec import TINY
+    from paper_2603_02599_b200.weights import DeviceWeights, init_weights
+
+    spec, B, steps = TINY, 6, 12
+    ctx = [5, 17, 30, 2, 44, 21]
+    max_ctx = max(ctx) + steps + 8
+    dw = DeviceWeights(spec, init_weights(spec, 3), cuda, max_ctx)
+    npg = pages_for(max_ctx)
+    bt = torch.zeros(B, npg, dtype=torch.int32)
+    for i in range(B):
+        bt[i] = torch.arange(i * npg, (i + 1) * npg, dtype=torch.int32)
+    tok0 = torch.tensor([3, 99, 7, 250, 1, 42], dtype=torch.int32)
+    finals = []
+    for mode in ("sync", "pipelined"):
+        kv = KvPool(spec, B * npg + 2, cuda)
+        kv.fill_random_(11)
+        dec = SharedDecodeModule(spec, dw, kv, B, max_ctx)
+        h_tok, h_bt = tok0.clone().pin_memory(), bt.clone().pin_memory()
+        pos = [torch.tensor(ctx, dtype=torch.int32).pin_memory() for _ in range(2)]
+        if mode == "sync":
+            out = torch.zeros(B, dtype=torch.int32).pin_memory()
+            for t in range(steps):
+                pos[0].copy_(torch.tensor(ctx, dtype=torch.int32) + t)
+                dec.decode_host(h_tok, pos[0], h_bt, out)
+                h_tok.copy_(out)
+        else:
+            evs = [torch.cuda.Event(), torch.cuda.Event()]
+            for t in range(steps):
+                k = t & 1
+                if t >= 2:
+                    evs[k].synchronize()
+                pos[k].copy_(torch.tensor(ctx, dtype=torch.int32) + t)
+                dec.decode_host(h_tok, pos[k], h_bt, h_tok, sync=False)
+                evs[k].record()
+            torch.cuda.synchronize()
+        finals.append((h_tok.clone(), kv.tensor.clone().cpu()))
+    assert torch.equal(finals[0][0], finals[1][0])
+    assert torch.equal(finals[0][1].view(torch.int16), finals[1][1].view(torch.int16))
