@@ -502,7 +502,10 @@ def gpu_arm(args, cfg):
         pin = lambda t: t.pin_memory()  # noqa: E731
         h_tok = pin(tokens0.clone())
         h_bt = pin(bt.clone())
-        h_pos = pin(torch.tensor(pos_now, dtype=torch.int32))
+        # the same contexts as the device-timed loop (its first step's positions; the warm
+        # calls below re-run the two before them): the KV those steps wrote is rewritten, and
+        # e2e and `value` time the same work
+        h_pos = pin(torch.tensor([c + args.warmup - 2 for c in ctx], dtype=torch.int32))
         out = pin(torch.zeros(B, dtype=torch.int32))
         for i in range(2):  # warm (the first call also captures the host-copy graph)
             if graph:
@@ -528,7 +531,10 @@ def gpu_arm(args, cfg):
         pos_base = h_pos.clone()
         te = time.perf_counter()
         for i in range(args.steps):
-            if graph:  # H2D inputs + step + D2H next tokens as one graph launch per step
+            if graph and args.e2e_sync:  # (A/B: synchronise every step, host feedback)
+                dec.decode_host(h_tok, h_pos2[0], h_bt, h_tok, pages_per_split=args.pps)
+                torch.add(pos_base, i + 1, out=h_pos2[0])
+            elif graph:  # H2D inputs + step + D2H next tokens as one graph launch per step
                 k = i & 1
                 if i >= 2:
                     evs[k].synchronize()  # the step that last read h_pos2[k] is done
@@ -679,6 +685,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-handoff", action="store_true")
     ap.add_argument("--dry-run", action="store_true", help="CPU/gloo run of the rank plumbing (tests)")
+    ap.add_argument("--e2e-sync", action="store_true", help="e2e: synchronise every step (A/B of the pipelining)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
