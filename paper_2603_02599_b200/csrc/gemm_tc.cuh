@@ -45,7 +45,7 @@ enum EpiKind : int {
   EPI_STORE_F32 = 0,  // out_f32[b*ldo + row] = acc
   EPI_RESID_ADD = 1,  // out_f32[b*ldo + row] += acc           (O-proj, down-proj)
   EPI_QKV_ROPE = 2,   // +bias, RoPE(q,k), q -> bf16, k/v -> paged KV cache
-  EPI_SWIGLU = 3,     // rows interleaved in 64-row blocks: act = silu(gate) * up
+  EPI_SWIGLU = 3,     // rows pair-interleaved (2i gate, 2i+1 up): act = silu(gate) * up
   EPI_LOGITS = 4,     // logits fp32 + per-tile (max, argmax) per batch column
 };
 
@@ -322,10 +322,34 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
       a.amax_idx[static_cast<long long>(m_tile) * a.bn + c0 + lane] = idx;
     }
     epi_bar();
+  } else if constexpr (EPI == EPI_SWIGLU) {
+    // tile rows 2i / 2i+1 are gate / up of output m_tile*64 + i: the partner is the
+    // neighbouring lane (no staging, no barrier). The gate lane writes the chunk's first
+    // H = NC/2 columns, the up lane the rest (the sigmoid's division was the epilogue's
+    // critical path when one thread did all NC), one shuffle per column pair: the gate
+    // lane sends v[jj + H], the up lane v[jj]; indices stay compile-time (no local memory).
+    constexpr int H = NC / 2;
+    const bool is_gate = (row_local & 1) == 0;
+    const int jo = m_tile * 64 + (row_local >> 1);
+    const int cb = c0 + (is_gate ? 0 : H);
+#pragma unroll
+    for (int jj = 0; jj < H; ++jj) {
+      const float recv = __shfl_xor_sync(0xffffffffu, is_gate ? v[jj + H] : v[jj], 1);
+      const float g = is_gate ? v[jj] : recv;
+      const float u = is_gate ? recv : v[jj + H];
+      const int b = cb + jj;
+      if (jo < a.n_valid_out && b < B) {
+        // fast exp / divide (~2 ulp in fp32, below the bf16 rounding of the output):
+        // the IEEE versions were a third of the gate_up epilogue tail
+        const float s = __fdividef(g, 1.f + __expf(-g));
+        *reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<uint8_t*>(a.out_bf16) + act_offset(b, jo, a.bn)) =
+            __float2bfloat16_rn(s * u);
+      }
+    }
   } else {
-    // QKV_ROPE / SWIGLU need a partner row of the same tile: stage through smem.
+    // QKV_ROPE needs a partner row half a head away: stage through smem.
     epi_bar();  // previous chunk's partner reads are done
-    if constexpr (EPI == EPI_QKV_ROPE) {
+    {
       const float bias = (a.bias != nullptr && row < a.n_out) ? __bfloat162float(a.bias[row]) : 0.f;
 #pragma unroll
       for (int j = 0; j < NC; ++j) v[j] += bias;
@@ -333,30 +357,7 @@ SUN_DEVICE void epi_chunk(const GemmArgs& a, int m_tile, int row_local, int c0, 
 #pragma unroll
     for (int j = 0; j < NC; ++j) stage_f32[j * kTileM + row_local] = v[j];
     epi_bar();
-    if constexpr (EPI == EPI_SWIGLU) {
-      // rows 0..63 of the tile are gate, 64..127 up: all 128 threads produce outputs,
-      // thread t the output row t % 64 for half of the chunk's columns (t / 64) — the
-      // sigmoid's division was the epilogue's critical path on 64 threads
-      const int jl = row_local & 63;
-      const int jo = m_tile * 64 + jl;
-      if (jo < a.n_valid_out) {
-        const int j0 = (row_local >> 6) * (NC / 2);
-#pragma unroll
-        for (int jj = 0; jj < NC / 2; ++jj) {
-          const int j = j0 + jj;
-          const int b = c0 + j;
-          if (b < B) {
-            const float g = stage_f32[j * kTileM + jl];
-            const float u = stage_f32[j * kTileM + jl + 64];
-            // fast exp / divide (~2 ulp in fp32, below the bf16 rounding of the output):
-            // the IEEE versions were a third of the gate_up epilogue tail
-            const float s = __fdividef(g, 1.f + __expf(-g));
-            *reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<uint8_t*>(a.out_bf16) + act_offset(b, jo, a.bn)) =
-                __float2bfloat16_rn(s * u);
-          }
-        }
-      }
-    } else {  // EPI_QKV_ROPE
+    {
       if (row < a.n_out) {
         const int d = a.head_dim;
         const int half = d >> 1;

@@ -83,16 +83,14 @@ def rope_tables(max_pos: int, head_dim: int, theta: float) -> tuple[torch.Tensor
 
 
 def interleave_gate_up(wg: torch.Tensor, wu: torch.Tensor) -> torch.Tensor:
-    """[f,h] x2 -> [ceil(f/64)*128, h]: block j = gate rows 64j.. then up rows 64j.. (zero pad)."""
+    """[f,h] x2 -> [ceil(f/64)*128, h]: row 2i of block j = gate row 64j+i, row 2i+1 the
+    matching up row (zero pad) — the SWIGLU epilogue pairs them with one lane shuffle."""
     f, h = wg.shape
     nb = (f + 63) // 64
-    out = torch.zeros(nb, 2, 64, h, dtype=wg.dtype, device=wg.device)
     pad = nb * 64 - f
     gp = torch.cat([wg, wg.new_zeros(pad, h)]) if pad else wg
     up = torch.cat([wu, wu.new_zeros(pad, h)]) if pad else wu
-    out[:, 0] = gp.view(nb, 64, h)
-    out[:, 1] = up.view(nb, 64, h)
-    return out.view(nb * 128, h)
+    return torch.stack([gp.view(nb, 64, h), up.view(nb, 64, h)], dim=2).reshape(nb * 128, h)
 
 
 class DeviceWeights:
