@@ -19,7 +19,7 @@ quantised checkpoint. Here that is two load paths that never re-quantise:
   published packing rule (``pack_to_int32``: unsigned q + 8, element 8j+i of a row
   in bits 4i..4i+3 of word j), version unpinned.
 
-File layout: b"SUNCKPT\\x01", u64 little-endian header length, UTF-8 JSON header
+File layout: b"SUNCKPT\\x02", u64 little-endian header length, UTF-8 JSON header
 {"format", "spec", "tensors": [{"name", "dtype", "shape", "offset", "nbytes"}]},
 then each tensor's raw bytes at its offset (4 KiB aligned).
 """
@@ -36,7 +36,7 @@ import torch
 from .errors import UnsupportedShape
 from .spec import DecoderSpec
 
-MAGIC = b"SUNCKPT\x01"
+MAGIC = b"SUNCKPT\x02"  # \x02: gate/up pair-interleaved rows (weights.interleave_gate_up)
 ALIGN = 4096
 _DT = {torch.uint8: "u8", torch.bfloat16: "bf16", torch.float32: "f32", torch.int32: "i32"}
 _DT_INV = {v: k for k, v in _DT.items()}
@@ -75,7 +75,10 @@ def save(path: str | os.PathLike, dw) -> None:
 
 def read_header(path: str | os.PathLike) -> tuple[dict, int]:
     with open(path, "rb") as f:
-        if f.read(len(MAGIC)) != MAGIC:
+        magic = f.read(len(MAGIC))
+        if magic[:7] == MAGIC[:7] and magic != MAGIC:
+            raise ValueError(f"{path}: SUNCKPT version {magic[7]} (this build reads {MAGIC[7]}): re-export it")
+        if magic != MAGIC:
             raise ValueError(f"{path}: not a SUNCKPT checkpoint")
         (n,) = struct.unpack("<Q", f.read(8))
         header = json.loads(f.read(n))

@@ -54,6 +54,10 @@ def test_sunckpt_rejects_foreign_files(tmp_path):
 
     with pytest.raises(ValueError):
         checkpoint.read_header(p)
+    old = tmp_path / "v1.sunckpt"  # the previous layout (gate/up in 64-row blocks) is refused by version
+    old.write_bytes(b"SUNCKPT\x01" + bytes(8))
+    with pytest.raises(ValueError, match="version 1"):
+        checkpoint.read_header(old)
 
 
 def test_compressed_tensors_packing_rule():
