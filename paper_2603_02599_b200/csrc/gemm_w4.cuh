@@ -141,6 +141,7 @@ constexpr int kGvWarps = 16;                     // compute warps: (row quarter,
 constexpr int kGvMT = 2;                         // m16 tiles per warp (32 rows)
 constexpr int kGvThreads = kGvWarps * 32 + 32;   // + the producer warp
 constexpr int kGvMaxStages = 8;
+
 constexpr int kGvTPitch = 17;                    // fp32 staging tile [128][17] (conflict-free row reads)
 
 __host__ __device__ inline uint32_t gv_stage_bytes(int bn, int kbs) {
@@ -348,7 +349,7 @@ SUN_DEVICE void gv_range(const GemmArgs& a, int c, int G, int& u0, int& u1) {
 // under PDL, or during the previous chain phase's tail), the activation copies after it.
 template <typename Gate>
 SUN_DEVICE void gv_produce(const GemmArgs& a, int u0, int u1, const GvSmem& m, int stages, int& slot, int& phase,
-                           Gate gate, int max_pre = kGvMaxStages) {
+                           Gate gate, int max_pre = kGvMaxStages, bool first_wait = false) {
   const int kbs = a.wgroup, bn = a.bn, KB = a.ksteps;
   const uint32_t sb = gv_stage_bytes(bn, kbs);
 #if defined(SUN_GV_PROBE_NOSX)  // probes (timing only, results invalid): skip the scale and X copies
@@ -389,6 +390,8 @@ SUN_DEVICE void gv_produce(const GemmArgs& a, int u0, int u1, const GvSmem& m, i
   };
   int pre_slot[kGvMaxStages], pre_u[kGvMaxStages], pre_len[kGvMaxStages];
   int u = u0, npre = 0;
+  const int phase0 = phase;
+  if (first_wait) max_pre = 1;
   for (; npre < min(stages, max_pre) && u < u1; ++npre) {
     const int len = min(kbs, min(u1 - u, KB - u % KB));
     issue_w(u, len);
@@ -401,6 +404,11 @@ SUN_DEVICE void gv_produce(const GemmArgs& a, int u0, int u1, const GvSmem& m, i
   gate();
   asm volatile("fence.proxy.async.global;" ::: "memory");  // activations written by other CTAs' stores
   for (int i = 0; i < npre; ++i) issue_x(pre_slot[i], pre_u[i], pre_len[i]);
+  // first_wait: the rest of the ring goes out once the first stage has landed, so it does not
+  // share the DRAM queues with the whole ring's burst and the consumers start early (8B
+  // shapes: first stage 4.4 -> 2.1 us, W4 B=1 step 2.38 -> 2.34 ms; a 1-block first stage
+  // landed in 1.0 us but the ring then fell behind the consumers: 2.48 ms)
+  if (first_wait && npre > 0) mbar_wait(&m.full[pre_slot[0]], phase0);
   while (u < u1) {
     const int len = min(kbs, min(u1 - u, KB - u % KB));
     const int sl = slot;
@@ -632,7 +640,7 @@ __global__ void __launch_bounds__(kGvThreads, 1) gemv_w4_kernel(const GemmArgs a
   int slot = 0, phase = 0;
   if (warp == kGvWarps) {
     if (elect_one()) {
-      gv_produce(a, u0, u1, m, stages, slot, phase, [] { pdl_wait(); });
+      gv_produce(a, u0, u1, m, stages, slot, phase, [] { pdl_wait(); }, kGvMaxStages, /*first_wait=*/true);
       // every stage of this CTA is in flight: pull the next GEMV's first weight bytes into L2
       // while this kernel's ring drains and its tail runs (the next kernel's CTAs cannot be
       // resident before this one exits, so their own first loads would start cold)
