@@ -20,3 +20,11 @@ for cl in c3:68 c4:68; do
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"gemm_kernel|gemm_chain|gemv_w4|attn_|embed_norm|argmax" -s $nl -c $nl --csv --log-file gpurun_out/launches_$cfg.csv python scripts/profile_step.py --config $cfg --steps 2 > gpurun_out/ncu1_$cfg.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gemm_chain|attn_decode" -s 4 -c 2 -o gpurun_out/full_$cfg python scripts/profile_step.py --config $cfg --steps 1 > gpurun_out/ncu2_$cfg.log 2>&1
 done
+# small-batch QSUN (8B W4, B=1, ctx 256): one step's launch list, per-CTA GEMV stamps
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"gemm_kernel|gemm_chain|gemv_w4|attn_|embed_norm|argmax" -s 195 -c 195 --csv --log-file gpurun_out/launches_w4_b1.csv python scripts/profile_step.py --config c4 --batch 1 --isl 256 --steps 2 > gpurun_out/ncu1_w4_b1.log 2>&1
+timeout 300 python scripts/gv_timeline.py > gpurun_out/gemv_w4_cta_stamps.txt 2>&1
+# per-CTA phase stamps of one layer chain (C2 bf16, C4 W4)
+python scripts/step_timeline.py --config c2 --layers 1 --stamp 4 > gpurun_out/tl_c2_chain.txt 2>&1
+python scripts/step_timeline.py --config c4 --layers 1 --stamp 4 > gpurun_out/tl_c4_chain.txt 2>&1
+# BASELINE-shape parity log
+timeout 1200 python -m pytest -q -s -m gpu tests/test_parity_baseline_gpu.py > gpurun_out/parity_baseline.log 2>&1; tail -1 gpurun_out/parity_baseline.log
