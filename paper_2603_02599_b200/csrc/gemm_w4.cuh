@@ -334,13 +334,54 @@ SUN_DEVICE void gv_range(const GemmArgs& a, int c, int G, int& u0, int& u1) {
   if (S == 0) {
     u0 = static_cast<int>(static_cast<long long>(c) * a.m_tiles / G) * KB;
     u1 = static_cast<int>(static_cast<long long>(c + 1) * a.m_tiles / G) * KB;
-  } else if (c < a.m_tiles * S) {
+  } else if (S > 0 && c < a.m_tiles * S) {
     const int t0 = c / S, r = c % S;
     u0 = t0 * KB + r * KB / S;
     u1 = t0 * KB + (r + 1) * KB / S;
+  } else if (S < 0) {  // balanced: the whole tiles (second range: gv_bal_range)
+    const int W = a.m_tiles / G;
+    u0 = c * W * KB;
+    u1 = (c + 1) * W * KB;
   } else {
     u0 = u1 = 0;
   }
+}
+
+// Balanced schedule (splits < 0): W = m_tiles / G whole tiles per CTA (first range), then the
+// R = m_tiles - W G remaining tiles' Ur = R KB blocks spread contiguously, CTA c taking
+// [B0 + f(c), B0 + f(c + 1)) with f(c) = c Ur / G and B0 = W G KB (second range). The host
+// picks it only when G <= Ur and ceil(Ur / G) <= KB, so every CTA has remainder work and its
+// range touches at most two tiles (partial pieces 0 and 1, parked in sk_part slots 2c, 2c + 1).
+// 8B gate_up at B <= 16 (224 tiles on 148 CTAs): 64 -> 49 K blocks for the busiest CTA.
+SUN_DEVICE int gv_bal_f(int c, int Ur, int G) { return static_cast<int>(static_cast<long long>(c) * Ur / G); }
+SUN_DEVICE void gv_bal_range(const GemmArgs& a, int c, int G, int& v0, int& v1) {
+  if (a.splits >= 0) {
+    v0 = v1 = 0;
+    return;
+  }
+  const int KB = a.ksteps, W = a.m_tiles / G, Ur = (a.m_tiles - W * G) * KB, B0 = W * G * KB;
+  v0 = B0 + gv_bal_f(c, Ur, G);
+  v1 = B0 + gv_bal_f(c + 1, Ur, G);
+}
+// Contributors [cf, cl] of a split tile and the sk_part slot of contributor c' (the tile's
+// last arrival adds the slots in contributor order: deterministic).
+SUN_DEVICE void gv_tile_contrib(const GemmArgs& a, int G, int tile, int& cf, int& cl) {
+  if (a.splits > 0) {
+    cf = tile * a.splits;
+    cl = cf + a.splits - 1;
+    return;
+  }
+  const int KB = a.ksteps, W = a.m_tiles / G, Ur = (a.m_tiles - W * G) * KB;
+  const int x0 = (tile - W * G) * KB, x1 = x0 + KB - 1;  // remainder-relative first / last block
+  // owner(x) = the largest c with f(c) <= x = ceil((x + 1) G / Ur) - 1
+  cf = static_cast<int>((static_cast<long long>(x0 + 1) * G + Ur - 1) / Ur) - 1;
+  cl = static_cast<int>((static_cast<long long>(x1 + 1) * G + Ur - 1) / Ur) - 1;
+}
+SUN_DEVICE int gv_part_slot(const GemmArgs& a, int G, int cp, int tile) {
+  if (a.splits > 0) return 2 * cp;
+  const int KB = a.ksteps, W = a.m_tiles / G, Ur = (a.m_tiles - W * G) * KB;
+  const int first_tile = (W * G * KB + gv_bal_f(cp, Ur, G)) / KB;
+  return 2 * cp + (first_tile == tile ? 0 : 1);
 }
 
 // Producer (one elected thread): the stages of [u0, u1) — up to kbs consecutive K blocks
@@ -426,15 +467,15 @@ SUN_DEVICE void gv_produce(const GemmArgs& a, int u0, int u1, const GvSmem& m, i
 // work's outputs.
 template <int EPI, int NB, typename Gate>
 SUN_DEVICE void gv_consume(const GemmArgs& a, int u0, int u1, const GvSmem& m, int stages, int& slot, int& phase,
-                           Gate gate, unsigned long long* pst = nullptr) {
+                           Gate gate, unsigned long long* pst = nullptr, bool meta = true) {
   const int kbs = a.wgroup, bn = a.bn, KB = a.ksteps, S = a.splits;
   const uint32_t sb = gv_stage_bytes(bn, kbs);
   const int warp = static_cast<int>(threadIdx.x >> 5), lane = threadIdx.x & 31;
-  const int c = static_cast<int>(blockIdx.x);
+  const int c = static_cast<int>(blockIdx.x), G = static_cast<int>(gridDim.x);
   float* T = m.T;
   gate();
   if (pst && threadIdx.x == 0) pst[0] = gtimer();
-  if (warp >= 2 && warp < 6) load_qkv_meta<EPI>(a, m.epi);  // epilogue group: positions / pages / r_b
+  if (meta && warp >= 2 && warp < 6) load_qkv_meta<EPI>(a, m.epi);  // epilogue group: positions / pages / r_b
   const int rq = warp & 3, ch = warp >> 2;  // row quarter, 32-k chunk of every block
   const int g = lane >> 2, t = lane & 3;
   const uint32_t ring_s = smem_u32(m.ring);
@@ -453,7 +494,7 @@ SUN_DEVICE void gv_consume(const GemmArgs& a, int u0, int u1, const GvSmem& m, i
     while (u < seg_end) {
       const int len = min(kbs, seg_end - u);
       mbar_wait(&m.full[slot], phase);
-      if (threadIdx.x == 0 && u == u0) {
+      if (threadIdx.x == 0 && u == u0 && meta) {
         SUN_STAMP(2);  // first stage landed
         if (pst) pst[1] = gtimer();
       }
@@ -554,12 +595,12 @@ SUN_DEVICE void gv_consume(const GemmArgs& a, int u0, int u1, const GvSmem& m, i
       continue;
     }
     if (!whole) {
-      // park the partial: [c][128 rows][16] fp32, 8 floats per thread (split schedule:
-      // one segment per CTA)
+      // park the partial: slot [2c + piece][128 rows][16] fp32, 8 floats per thread (split
+      // schedule: one segment per CTA; balanced: up to two)
       const int tid = threadIdx.x & 255, row = tid >> 1, h = (tid & 1) * 8;
       const bool mover = threadIdx.x < 256;  // 8 floats each
       if (mover) {
-        float* dst = a.sk_part + static_cast<long long>(c) * 2 * (kTileM * 16) + row * 16 + h;
+        float* dst = a.sk_part + static_cast<long long>(gv_part_slot(a, G, c, tile)) * (kTileM * 16) + row * 16 + h;
         __stcg(reinterpret_cast<float4*>(dst), make_float4(T[row * kGvTPitch + h], T[row * kGvTPitch + h + 1],
                                                            T[row * kGvTPitch + h + 2], T[row * kGvTPitch + h + 3]));
         __stcg(reinterpret_cast<float4*>(dst + 4), make_float4(T[row * kGvTPitch + h + 4], T[row * kGvTPitch + h + 5],
@@ -567,7 +608,8 @@ SUN_DEVICE void gv_consume(const GemmArgs& a, int u0, int u1, const GvSmem& m, i
         __threadfence();
       }
       gv_bar();
-      const int cf = tile * S, cl = tile * S + S - 1;
+      int cf, cl;
+      gv_tile_contrib(a, G, tile, cf, cl);
       if (threadIdx.x == 0) {
         const unsigned old = atomicAdd(a.sk_flags + tile, 1u);
         *m.flag = (old == static_cast<unsigned>(cl - cf)) ? 1 : 0;
@@ -583,8 +625,8 @@ SUN_DEVICE void gv_consume(const GemmArgs& a, int u0, int u1, const GvSmem& m, i
           float4 pp[4][2];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const float* src = a.sk_part + static_cast<long long>(c0 + e <= cl ? c0 + e : cl) * 2 * (kTileM * 16) +
-                               row * 16 + h;
+            const int slot_e = gv_part_slot(a, G, c0 + e <= cl ? c0 + e : cl, tile);
+            const float* src = a.sk_part + static_cast<long long>(slot_e) * (kTileM * 16) + row * 16 + h;
             pp[e][0] = __ldcg(reinterpret_cast<const float4*>(src));
             pp[e][1] = __ldcg(reinterpret_cast<const float4*>(src + 4));
           }

@@ -757,7 +757,16 @@ SunStatus run_gemv_w4(const void* packed, const void* scales, GemmArgs a, const 
   int grid;
   a.vcluster = 1;
   g_cluster = 1;
-  if (p.m_tiles >= slots) {
+  // SUN_GV_BALANCE: 1 (default) the balanced schedule (gv_bal_range) when whole tiles leave a
+  // remainder (8B gate_up: 224 tiles on 148 CTAs); 2 also in place of the per-tile split
+  // (every tile spread contiguously); 0 off
+  static const int bal_env = [] { const char* e = getenv("SUN_GV_BALANCE"); return e ? atoi(e) : 1; }();
+  const int W = p.m_tiles / slots, Ur = (p.m_tiles - W * slots) * p.ksteps;
+  const bool bal_ok = Ur >= slots && (Ur + slots - 1) / slots <= p.ksteps;
+  if (bal_ok && ((W >= 1 && bal_env >= 1) || (W == 0 && bal_env >= 2))) {
+    a.splits = -1;
+    grid = slots;
+  } else if (p.m_tiles >= slots) {
     a.splits = 0;
     grid = slots;
   } else {

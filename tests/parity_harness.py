@@ -45,6 +45,8 @@ CASES = {
     "c2": dict(base="llama3.2-1b", layers=16, bits=16, batch=64, n_models=4, lo=1984, hi=2045, steps=3),
     "c3": dict(base="llama3.1-8b", layers=2, bits=16, batch=64, n_models=8, lo=1024, hi=1279, steps=3),
     "c4": dict(base="llama3.1-8b", layers=2, bits=4, batch=128, n_models=8, lo=4000, hi=4094, steps=2),
+    # QSUN at decode batch 8: the small-batch W4 GEMV (balanced gate_up schedule, split O / down / QKV)
+    "c4s": dict(base="llama3.1-8b", layers=2, bits=4, batch=8, n_models=4, lo=200, hi=300, steps=3),
     "c5": dict(base="qwen2.5-14b", layers=2, bits=16, batch=32, n_models=16, lo=16300, hi=16382, steps=2),
 }
 

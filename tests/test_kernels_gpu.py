@@ -59,7 +59,7 @@ def test_gemm_deterministic_stream_k(cuda):
 
 
 @pytest.mark.parametrize("sched", ["0", "2", "vcl2", "novcl", "push", "nochain", "l2chain", "nogemv", "gvchain",
-                                   "tileready", "gvcluster"])
+                                   "tileready", "gvcluster", "gvbal0", "gvbal2"])
 def test_gemm_schedules_subprocess(sched):
     """The GEMM kernel tests and the end-to-end decode parity under the other
     schedules: 0 = cluster split-K / whole tiles only, 2 = stream-K on every
@@ -73,7 +73,9 @@ def test_gemm_schedules_subprocess(sched):
     rows on the tcgen05 W4 GEMM instead of the small-batch W4 GEMV, gvchain = the small-batch
     W4 GEMV as a persistent layer chain (opt-in), tileready = the bf16 chain's activation
     loads waiting for the producing tiles instead of the whole previous phase (opt-in), gvcluster =
-    the W4 GEMV's split tiles reduced over DSMEM in hardware clusters instead of through L2."""
+    the W4 GEMV's split tiles reduced over DSMEM in hardware clusters instead of through L2,
+    gvbal0 / gvbal2 = the W4 GEMV without its balanced schedule (whole tiles + remainder
+    spread contiguously) / with it also in place of the per-tile split."""
     import os
     import subprocess
     import sys
@@ -98,9 +100,12 @@ def test_gemm_schedules_subprocess(sched):
         env["SUN_CHAIN_TILE_READY"] = "1"
     elif sched == "gvcluster":
         env["SUN_GV_CLUSTER"] = "1"
+    elif sched in ("gvbal0", "gvbal2"):
+        env["SUN_GV_BALANCE"] = sched[-1]
     else:
         env["SUN_GEMM_SCHED"] = sched
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", "(gemm or tiny) and not subprocess",
+    sel = "(gemm or tiny or gemv) and not subprocess" if sched.startswith("gv") else "(gemm or tiny) and not subprocess"
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", sel,
                         os.path.join(here, "test_kernels_gpu.py"), os.path.join(here, "test_decode_parity_gpu.py")],
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
@@ -242,7 +247,7 @@ def test_gemm_w4_matches_dequantized_fp32(cuda, n_out, k, batch):
 
 @pytest.mark.parametrize("n_out,k,batch", [(256, 256, 1), (300, 512, 5), (768, 512, 8), (4096, 4096, 9),
                                            (6144, 4096, 16), (28672, 4096, 16), (4096, 14336, 1), (1536, 14336, 3),
-                                           (128, 128, 2)])
+                                           (128, 128, 2), (24576, 4096, 4)])
 def test_gemv_w4_matches_group_scaled_fp64(cuda, n_out, k, batch):
     """Small-batch W4 GEMV (stream-K, L2 partials): exactly sum_g s_g * sum_k q x up to
     fp32 summation order; and within the bf16 rounding of q*s of the tcgen05 operand."""
