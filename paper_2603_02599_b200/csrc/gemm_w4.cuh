@@ -673,8 +673,14 @@ __global__ void __launch_bounds__(kGvThreads, 1) gemv_w4_kernel(const GemmArgs a
   const int stages = a.stages;
   const GvSmem m = gv_smem(smem, stages, gv_stage_bytes(a.bn, a.wgroup));
   const int warp = warp_id_sync();
-  int u0, u1;
+  int u0, u1, v0, v1;  // v: the balanced schedule's remainder range (empty otherwise)
   gv_range(a, static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), u0, u1);
+  gv_bal_range(a, static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), v0, v1);
+  if (u0 == u1) {
+    u0 = v0;
+    u1 = v1;
+    v0 = v1 = 0;
+  }
   if (threadIdx.x == 0) SUN_STAMP(0);
   gv_init_ring(m, stages);
   pdl_launch_dependents();
@@ -683,6 +689,7 @@ __global__ void __launch_bounds__(kGvThreads, 1) gemv_w4_kernel(const GemmArgs a
   if (warp == kGvWarps) {
     if (elect_one()) {
       gv_produce(a, u0, u1, m, stages, slot, phase, [] { pdl_wait(); }, kGvMaxStages, /*first_wait=*/true);
+      if (v0 < v1) gv_produce(a, v0, v1, m, stages, slot, phase, [] {}, 0);
       // every stage of this CTA is in flight: pull the next GEMV's first weight bytes into L2
       // while this kernel's ring drains and its tail runs (the next kernel's CTAs cannot be
       // resident before this one exits, so their own first loads would start cold)
@@ -695,6 +702,7 @@ __global__ void __launch_bounds__(kGvThreads, 1) gemv_w4_kernel(const GemmArgs a
     }
   } else {
     gv_consume<EPI, NB>(a, u0, u1, m, stages, slot, phase, [] { pdl_wait(); });
+    if (v0 < v1) gv_consume<EPI, NB>(a, v0, v1, m, stages, slot, phase, [] {}, nullptr, /*meta=*/false);
   }
   if (threadIdx.x == 64) SUN_STAMP(5);  // (epilogue warp) last epilogue done
   if (threadIdx.x == 0) SUN_STAMP(6);
