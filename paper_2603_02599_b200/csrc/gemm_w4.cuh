@@ -710,6 +710,233 @@ __global__ void __launch_bounds__(kGvThreads, 1) gemv_w4_kernel(const GemmArgs a
 }
 
 // ---------------------------------------------------------------------------
+// GEMV with a dedicated epilogue group (gemv_w4a_kernel, SUN_GV_ASYNC_EPI): warps 2..5 only
+// run the epilogue (and the split partials' park / last-arrival reduction); the 16 compute
+// warps (0, 1, 6..19) reduce a segment into T, hand it over through a named barrier and go
+// straight on with the next segment's stages — in gemv_w4_kernel warps 2..5 are compute
+// warps too, so a tile's epilogue, and a split segment's L2 round trips, stall the ring's
+// consumers (which pace the kernel). One T buffer: the epilogue warps copy their row into
+// registers and release it at once. Warp 20 is the producer.
+// ---------------------------------------------------------------------------
+constexpr int kGvaThreads = 21 * 32;
+constexpr int kGvaProducerWarp = 20;
+SUN_DEVICE void gva_bar_sync(int id) { asm volatile("bar.sync %0, 640;" ::"r"(id) : "memory"); }
+SUN_DEVICE void gva_bar_arrive(int id) { asm volatile("bar.arrive %0, 640;" ::"r"(id) : "memory"); }
+constexpr int kGvaFull = 4, kGvaEmpty = 5;  // named barriers: T holds a segment / T was read
+
+// segments (one tile's part of a range) of [u0, u1) then [v0, v1), in order
+template <typename F>
+SUN_DEVICE void gv_for_segments(int KB, int u0, int u1, int v0, int v1, F f) {
+#pragma unroll 1
+  for (int r = 0; r < 2; ++r) {
+    const int a0 = r ? v0 : u0, a1 = r ? v1 : u1;
+    for (int u = a0; u < a1;) {
+      const int tile = u / KB;
+      const int e = min(a1, (tile + 1) * KB);
+      f(tile, u, e, u == tile * KB && e == (tile + 1) * KB);
+      u = e;
+    }
+  }
+}
+
+template <int NB>
+SUN_DEVICE void gva_math(const GemmArgs& a, int u0, int u1, int v0, int v1, const GvSmem& m, int stages) {
+  const int kbs = a.wgroup, bn = a.bn, KB = a.ksteps;
+  const uint32_t sb = gv_stage_bytes(bn, kbs);
+  const int warp = static_cast<int>(threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int ci = warp < 2 ? warp : warp - 4;  // compute index 0..15
+  const int rq = ci & 3, ch = ci >> 2;
+  const int g = lane >> 2, t = lane & 3;
+  float* T = m.T;
+  pdl_wait();
+  const uint32_t ring_s = smem_u32(m.ring);
+  const bool fast = kbs == kGvFastKbs && bn == kGvFastBn;
+  const GvBase<NB> base = gv_base<NB>(ring_s, rq, ch, lane);
+  int slot = 0, phase = 0, i = 0;
+  gv_for_segments(KB, u0, u1, v0, v1, [&](int tile, int s0, int s1, bool whole) {
+    float acc[kGvMT][NB][4];
+#pragma unroll
+    for (int mt = 0; mt < kGvMT; ++mt)
+#pragma unroll
+      for (int j = 0; j < NB; ++j) acc[mt][j][0] = acc[mt][j][1] = acc[mt][j][2] = acc[mt][j][3] = 0.f;
+    for (int u = s0; u < s1;) {
+      const int len = min(kbs, s1 - u);
+      mbar_wait(&m.full[slot], phase);
+      if (threadIdx.x == 0 && u == u0) SUN_STAMP(2);  // first stage landed
+      const uint32_t st = ring_s + slot * sb;
+      if (fast && len == kGvFastKbs) {
+        const uint32_t so = slot * sb;
+        GvFrag<NB> f2[2];
+        gv_load_fast<NB, 0>(f2[0], base, so);
+        gv_load_fast<NB, 1>(f2[1], base, so);
+        gv_math<NB, 2>(f2, acc);
+        gv_load_fast<NB, 2>(f2[0], base, so);
+        gv_load_fast<NB, 3>(f2[1], base, so);
+        gv_math<NB, 2>(f2, acc);
+      } else {
+        auto ld = [&](GvFrag<NB>& f, int ib) {
+          gv_load<NB>(f, st + ib * kW4PackedBytes, st + kbs * kW4PackedBytes + ib * 256,
+                      st + kbs * (kW4PackedBytes + 256u) + ib * bn * 256, bn, rq, ch, lane);
+        };
+        int ib = 0;
+        for (; ib + 1 < len; ib += 2) {
+          GvFrag<NB> f2[2];
+          ld(f2[0], ib);
+          ld(f2[1], ib + 1);
+          gv_math<NB, 2>(f2, acc);
+        }
+        if (ib < len) {
+          GvFrag<NB> f1[1];
+          ld(f1[0], ib);
+          gv_math<NB, 1>(f1, acc);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&m.empty[slot]);
+      u += len;
+      if (++slot == stages) {
+        slot = 0;
+        phase ^= 1;
+      }
+    }
+    if (threadIdx.x == 0 && s1 == (v1 > v0 ? v1 : u1)) SUN_STAMP(3);  // last stage consumed
+    if (i > 0) gva_bar_sync(kGvaEmpty);  // the epilogue warps hold the previous segment's rows
+    // fragments -> T[row][batch] (as gv_consume: chunk 0 stores, chunks 1..3 add in order)
+    for (int cc = 0; cc < 4; ++cc) {
+      if (ch == cc) {
+#pragma unroll
+        for (int mt = 0; mt < kGvMT; ++mt) {
+          const int r = 32 * rq + 16 * mt + g;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int jj = j < NB ? j : 0;
+            const bool have = j < NB;
+            float* p0 = T + r * kGvTPitch + 8 * j + t;
+            float* p1 = T + (r + 8) * kGvTPitch + 8 * j + t;
+            const float w0 = have ? acc[mt][jj][0] : 0.f, w1 = have ? acc[mt][jj][1] : 0.f;
+            const float w2 = have ? acc[mt][jj][2] : 0.f, w3 = have ? acc[mt][jj][3] : 0.f;
+            if (cc == 0) {
+              p0[0] = w0; p0[4] = w1; p1[0] = w2; p1[4] = w3;
+            } else {
+              p0[0] += w0; p0[4] += w1; p1[0] += w2; p1[4] += w3;
+            }
+          }
+        }
+      }
+      gv_bar();
+    }
+    gva_bar_arrive(kGvaFull);
+    ++i;
+    (void)tile;
+    (void)whole;
+  });
+}
+
+template <int EPI>
+SUN_DEVICE void gva_epilogue(const GemmArgs& a, int u0, int u1, int v0, int v1, const GvSmem& m) {
+  const int KB = a.ksteps, G = static_cast<int>(gridDim.x), c = static_cast<int>(blockIdx.x);
+  const int row_local = (static_cast<int>(threadIdx.x >> 5) - 2) * 32 + (threadIdx.x & 31);
+  pdl_wait();
+  load_qkv_meta<EPI>(a, m.epi);  // positions / pages / r_b (ends with the group barrier)
+  int nseg = 0;
+  gv_for_segments(KB, u0, u1, v0, v1, [&](int, int, int, bool) { ++nseg; });
+  int i = 0;
+  gv_for_segments(KB, u0, u1, v0, v1, [&](int tile, int, int, bool whole) {
+    gva_bar_sync(kGvaFull);
+    float v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = m.T[row_local * kGvTPitch + j];
+    if (i + 1 < nseg) gva_bar_arrive(kGvaEmpty);
+    ++i;
+    if (!whole) {
+      // park this segment's rows (slot [2c + piece][128][16] fp32), count the tile; its last
+      // contributor adds the slots in contributor order (deterministic) and runs the epilogue
+      float* dst = a.sk_part + static_cast<long long>(gv_part_slot(a, G, c, tile)) * (kTileM * 16) + row_local * 16;
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) __stcg(reinterpret_cast<float4*>(dst + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+      __threadfence();
+      epi_bar();
+      int cf, cl;
+      gv_tile_contrib(a, G, tile, cf, cl);
+      if (epi_lead_thread()) {
+        const unsigned old = atomicAdd(a.sk_flags + tile, 1u);
+        *m.flag = (old == static_cast<unsigned>(cl - cf)) ? 1 : 0;
+      }
+      epi_bar();
+      if (*m.flag == 0) return;
+      __threadfence();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = 0.f;
+      for (int c0 = cf; c0 <= cl; c0 += 2) {  // two partials' loads in flight per round trip
+        float4 pp[2][4];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int slot_e = gv_part_slot(a, G, c0 + e <= cl ? c0 + e : cl, tile);
+          const float* src = a.sk_part + static_cast<long long>(slot_e) * (kTileM * 16) + row_local * 16;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) pp[e][q] = __ldcg(reinterpret_cast<const float4*>(src + 4 * q));
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (c0 + e > cl) break;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            v[4 * q] += pp[e][q].x; v[4 * q + 1] += pp[e][q].y; v[4 * q + 2] += pp[e][q].z; v[4 * q + 3] += pp[e][q].w;
+          }
+        }
+      }
+      if (epi_lead_thread()) a.sk_flags[tile] = 0u;  // self-resetting for the next use
+    }
+    epi_chunk<EPI>(a, tile, row_local, 0, v, m.epi);
+  });
+}
+
+template <int EPI, int NB>
+__global__ void __launch_bounds__(kGvaThreads, 1) gemv_w4a_kernel(const GemmArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  tl_begin(a.tl, a.tl_idx);
+  const int stages = a.stages;
+  const GvSmem m = gv_smem(smem, stages, gv_stage_bytes(a.bn, a.wgroup));
+  const int warp = warp_id_sync();
+  int u0, u1, v0, v1;
+  gv_range(a, static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), u0, u1);
+  gv_bal_range(a, static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), v0, v1);
+  if (u0 == u1) {
+    u0 = v0;
+    u1 = v1;
+    v0 = v1 = 0;
+  }
+  if (threadIdx.x == 0) SUN_STAMP(0);
+  if (warp == kGvaProducerWarp && elect_one()) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&m.full[s], 1);
+      mbar_init(&m.empty[s], kGvWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) SUN_STAMP(1);
+  if (warp == kGvaProducerWarp) {
+    if (elect_one()) {
+      int slot = 0, phase = 0;
+      gv_produce(a, u0, u1, m, stages, slot, phase, [] { pdl_wait(); }, kGvMaxStages, /*first_wait=*/true);
+      if (v0 < v1) gv_produce(a, v0, v1, m, stages, slot, phase, [] {}, 0);
+      prefetch_next_weights(a);
+    }
+    __syncwarp();
+  } else if (warp >= 2 && warp < 6) {
+    gva_epilogue<EPI>(a, u0, u1, v0, v1, m);
+  } else {
+    gva_math<NB>(a, u0, u1, v0, v1, m, stages);
+  }
+  if (threadIdx.x == 64) SUN_STAMP(5);  // (epilogue warp) last epilogue done
+  if (threadIdx.x == 0) SUN_STAMP(6);
+  tl_end(a.tl, a.tl_idx);
+}
+
+// ---------------------------------------------------------------------------
 // Small-batch QSUN layer chain: O -> gate_up -> down -> next layer's QKV as GEMV phases of
 // one persistent launch (one CTA per SM, all resident). The ring and its producer run across
 // the phase boundaries: the next phase's weight and scale stages stream in while the compute

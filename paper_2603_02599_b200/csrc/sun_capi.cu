@@ -203,6 +203,14 @@ void init_kernel_attrs() {
     set_max_smem(gemv_w4_kernel<EPI_QKV_ROPE, 2>);
     set_max_smem(gemv_w4_kernel<EPI_SWIGLU, 1>);
     set_max_smem(gemv_w4_kernel<EPI_SWIGLU, 2>);
+    set_max_smem(gemv_w4a_kernel<EPI_STORE_F32, 1>);
+    set_max_smem(gemv_w4a_kernel<EPI_STORE_F32, 2>);
+    set_max_smem(gemv_w4a_kernel<EPI_RESID_ADD, 1>);
+    set_max_smem(gemv_w4a_kernel<EPI_RESID_ADD, 2>);
+    set_max_smem(gemv_w4a_kernel<EPI_QKV_ROPE, 1>);
+    set_max_smem(gemv_w4a_kernel<EPI_QKV_ROPE, 2>);
+    set_max_smem(gemv_w4a_kernel<EPI_SWIGLU, 1>);
+    set_max_smem(gemv_w4a_kernel<EPI_SWIGLU, 2>);
     set_max_smem(gemv_chain_w4_kernel<1>);
     set_max_smem(gemv_chain_w4_kernel<2>);
     set_max_smem(gemm_chain_kernel);
@@ -757,10 +765,12 @@ SunStatus run_gemv_w4(const void* packed, const void* scales, GemmArgs a, const 
   int grid;
   a.vcluster = 1;
   g_cluster = 1;
-  // SUN_GV_BALANCE: 1 (default) the balanced schedule (gv_bal_range) when whole tiles leave a
-  // remainder (8B gate_up: 224 tiles on 148 CTAs); 2 also in place of the per-tile split
-  // (every tile spread contiguously); 0 off
-  static const int bal_env = [] { const char* e = getenv("SUN_GV_BALANCE"); return e ? atoi(e) : 1; }();
+  // SUN_GV_BALANCE (default 0: off): 1 the balanced schedule (gv_bal_range) when whole tiles
+  // leave a remainder (8B gate_up: 224 tiles on 148 CTAs), 2 also in place of the per-tile
+  // split. Measured slower (profiles/r02/gv_balance_ab.txt, same box): gate_up 24.1 -> 28.7 us
+  // at B=1, W4 B=1 step 2.44 -> 2.62 ms (2: 3.13) — every CTA now streams, and the mid-stream
+  // partial park / reduction round trips stall the compute warps that also run the epilogue
+  static const int bal_env = [] { const char* e = getenv("SUN_GV_BALANCE"); return e ? atoi(e) : 0; }();
   const int W = p.m_tiles / slots, Ur = (p.m_tiles - W * slots) * p.ksteps;
   const bool bal_ok = Ur >= slots && (Ur + slots - 1) / slots <= p.ksteps;
   if (bal_ok && ((W >= 1 && bal_env >= 1) || (W == 0 && bal_env >= 2))) {
@@ -776,6 +786,13 @@ SunStatus run_gemv_w4(const void* packed, const void* scales, GemmArgs a, const 
       a.vcluster = 0;
       g_cluster = unsigned(a.splits);
     }
+  }
+  // SUN_GV_ASYNC_EPI (default 1): the kernel with a dedicated epilogue group (gemv_w4a_kernel)
+  static const int async_env = [] { const char* e = getenv("SUN_GV_ASYNC_EPI"); return e ? atoi(e) : 1; }();
+  if (async_env && a.vcluster) {
+    if (a.batch <= 8) SUN_CUDA(launch(gemv_w4a_kernel<EPI, 1>, dim3(grid), dim3(kGvaThreads), c.smem, st, pdl, a));
+    else SUN_CUDA(launch(gemv_w4a_kernel<EPI, 2>, dim3(grid), dim3(kGvaThreads), c.smem, st, pdl, a));
+    return SUN_OK;
   }
   if (a.batch <= 8) SUN_CUDA(launch(gemv_w4_kernel<EPI, 1>, dim3(grid), dim3(kGvThreads), c.smem, st, pdl, a));
   else SUN_CUDA(launch(gemv_w4_kernel<EPI, 2>, dim3(grid), dim3(kGvThreads), c.smem, st, pdl, a));
