@@ -668,7 +668,11 @@ struct GvCfg {
   int kbs, stages, per_sm;
   size_t smem;
 };
-GvCfg gv_cfg(int bn) {
+int gv_async_epi() {  // SUN_GV_ASYNC_EPI (default 1): the kernel with a dedicated epilogue group
+  static const int v = [] { const char* e = getenv("SUN_GV_ASYNC_EPI"); return e ? atoi(e) : 1; }();
+  return v;
+}
+GvCfg gv_cfg(int bn, bool async = false) {
   static const int env_kbs = [] { const char* e = getenv("SUN_GV_KBS"); return e ? atoi(e) : 0; }();
   static const int env_st = [] { const char* e = getenv("SUN_GV_STAGES"); return e ? atoi(e) : 0; }();
   static const int env_ps = [] { const char* e = getenv("SUN_GV_CTAS_PER_SM"); return e ? atoi(e) : 0; }();
@@ -677,6 +681,9 @@ GvCfg gv_cfg(int bn) {
   c.per_sm = env_ps > 0 ? env_ps : 1;
   const int budget = kSmemPerSm / c.per_sm - int(gv_smem_bytes(bn, c.kbs, 0)) - 1024;
   c.stages = std::max(2, std::min(kGvMaxStages, budget / int(gv_stage_bytes(bn, c.kbs))));
+  // gemv_w4a_kernel: a 2-stage ring (8 K blocks in flight) measured best (8B W4 B=1 ctx 256:
+  // 2 / 3 / 4 stages 2.33 / 2.34 / 2.39 ms, profiles/r02/gv_async_stages.txt)
+  if (async) c.stages = std::min(c.stages, 2);
   if (env_st > 0) c.stages = std::min(env_st, kGvMaxStages);
   c.smem = gv_smem_bytes(bn, c.kbs, c.stages);
   return c;
@@ -746,7 +753,9 @@ SunStatus run_gemv_w4(const void* packed, const void* scales, GemmArgs a, const 
                       unsigned* cnt, cudaStream_t st, bool pdl, int num_sms) {
   if (a.bn != 16 || a.batch > kGemvKernelMaxBatch) return fail(SUN_ERR_VALUE, "W4 GEMV takes batches of <= 16 rows");
   if (p.m_tiles > kGvMaxTiles) return fail(SUN_ERR_UNSUPPORTED, "W4 GEMV: %d tiles > %d", p.m_tiles, kGvMaxTiles);
-  const GvCfg c = gv_cfg(a.bn);
+  static const int cl_env = [] { const char* e = getenv("SUN_GV_CLUSTER"); return e ? atoi(e) : 0; }();
+  const bool async = gv_async_epi() && !cl_env;  // (the DSMEM cluster reduction is gemv_w4_kernel's)
+  const GvCfg c = gv_cfg(a.bn, async);
   a.w4_packed = static_cast<const uint8_t*>(packed);
   a.w4_scales = static_cast<const __nv_bfloat16*>(scales);
   a.wgroup = c.kbs;
@@ -760,7 +769,6 @@ SunStatus run_gemv_w4(const void* packed, const void* scales, GemmArgs a, const 
   // partials reduced through L2 by the tile's last arrival — or (SUN_GV_CLUSTER=1, off: measured
   // slower, the 8B O / down GEMV tails 2.6 -> 7.4 us, W4 B=1 step 2.35 -> 2.52 ms) one hardware
   // cluster of S CTAs per tile reducing over DSMEM between two cluster barriers
-  static const int cl_env = [] { const char* e = getenv("SUN_GV_CLUSTER"); return e ? atoi(e) : 0; }();
   const int slots = std::min(num_sms * c.per_sm, kMaxGemmCtas);
   int grid;
   a.vcluster = 1;
@@ -787,9 +795,7 @@ SunStatus run_gemv_w4(const void* packed, const void* scales, GemmArgs a, const 
       g_cluster = unsigned(a.splits);
     }
   }
-  // SUN_GV_ASYNC_EPI (default 1): the kernel with a dedicated epilogue group (gemv_w4a_kernel)
-  static const int async_env = [] { const char* e = getenv("SUN_GV_ASYNC_EPI"); return e ? atoi(e) : 1; }();
-  if (async_env && a.vcluster) {
+  if (async && a.vcluster) {
     if (a.batch <= 8) SUN_CUDA(launch(gemv_w4a_kernel<EPI, 1>, dim3(grid), dim3(kGvaThreads), c.smem, st, pdl, a));
     else SUN_CUDA(launch(gemv_w4a_kernel<EPI, 2>, dim3(grid), dim3(kGvaThreads), c.smem, st, pdl, a));
     return SUN_OK;
