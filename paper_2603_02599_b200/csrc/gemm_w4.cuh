@@ -932,6 +932,7 @@ __global__ void __launch_bounds__(kGvaThreads, 1) gemv_w4a_kernel(const GemmArgs
     gva_math<NB>(a, u0, u1, v0, v1, m, stages);
   }
   if (threadIdx.x == 64) SUN_STAMP(5);  // (epilogue warp) last epilogue done
+  if (a.tl != nullptr || a.stamps != nullptr) __syncthreads();  // profiling: the exit stamps after every role
   if (threadIdx.x == 0) SUN_STAMP(6);
   tl_end(a.tl, a.tl_idx);
 }

@@ -717,7 +717,11 @@ int max_active_clusters_gv(unsigned size, size_t smem) {
 
 bool use_gemv(bool w4, int batch) {
   static const int v = [] { const char* e = getenv("SUN_W4_GEMV"); return e ? atoi(e) : 1; }();
-  return w4 && v != 0 && batch <= kGemvMaxBatch;
+  static const int mb = [] {  // SUN_GV_MAX_BATCH: largest decode batch on the GEMV (kernel: <= 16)
+    const char* e = getenv("SUN_GV_MAX_BATCH");
+    return e ? std::max(1, std::min(atoi(e), kGemvKernelMaxBatch)) : kGemvMaxBatch;
+  }();
+  return w4 && v != 0 && batch <= mb;
 }
 
 // L2 prefetch budget per next-GEMV CTA (SUN_GV_PREFETCH_KB, default 0: 32-128 KB measured
