@@ -275,9 +275,11 @@ SUN_DEVICE void gv_math(const GvFrag<NB> (&f)[NBLK], float (&acc)[kGvMT][NB][4])
   for (int step = 0; step < 2; ++step) {
 #pragma unroll
     for (int b = 0; b < NBLK; ++b) {
+#ifndef SUN_GV_PROBE_NOCX  // probe: no -136 sum x MMAs (timing only, results invalid)
 #pragma unroll
       for (int j = 0; j < NB; ++j)
         mma_16816_q(cx[b][j], kOnes, kOnes, kOnes, kOnes, f[b].x[j][2 * step], f[b].x[j][2 * step + 1]);
+#endif
 #pragma unroll
       for (int m = 0; m < kGvMT; ++m) {
         const uint32_t lo = f[b].wq[2 * m], hi = f[b].wq[2 * m + 1];
