@@ -547,8 +547,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_chain_kernel(const __gri
       epi_pair_bar();
       if (threadIdx.x == 64) {  // this CTA's outputs of phase p are written
         SUN_CSTAMP(4 * p + 3);
-        __threadfence();
-        atomicAdd(c.bar, 1u);
+        count_arrive_release(c.bar);
       }
     }
   }
@@ -1022,8 +1021,7 @@ __global__ void __launch_bounds__(kW4Threads, 1) gemm_chain_w4_kernel(const __gr
         if (p < 3)
 #endif
         SUN_CSTAMP(4 * p + 3);
-        __threadfence();
-        atomicAdd(c.bar, 1u);
+        count_arrive_release(c.bar);
       }
     }
   } else if (warp < kXProd) {

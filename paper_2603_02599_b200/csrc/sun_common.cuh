@@ -130,6 +130,18 @@ SUN_DEVICE void tl_end(unsigned long long* tl, int idx) {
 // Programmatic dependent launch
 // ----------------------------------------------------------------------------
 SUN_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Phase-count arrival: the writes this CTA made (ordered before it by a CTA barrier) become
+// visible at GPU scope before the count. -DSUN_COUNT_RELEASE: one release reduction instead
+// of fence.sc + atomic (measured neutral on C2 / C3 / C4 same box, scripts/gpu_lib_ab.sh)
+SUN_DEVICE void count_arrive_release(unsigned* p) {
+#ifdef SUN_COUNT_RELEASE
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+#else
+  __threadfence();
+  atomicAdd(p, 1u);
+#endif
+}
 SUN_DEVICE void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
