@@ -48,6 +48,12 @@ struct AttnArgs {
   // kernel writes only each row's last page: the other pages are staged before
   // griddepcontrol.wait, i.e. while the QKV grid is still finishing (PDL)
   int prestage;
+  // non-null (decode, layer >= 1, prestage): per-tile writer counts of this layer's QKV output,
+  // published by the previous layer chain's epilogues; the kernel waits for its Q / K / V tiles
+  // (>= ready_writers each) instead of the chain grid, and runs griddepcontrol.wait before it
+  // exits so that completion still orders the chain before the next kernel
+  const unsigned* qkv_ready;
+  unsigned ready_writers;
   int max_ctx;             // tokens a block-table row can address (decoder max_context): positions
                            // outside [0, max_ctx) are clamped, so a bad position cannot read past
                            // its block-table row (sun_decode_step flags it in the error word)
@@ -152,7 +158,31 @@ __global__ void __launch_bounds__(128)
     if (pre)  // pages before the row's last one: untouched by this step's KV append
       for (; ipre < npre && p0 + warp + ipre * C::kWarps < n_pages - 1; ++ipre) issue(ipre);
   }
-  if (pre) {
+  const bool tile_ready = pre && a.qkv_ready != nullptr;
+  if (tile_ready) {
+    // q and the appended K/V of this (kv head, group) are written once their QKV tiles are
+    // published (tile = 128 rows of [Q heads | K heads | V heads] x head_dim)
+    if (threadIdx.x < 3) {
+      const int qd = a.n_q_heads * D, kd = a.n_kv_heads * D;
+      int lo, hi;
+      if (threadIdx.x == 0) {
+        lo = (kvh * G * D) / 128;
+        hi = ((kvh + 1) * G * D - 1) / 128;
+      } else {
+        lo = hi = (qd + (threadIdx.x == 2 ? kd : 0) + kvh * D) / 128;
+      }
+      const unsigned long long t0 = global_timer_ns();
+      for (int t = lo; t <= hi; ++t) {
+        while (ld_acquire_u32(a.qkv_ready + t) < a.ready_writers) {
+          __nanosleep(32);
+          if (global_timer_ns() - t0 > 2000000000ull) __trap();  // (never: the chain is resident)
+        }
+      }
+    }
+    __syncthreads();
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy stores -> TMA page loads
+    pdl_launch_dependents();
+  } else if (pre) {
     pdl_wait();  // q and the appended K/V are the QKV kernel's outputs
     pdl_launch_dependents();
   }
@@ -333,6 +363,7 @@ __global__ void __launch_bounds__(128)
       }
     }
   }
+  if (tile_ready) pdl_wait();  // completion of this grid still implies the chain's (PDL ordering)
   tl_end(a.tl, a.tl_idx);
 }
 

@@ -38,6 +38,11 @@ struct ChainArgs {
   unsigned* ready;  // bf16 chain, non-null: [kChainMaxPhases][kChainReadyTiles] per-tile counts of the
                     // CTAs that finished writing a phase's output tile; the next phase's activation
                     // stages wait only for the tiles they read (zeroed by the last CTA out)
+  unsigned* qkv_ready;  // non-null: the last (QKV) phase publishes its tiles here (per-tile writer
+                        // counts) for the next layer's attention (SUN_ATTN_TILE_READY)
+  unsigned* qkv_reset;  // non-null: this layer's counters, read by the attention that precedes this
+                        // chain: zeroed once that attention has completed (after griddepcontrol.wait)
+  int qkv_reset_n;
   unsigned long long* tl;
   int tl_idx;
 };
@@ -78,6 +83,7 @@ SUN_DEVICE PhaseSched phase_sched(const GemmArgs& a) {
 // an error instead of hanging the GPU.
 constexpr unsigned long long kChainWatchdogNs = 2000000000ull;
 constexpr int kChainReadyTiles = 1024;
+constexpr int kQkvReadyStride = 256;  // per-layer QKV tile counters of the attention hand-off
 
 // Per-tile readiness (bf16 chain): the activation producer of phase p waits for the
 // producer tiles of phase p - 1 that its K steps read, instead of the whole phase. `rp`
@@ -438,7 +444,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_chain_kernel(const __gri
         const int ptiles = p > 0 ? c.ph[p - 1].m_tiles : 0;
         int rp = 0;
         if (!wprod) {
-          if (p == 0) pdl_wait();
+          if (p == 0) {
+            pdl_wait();
+            if (c.qkv_reset != nullptr)  // the previous attention has completed: its counters are free
+              for (int t = static_cast<int>(blockIdx.x); t < c.qkv_reset_n; t += G) c.qkv_reset[t] = 0u;
+          }
           else if (!tiles_wait) chain_wait_phase(c.bar, G * p);
           SUN_CSTAMP(4 * p);
         }
@@ -537,7 +547,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_chain_kernel(const __gri
         if (threadIdx.x == 64) chain_wait_phase(c.bar, G * p);
         epi_pair_bar();
       }
-      unsigned* ready_p = (c.ready != nullptr && p + 1 < c.nph) ? c.ready + p * kChainReadyTiles : nullptr;
+      unsigned* ready_p = (c.ready != nullptr && p + 1 < c.nph) ? c.ready + p * kChainReadyTiles
+                          : (p + 1 == c.nph && c.qkv_ready != nullptr && c.epi[p] == EPI_QKV_ROPE) ? c.qkv_ready
+                                                                                                  : nullptr;
       switch (c.epi[p]) {
         case EPI_RESID_ADD: chain_epilogue_phase<EPI_RESID_ADD>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase, recv, &rbar[p], ready_p); break;
         case EPI_SWIGLU: chain_epilogue_phase<EPI_SWIGLU>(a, ps, epi, tmem_base, tfull, tempty, buf, tphase, recv, &rbar[p], ready_p); break;

@@ -354,7 +354,7 @@ int gemm_sched() {
 // Workspace layout shared by sizing and creation.
 struct WsLayout {
   size_t resid, xn, q, attn, act, part_o, part_ml, attn_cnt, ss, amax_val, amax_idx, logits, sk_part, sk_flags,
-      chain_bar, err, gv_part, gv_cnt, total;
+      chain_bar, err, gv_part, gv_cnt, qkv_ready, total;
   int max_splits;
 };
 
@@ -394,6 +394,7 @@ WsLayout layout_ws(const SunDecoderDims& d, int max_batch) {
   w.err = take(64);
   w.gv_part = take(gv_part_bytes());
   w.gv_cnt = take(kGvMaxTiles * 4);
+  w.qkv_ready = take(size_t(d.n_layers) * kQkvReadyStride * 4);
   w.total = off;
   return w;
 }
@@ -468,6 +469,7 @@ struct SunDecoder {
   float* sk_part;
   unsigned* sk_flags;
   unsigned* chain_bar;
+  unsigned* qkv_ready;  // [layer][kQkvReadyStride] QKV tiles written by the previous layer's chain
   unsigned* err;  // SUN_STEP_ERR_* bits (sun_decoder_status)
   float* gv_part;     // small-batch W4 GEMV partials / per-tile counters
   unsigned* gv_cnt;
@@ -992,7 +994,8 @@ SunStatus run_chain_w4(GemmArgs* ph, const int* epi, const GemmPlan* plans, cons
 }
 
 SunStatus run_chain(GemmArgs* ph, const int* epi, const GemmPlan* plans, const void* const* wblk, int nph,
-                    unsigned* bar, cudaStream_t st, bool pdl, int num_sms) {
+                    unsigned* bar, cudaStream_t st, bool pdl, int num_sms, unsigned* qkv_ready = nullptr,
+                    unsigned* qkv_reset = nullptr, int* qkv_writers = nullptr) {
   ChainArgs c;
   memset(&c, 0, sizeof(c));
   const int bn = ph[0].bn;
@@ -1044,6 +1047,13 @@ SunStatus run_chain(GemmArgs* ph, const int* epi, const GemmPlan* plans, const v
   bool tr = tr_env != 0;
   for (int i = 0; i < nph; ++i) tr = tr && plans[i].m_tiles <= kChainReadyTiles;
   if (tr) c.ready = bar + 16;
+  // per-tile hand-off of the last (QKV) phase to the next layer's attention (SUN_ATTN_TILE_READY)
+  if (qkv_ready && epi[nph - 1] == EPI_QKV_ROPE && plans[nph - 1].m_tiles <= kQkvReadyStride) {
+    c.qkv_ready = qkv_ready;
+    if (qkv_writers) *qkv_writers = c.ph[nph - 1].splits > 1 ? c.ph[nph - 1].splits : 1;
+  }
+  c.qkv_reset = qkv_reset;
+  c.qkv_reset_n = kQkvReadyStride;
   tl_assign(c);
   if (g_tl.stamps != nullptr && c.tl != nullptr && c.tl_idx == g_tl.stamp_idx) c.stamps = g_tl.stamps;
   g_cluster = c.hw ? 4u : 1u;
@@ -1059,6 +1069,14 @@ int attn_fused_combine() {
     const char* e = getenv("SUN_ATTN_FUSED_COMBINE");
     return e ? atoi(e) : 0;
   }();
+  return v;
+}
+
+// The decode attention of layer l >= 1 starts on the QKV tiles it reads as soon as the previous
+// layer chain's epilogues publish them (per-tile counters) instead of waiting for that chain
+// grid to complete (SUN_ATTN_TILE_READY, bf16 layer chain only).
+int attn_tile_ready() {
+  static const int v = [] { const char* e = getenv("SUN_ATTN_TILE_READY"); return e ? atoi(e) : 0; }();
   return v;
 }
 
@@ -1097,6 +1115,7 @@ SunStatus run_attention(const SunDecoderDims& d, const CUtensorMap& tm_kv, AttnA
     aa.group_start = g_groups.start;
     aa.group_len = g_groups.len;
     aa.fused_combine = 0;
+    aa.qkv_ready = nullptr;
     dim3 ggrid(aa.max_splits, d.n_kv_heads, g_groups.n);
     if (d.head_dim == 128) SUN_CUDA(launch(attn_group_kernel<128>, ggrid, dim3(128), AttnCfg<128>::kSmem, st, pdl, tm_kv, aa));
     else SUN_CUDA(launch(attn_group_kernel<64>, ggrid, dim3(128), AttnCfg<64>::kSmem, st, pdl, tm_kv, aa));
@@ -1183,6 +1202,7 @@ SunStatus sun_decoder_create(const SunDecoderDims* dims, const SunWeights* weigh
   dec->err = reinterpret_cast<unsigned*>(ws + dec->L.err);
   dec->gv_part = reinterpret_cast<float*>(ws + dec->L.gv_part);
   dec->gv_cnt = reinterpret_cast<unsigned*>(ws + dec->L.gv_cnt);
+  dec->qkv_ready = reinterpret_cast<unsigned*>(ws + dec->L.qkv_ready);
 
   const SunDecoderDims& d = *dims;
   const int qd = d.n_q_heads * d.head_dim;
@@ -1200,6 +1220,7 @@ SunStatus sun_decoder_create(const SunDecoderDims* dims, const SunWeights* weigh
   if (e == cudaSuccess) e = cudaMemset(ws + dec->L.chain_bar, 0, 64 + size_t(kChainMaxPhases) * kChainReadyTiles * 4);
   if (e == cudaSuccess) e = cudaMemset(ws + dec->L.err, 0, 64);
   if (e == cudaSuccess) e = cudaMemset(ws + dec->L.gv_cnt, 0, kGvMaxTiles * 4);
+  if (e == cudaSuccess) e = cudaMemset(ws + dec->L.qkv_ready, 0, size_t(d.n_layers) * kQkvReadyStride * 4);
   if (e != cudaSuccess) {
     delete dec;
     return fail(SUN_ERR_CUDA, "cudaMemset ws: %s", cudaGetErrorString(e));
@@ -1339,6 +1360,8 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     if (next_p) gv_set_prefetch(g, next_pk, *next_p, dec->num_sms);
     return run_gemv_w4<E>(pk, sc, g, p, dec->gv_part, dec->gv_cnt, st, pdl, dec->num_sms);
   };
+  const bool tile_ho = attn_tile_ready() && chain && !w4 && !gemv && aa.prestage;
+  int qkv_writers = 0;  // writers per QKV tile of the chain that precedes the next attention
   using QkvT = std::integral_constant<int, EPI_QKV_ROPE>;
   using ResT = std::integral_constant<int, EPI_RESID_ADD>;
   using SwiT = std::integral_constant<int, EPI_SWIGLU>;
@@ -1354,6 +1377,8 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
     }
     // paged attention
     aa.layer = l;
+    aa.qkv_ready = (chain && tile_ho && l > 0 && qkv_writers > 0) ? dec->qkv_ready + size_t(l) * kQkvReadyStride : nullptr;
+    aa.ready_writers = static_cast<unsigned>(qkv_writers);
     if (!(skip & 2) && (s = run_attention(d, dec->tm_kv, aa, batch, st, pdl)) != SUN_OK) return s;
     if (chain) {  // O -> gate_up -> down (-> next layer's QKV) in one persistent launch
       GemmArgs ph[4] = {o_args(l), gu_args(l), down_args(l), GemmArgs{}};
@@ -1371,7 +1396,9 @@ SunStatus sun_decode_step(SunDecoder* dec, const int32_t* tokens, const int32_t*
       s = gemv ? run_gemv_chain_w4(ph, plans, wb, sc, nph, dec->gv_part, dec->gv_cnt, dec->chain_bar, st, pdl,
                                    dec->num_sms)
           : w4 ? run_chain_w4(ph, epi, plans, wb, sc, nph, dec->chain_bar, st, pdl, dec->num_sms)
-               : run_chain(ph, epi, plans, wb, nph, dec->chain_bar, st, pdl, dec->num_sms);
+               : run_chain(ph, epi, plans, wb, nph, dec->chain_bar, st, pdl, dec->num_sms,
+                           tile_ho && nph == 4 ? dec->qkv_ready + size_t(l + 1) * kQkvReadyStride : nullptr,
+                           tile_ho && l > 0 ? dec->qkv_ready + size_t(l) * kQkvReadyStride : nullptr, &qkv_writers);
       if (s != SUN_OK) return s;
       continue;
     }
