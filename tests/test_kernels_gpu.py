@@ -59,7 +59,7 @@ def test_gemm_deterministic_stream_k(cuda):
 
 
 @pytest.mark.parametrize("sched", ["0", "2", "vcl2", "novcl", "push", "nochain", "l2chain", "nogemv", "gvchain",
-                                   "tileready", "gvcluster", "gvbal0", "gvbal2"])
+                                   "tileready", "gvcluster", "gvbal0", "gvbal2", "attntile"])
 def test_gemm_schedules_subprocess(sched):
     """The GEMM kernel tests and the end-to-end decode parity under the other
     schedules: 0 = cluster split-K / whole tiles only, 2 = stream-K on every
@@ -75,7 +75,8 @@ def test_gemm_schedules_subprocess(sched):
     loads waiting for the producing tiles instead of the whole previous phase (opt-in), gvcluster =
     the W4 GEMV's split tiles reduced over DSMEM in hardware clusters instead of through L2,
     gvbal0 / gvbal2 = the W4 GEMV without its balanced schedule (whole tiles + remainder
-    spread contiguously) / with it also in place of the per-tile split."""
+    spread contiguously) / with it also in place of the per-tile split, attntile = the decode
+    attention starting on its QKV tiles as the previous layer chain publishes them (opt-in)."""
     import os
     import subprocess
     import sys
@@ -100,6 +101,8 @@ def test_gemm_schedules_subprocess(sched):
         env["SUN_CHAIN_TILE_READY"] = "1"
     elif sched == "gvcluster":
         env["SUN_GV_CLUSTER"] = "1"
+    elif sched == "attntile":
+        env["SUN_ATTN_TILE_READY"] = "1"
     elif sched in ("gvbal0", "gvbal2"):
         env["SUN_GV_BALANCE"] = sched[-1]
     else:
