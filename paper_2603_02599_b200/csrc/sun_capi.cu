@@ -794,7 +794,10 @@ SunStatus run_gemv_w4(const void* packed, const void* scales, GemmArgs a, const 
     a.splits = 0;
     grid = slots;
   } else {
+    // SUN_GV_SPLIT_CAP: largest split-K factor per tile (default: as many as the SMs allow)
+    static const int cap_env = [] { const char* e = getenv("SUN_GV_SPLIT_CAP"); return e ? atoi(e) : 0; }();
     a.splits = std::max(1, std::min(p.ksteps, slots / p.m_tiles));
+    if (cap_env > 0) a.splits = std::min(a.splits, cap_env);
     grid = p.m_tiles * a.splits;
     if (cl_env && a.splits > 1 && a.splits <= 8 && max_active_clusters_gv(unsigned(a.splits), c.smem) >= p.m_tiles) {
       a.vcluster = 0;
