@@ -1,0 +1,13 @@
+#!/bin/bash
+# W4 GEMV variant build (-DSUN_GV_CX_CHAIN): tests through the variant, then same-box A/B.
+export SUN_LIB=$PWD/paper_2603_02599_b200/libsun_b200_cxchain.so
+timeout 600 python -m pytest -q -x -m gpu tests/test_kernels_gpu.py -k "gemv and not subprocess" 2>&1 | tail -1
+timeout 600 python -m pytest -q -x -s -m gpu tests/test_parity_baseline_gpu.py -k c4s 2>&1 | grep -a "c4s:\|passed\|failed" | tail -2
+unset SUN_LIB
+for rep in 1 2; do for lib in default cxchain; do
+  if [ $lib = default ]; then unset SUN_LIB; else export SUN_LIB=$PWD/paper_2603_02599_b200/libsun_b200_$lib.so; fi
+  timeout 300 python scripts/measure_step_grid.py --spec llama3.1-8b --bits 4 --batches 1,8 --contexts 256,2048 --out gpurun_out/grid_cx.json > gpurun_out/grid_cx.log 2>&1
+  echo "$lib rep=$rep $(grep "ms$" gpurun_out/grid_cx.log | sed 's/ctx=//;s/B=//' | tr -s ' ' | tr "\n" ";")"
+done; done
+unset SUN_LIB
+for lib in "" _cxchain; do SUN_LIB=$PWD/paper_2603_02599_b200/libsun_b200$lib.so timeout 120 python scripts/gv_timeline.py 2>&1 | grep "B= 1" | cut -c1-170; done
