@@ -65,6 +65,7 @@ struct GemmArgs {
   int vcluster;      // 1: the S CTAs of a tile are not a hardware cluster: partials and the
                      // rank-sliced reduction go through L2 (sk_part) with a per-tile counter
   int stages;        // smem pipeline depth (W4: weight stages of wgroup K blocks)
+  int gv_first_wait; // W4 GEMV (epilogue-group kernel): the rest of the ring after the first stage landed
   int xstages;       // W4: activation stages of xk K blocks
   int wgroup;        // W4: K blocks per weight stage (packed [wgroup][8 KB] | scales [wgroup][256 B])
   int xk;            // W4: K blocks per activation stage

@@ -968,7 +968,7 @@ __global__ void __launch_bounds__(kGvaThreads, 1) gemv_w4a_kernel(const GemmArgs
   if (warp == kGvaProducerWarp) {
     if (elect_one()) {
       int slot = 0, phase = 0;
-      gv_produce(a, u0, u1, m, stages, slot, phase, [] { pdl_wait(); }, kGvMaxStages, /*first_wait=*/true);
+      gv_produce(a, u0, u1, m, stages, slot, phase, [] { pdl_wait(); }, kGvMaxStages, /*first_wait=*/a.gv_first_wait != 0);
       if (v0 < v1) gv_produce(a, v0, v1, m, stages, slot, phase, [] {}, 0);
       prefetch_next_weights(a);
     }

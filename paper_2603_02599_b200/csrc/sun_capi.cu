@@ -766,6 +766,11 @@ SunStatus run_gemv_w4(const void* packed, const void* scales, GemmArgs a, const 
   a.w4_scales = static_cast<const __nv_bfloat16*>(scales);
   a.wgroup = c.kbs;
   a.stages = c.stages;
+  // SUN_GV_FIRST_WAIT (default 0): the epilogue-group GEMV issues its whole 2-stage ring at
+  // once; 1 holds the second stage until the first has landed (helped the 4-stage ring of
+  // gemv_w4_kernel; here B=1 2.333 vs 2.347 ms same box, profiles/r02/gv_first_wait_ab.txt)
+  static const int fw_env = [] { const char* e = getenv("SUN_GV_FIRST_WAIT"); return e ? atoi(e) : 0; }();
+  a.gv_first_wait = fw_env;
   a.sk_units = 0;
   a.sk_part = part;
   a.sk_flags = cnt;
