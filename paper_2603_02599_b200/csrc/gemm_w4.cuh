@@ -879,8 +879,9 @@ SUN_DEVICE void gva_math(const GemmArgs& a, int u0, int u1, int v0, int v1, cons
   });
 }
 
-template <int EPI>
+template <int EPI, int NB>
 SUN_DEVICE void gva_epilogue(const GemmArgs& a, int u0, int u1, int v0, int v1, const GvSmem& m) {
+  constexpr int NCOL = 8 * NB;  // columns that can be non-zero (NB = 1: batch <= 8)
   const int KB = a.ksteps, G = static_cast<int>(gridDim.x), c = static_cast<int>(blockIdx.x);
   const int row_local = (static_cast<int>(threadIdx.x >> 5) - 2) * 32 + (threadIdx.x & 31);
   pdl_wait();
@@ -900,7 +901,7 @@ SUN_DEVICE void gva_epilogue(const GemmArgs& a, int u0, int u1, int v0, int v1, 
       // contributor adds the slots in contributor order (deterministic) and runs the epilogue
       float* dst = a.sk_part + static_cast<long long>(gv_part_slot(a, G, c, tile)) * (kTileM * 16) + row_local * 16;
 #pragma unroll
-      for (int j = 0; j < 16; j += 4) __stcg(reinterpret_cast<float4*>(dst + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+      for (int j = 0; j < NCOL; j += 4) __stcg(reinterpret_cast<float4*>(dst + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
       __threadfence();
       epi_bar();
       int cf, cl;
@@ -914,20 +915,22 @@ SUN_DEVICE void gva_epilogue(const GemmArgs& a, int u0, int u1, int v0, int v1, 
       __threadfence();
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = 0.f;
-      for (int c0 = cf; c0 <= cl; c0 += 2) {  // two partials' loads in flight per round trip
-        float4 pp[2][4];
+      // NB = 1: four partials' 8 columns in flight per round trip; NB = 2: two partials' 16
+      constexpr int PF = NB == 1 ? 4 : 2;
+      for (int c0 = cf; c0 <= cl; c0 += PF) {
+        float4 pp[PF][NCOL / 4];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
+        for (int e = 0; e < PF; ++e) {
           const int slot_e = gv_part_slot(a, G, c0 + e <= cl ? c0 + e : cl, tile);
           const float* src = a.sk_part + static_cast<long long>(slot_e) * (kTileM * 16) + row_local * 16;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) pp[e][q] = __ldcg(reinterpret_cast<const float4*>(src + 4 * q));
+          for (int q = 0; q < NCOL / 4; ++q) pp[e][q] = __ldcg(reinterpret_cast<const float4*>(src + 4 * q));
         }
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
+        for (int e = 0; e < PF; ++e) {
           if (c0 + e > cl) break;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < NCOL / 4; ++q) {
             v[4 * q] += pp[e][q].x; v[4 * q + 1] += pp[e][q].y; v[4 * q + 2] += pp[e][q].z; v[4 * q + 3] += pp[e][q].w;
           }
         }
@@ -974,7 +977,7 @@ __global__ void __launch_bounds__(kGvaThreads, 1) gemv_w4a_kernel(const GemmArgs
     }
     __syncwarp();
   } else if (warp >= 2 && warp < 6) {
-    gva_epilogue<EPI>(a, u0, u1, v0, v1, m);
+    gva_epilogue<EPI, NB>(a, u0, u1, v0, v1, m);
   } else {
     gva_math<NB>(a, u0, u1, v0, v1, m, stages);
   }
