@@ -890,6 +890,17 @@ SUN_DEVICE void gva_epilogue(const GemmArgs& a, int u0, int u1, int v0, int v1, 
   gv_for_segments(KB, u0, u1, v0, v1, [&](int, int, int, bool) { ++nseg; });
   int i = 0;
   gv_for_segments(KB, u0, u1, v0, v1, [&](int tile, int, int, bool whole) {
+    // residual epilogues: this row's old residual and next-norm gain are loaded before the
+    // segment's hand-off, off the tail's critical path (one round trip fewer after the reduction)
+    float pres[16], pg = 0.f;
+    if constexpr (EPI == EPI_RESID_ADD) {
+      const int row = tile * kTileM + row_local;
+      const bool in = row < a.n_out;
+      const float* base = a.out_f32 + row;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) pres[j] = (in && j < NCOL && j < a.batch) ? base[static_cast<long long>(j) * a.ldo] : 0.f;
+      if (a.norm_w != nullptr) pg = in ? __bfloat162float(a.norm_w[row]) : 0.f;
+    }
     gva_bar_sync(kGvaFull);
     float v[16];
 #pragma unroll
@@ -937,7 +948,8 @@ SUN_DEVICE void gva_epilogue(const GemmArgs& a, int u0, int u1, int v0, int v1, 
       }
       if (epi_lead_thread()) a.sk_flags[tile] = 0u;  // self-resetting for the next use
     }
-    epi_chunk<EPI>(a, tile, row_local, 0, v, m.epi);
+    if constexpr (EPI == EPI_RESID_ADD) epi_chunk<EPI>(a, tile, row_local, 0, v, m.epi, pres, &pg, 1);
+    else epi_chunk<EPI>(a, tile, row_local, 0, v, m.epi);
   });
 }
 
