@@ -901,6 +901,20 @@ SUN_DEVICE void gva_epilogue(const GemmArgs& a, int u0, int u1, int v0, int v1, 
       for (int j = 0; j < 16; ++j) pres[j] = (in && j < NCOL && j < a.batch) ? base[static_cast<long long>(j) * a.ldo] : 0.f;
       if (a.norm_w != nullptr) pg = in ? __bfloat162float(a.norm_w[row]) : 0.f;
     }
+    float pcs[16], psn[16];  // QKV epilogue: this row's RoPE factors per batch row
+    if constexpr (EPI == EPI_QKV_ROPE) {
+      const int row = tile * kTileM + row_local;
+      const int d = a.head_dim, half = d >> 1, i = row & (d - 1), fi = i < half ? i : i - half;
+      const bool is_v = row >= (a.n_q_heads + a.n_kv_heads) * d;
+      const int* meta = epi_meta(m.epi);  // positions (load_qkv_meta)
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const bool ok = !is_v && j < NCOL && j < a.batch && row < a.n_out;
+        const long long t = static_cast<long long>(meta[j]) * half + fi;
+        pcs[j] = ok ? a.rope_cos[t] : 1.f;
+        psn[j] = ok ? a.rope_sin[t] : 0.f;
+      }
+    }
     gva_bar_sync(kGvaFull);
     float v[16];
 #pragma unroll
@@ -949,6 +963,7 @@ SUN_DEVICE void gva_epilogue(const GemmArgs& a, int u0, int u1, int v0, int v1, 
       if (epi_lead_thread()) a.sk_flags[tile] = 0u;  // self-resetting for the next use
     }
     if constexpr (EPI == EPI_RESID_ADD) epi_chunk<EPI>(a, tile, row_local, 0, v, m.epi, pres, &pg, 1);
+    else if constexpr (EPI == EPI_QKV_ROPE) epi_chunk<EPI>(a, tile, row_local, 0, v, m.epi, pcs, psn, 1);
     else epi_chunk<EPI>(a, tile, row_local, 0, v, m.epi);
   });
 }
