@@ -767,6 +767,7 @@ __global__ void __launch_bounds__(kGvThreads, 1) gemv_w4_kernel(const GemmArgs a
 // ---------------------------------------------------------------------------
 constexpr int kGvaThreads = 21 * 32;
 constexpr int kGvaProducerWarp = 20;
+constexpr size_t kGvaExtraSmem = size_t(3) * kTileM * kGvTPitch * 4;  // reduction slices of chunks 1..3
 SUN_DEVICE void gva_bar_sync(int id) { asm volatile("bar.sync %0, 640;" ::"r"(id) : "memory"); }
 SUN_DEVICE void gva_bar_arrive(int id) { asm volatile("bar.arrive %0, 640;" ::"r"(id) : "memory"); }
 constexpr int kGvaFull = 4, kGvaEmpty = 5;  // named barriers: T holds a segment / T was read
@@ -787,7 +788,7 @@ SUN_DEVICE void gv_for_segments(int KB, int u0, int u1, int v0, int v1, F f) {
 }
 
 template <int NB>
-SUN_DEVICE void gva_math(const GemmArgs& a, int u0, int u1, int v0, int v1, const GvSmem& m, int stages) {
+SUN_DEVICE void gva_math(const GemmArgs& a, int u0, int u1, int v0, int v1, const GvSmem& m, int stages, float* Tx) {
   const int kbs = a.wgroup, bn = a.bn, KB = a.ksteps;
   const uint32_t sb = gv_stage_bytes(bn, kbs);
   const int warp = static_cast<int>(threadIdx.x >> 5), lane = threadIdx.x & 31;
@@ -848,29 +849,19 @@ SUN_DEVICE void gva_math(const GemmArgs& a, int u0, int u1, int v0, int v1, cons
     }
     if (threadIdx.x == 0 && s1 == (v1 > v0 ? v1 : u1)) SUN_STAMP(3);  // last stage consumed
     if (i > 0) gva_bar_sync(kGvaEmpty);  // the epilogue warps hold the previous segment's rows
-    // fragments -> T[row][batch] (as gv_consume: chunk 0 stores, chunks 1..3 add in order)
-    for (int cc = 0; cc < 4; ++cc) {
-      if (ch == cc) {
+    // fragments -> slice ch of T (chunk 0: T, chunks 1..3: Tx): one store round, no barrier
+    // among the compute warps; the epilogue group adds the slices in chunk order (the sum
+    // ((c0 + c1) + c2) + c3 of gv_consume, bit for bit)
+    float* Tq = ch == 0 ? T : Tx + (ch - 1) * (kTileM * kGvTPitch);
 #pragma unroll
-        for (int mt = 0; mt < kGvMT; ++mt) {
-          const int r = 32 * rq + 16 * mt + g;
+    for (int mt = 0; mt < kGvMT; ++mt) {
+      const int r = 32 * rq + 16 * mt + g;
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int jj = j < NB ? j : 0;
-            const bool have = j < NB;
-            float* p0 = T + r * kGvTPitch + 8 * j + t;
-            float* p1 = T + (r + 8) * kGvTPitch + 8 * j + t;
-            const float w0 = have ? acc[mt][jj][0] : 0.f, w1 = have ? acc[mt][jj][1] : 0.f;
-            const float w2 = have ? acc[mt][jj][2] : 0.f, w3 = have ? acc[mt][jj][3] : 0.f;
-            if (cc == 0) {
-              p0[0] = w0; p0[4] = w1; p1[0] = w2; p1[4] = w3;
-            } else {
-              p0[0] += w0; p0[4] += w1; p1[0] += w2; p1[4] += w3;
-            }
-          }
-        }
+      for (int j = 0; j < NB; ++j) {
+        float* p0 = Tq + r * kGvTPitch + 8 * j + t;
+        float* p1 = Tq + (r + 8) * kGvTPitch + 8 * j + t;
+        p0[0] = acc[mt][j][0]; p0[4] = acc[mt][j][1]; p1[0] = acc[mt][j][2]; p1[4] = acc[mt][j][3];
       }
-      gv_bar();
     }
     gva_bar_arrive(kGvaFull);
     ++i;
@@ -880,7 +871,7 @@ SUN_DEVICE void gva_math(const GemmArgs& a, int u0, int u1, int v0, int v1, cons
 }
 
 template <int EPI, int NB>
-SUN_DEVICE void gva_epilogue(const GemmArgs& a, int u0, int u1, int v0, int v1, const GvSmem& m) {
+SUN_DEVICE void gva_epilogue(const GemmArgs& a, int u0, int u1, int v0, int v1, const GvSmem& m, const float* Tx) {
   constexpr int NCOL = 8 * NB;  // columns that can be non-zero (NB = 1: batch <= 8)
   const int KB = a.ksteps, G = static_cast<int>(gridDim.x), c = static_cast<int>(blockIdx.x);
   const int row_local = (static_cast<int>(threadIdx.x >> 5) - 2) * 32 + (threadIdx.x & 31);
@@ -918,7 +909,10 @@ SUN_DEVICE void gva_epilogue(const GemmArgs& a, int u0, int u1, int v0, int v1, 
     gva_bar_sync(kGvaFull);
     float v[16];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = m.T[row_local * kGvTPitch + j];
+    for (int j = 0; j < 16; ++j) {
+      const int o = row_local * kGvTPitch + j;
+      v[j] = j < NCOL ? ((m.T[o] + Tx[o]) + Tx[kTileM * kGvTPitch + o]) + Tx[2 * kTileM * kGvTPitch + o] : 0.f;
+    }
     if (i + 1 < nseg) gva_bar_arrive(kGvaEmpty);
     ++i;
     if (!whole) {
@@ -975,6 +969,8 @@ __global__ void __launch_bounds__(kGvaThreads, 1) gemv_w4a_kernel(const GemmArgs
   tl_begin(a.tl, a.tl_idx);
   const int stages = a.stages;
   const GvSmem m = gv_smem(smem, stages, gv_stage_bytes(a.bn, a.wgroup));
+  // chunk slices 1..3 of the reduction tile, after the common layout (kGvaExtraSmem)
+  float* Tx = reinterpret_cast<float*>(smem + gv_smem_bytes(a.bn, a.wgroup, stages) - 1024);
   const int warp = warp_id_sync();
   int u0, u1, v0, v1;
   gv_range(a, static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), u0, u1);
@@ -1004,9 +1000,9 @@ __global__ void __launch_bounds__(kGvaThreads, 1) gemv_w4a_kernel(const GemmArgs
     }
     __syncwarp();
   } else if (warp >= 2 && warp < 6) {
-    gva_epilogue<EPI, NB>(a, u0, u1, v0, v1, m);
+    gva_epilogue<EPI, NB>(a, u0, u1, v0, v1, m, Tx);
   } else {
-    gva_math<NB>(a, u0, u1, v0, v1, m, stages);
+    gva_math<NB>(a, u0, u1, v0, v1, m, stages, Tx);
   }
   if (threadIdx.x == 64) SUN_STAMP(5);  // (epilogue warp) last epilogue done
   if (a.tl != nullptr || a.stamps != nullptr) __syncthreads();  // profiling: the exit stamps after every role

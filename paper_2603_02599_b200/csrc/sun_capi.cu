@@ -810,8 +810,9 @@ SunStatus run_gemv_w4(const void* packed, const void* scales, GemmArgs a, const 
     }
   }
   if (async && a.vcluster) {
-    if (a.batch <= 8) SUN_CUDA(launch(gemv_w4a_kernel<EPI, 1>, dim3(grid), dim3(kGvaThreads), c.smem, st, pdl, a));
-    else SUN_CUDA(launch(gemv_w4a_kernel<EPI, 2>, dim3(grid), dim3(kGvaThreads), c.smem, st, pdl, a));
+    const size_t sm = c.smem + kGvaExtraSmem;
+    if (a.batch <= 8) SUN_CUDA(launch(gemv_w4a_kernel<EPI, 1>, dim3(grid), dim3(kGvaThreads), sm, st, pdl, a));
+    else SUN_CUDA(launch(gemv_w4a_kernel<EPI, 2>, dim3(grid), dim3(kGvaThreads), sm, st, pdl, a));
     return SUN_OK;
   }
   if (a.batch <= 8) SUN_CUDA(launch(gemv_w4_kernel<EPI, 1>, dim3(grid), dim3(kGvThreads), c.smem, st, pdl, a));
