@@ -683,9 +683,10 @@ GvCfg gv_cfg(int bn, bool async = false) {
   c.per_sm = env_ps > 0 ? env_ps : 1;
   const int budget = kSmemPerSm / c.per_sm - int(gv_smem_bytes(bn, c.kbs, 0)) - 1024;
   c.stages = std::max(2, std::min(kGvMaxStages, budget / int(gv_stage_bytes(bn, c.kbs))));
-  // gemv_w4a_kernel: a 2-stage ring (8 K blocks in flight) measured best (8B W4 B=1 ctx 256:
-  // 2 / 3 / 4 stages 2.33 / 2.34 / 2.39 ms, profiles/r02/gv_async_stages.txt)
-  if (async) c.stages = std::min(c.stages, 2);
+  // gemv_w4a_kernel: a 3-stage ring (12 K blocks in flight; 2 / 3 / 4 stages 2.33 / 2.34 /
+  // 2.39 ms before the tail changes, 3 vs 2 after them: B=1 2.130 vs 2.133, B=8 2.232 vs
+  // 2.246 ms same box — profiles/r02/gv_async_stages.txt)
+  if (async) c.stages = std::min(c.stages, 3);
   if (env_st > 0) c.stages = std::min(env_st, kGvMaxStages);
   c.smem = gv_smem_bytes(bn, c.kbs, c.stages);
   return c;
